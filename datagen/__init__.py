@@ -131,3 +131,73 @@ def c5_rows(r0: int, r1: int, size: int = 32768, seed: int = SEEDS["c5"],
 def uniform(shape, seed: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
     """Generic seeded fp32 uniform input for ragged / edge-case parity tests."""
     return np.random.default_rng(seed).uniform(lo, hi, shape).astype(np.float32)
+
+
+# --------------------------------------------------------------------------- parallel fill
+def _fill_worker(args):
+    from multiprocessing import shared_memory
+    name, shape, dtype, kind, lo, hi, kw = args
+    shm = shared_memory.SharedMemory(name=name)
+    try:
+        arr = np.ndarray(shape, dtype=dtype, buffer=shm.buf)
+        if kind == "c2":
+            for i in range(lo, hi):
+                arr[i] = c2_signal(kw["first"] + i, n=shape[-1])
+        elif kind == "c4":
+            for i in range(lo, hi):
+                arr[i] = c4_image(kw["first"] + i, size=shape[-1])
+        elif kind == "c5":
+            br = kw["band_rows"]
+            arr[lo * br:hi * br] = c5_rows(kw["r0"] + lo * br, kw["r0"] + hi * br, size=kw["size"], band_rows=br)
+        else:
+            raise ValueError(kind)
+    finally:
+        shm.close()
+    return hi - lo
+
+
+def generate(kind: str, *, first: int = 0, count: int | None = None, size: int | None = None,
+             r0: int = 0, r1: int | None = None, workers: int | None = None, out: np.ndarray | None = None):
+    """Fill a (possibly pinned, caller-provided) fp32 array with config `kind` units in parallel
+    across host cores.  c2: signals [first, first+count); c4: images [first, first+count);
+    c5: rows [r0, r1) of the size x size image.  Bit-identical to the per-unit generators."""
+    import os
+    from concurrent.futures import ProcessPoolExecutor
+    from multiprocessing import shared_memory
+    cfg = CONFIGS[kind]
+    if kind == "c2":
+        n = size or cfg["n"]
+        count = cfg["batch"] if count is None else count
+        shape, units, kw = (count, n), count, {"first": first}
+    elif kind == "c4":
+        s = size or cfg["h"]
+        count = cfg["batch"] if count is None else count
+        shape, units, kw = (count, s, s), count, {"first": first}
+    elif kind == "c5":
+        s = size or cfg["h"]
+        r1 = s if r1 is None else r1
+        shape, units = (r1 - r0, s), (r1 - r0) // C5_BAND_ROWS
+        kw = {"r0": r0, "size": s, "band_rows": C5_BAND_ROWS}
+    else:
+        raise ValueError(kind)
+    workers = workers or min(32, len(os.sched_getaffinity(0)))
+    nbytes = int(np.prod(shape)) * 4
+    shm = shared_memory.SharedMemory(create=True, size=max(nbytes, 1))
+    try:
+        step = max(1, -(-units // (workers * 4)))
+        tasks = [(shm.name, shape, np.float32, kind, lo, min(units, lo + step), kw) for lo in range(0, units, step)]
+        if workers <= 1 or len(tasks) <= 1:
+            for t in tasks:
+                _fill_worker(t)
+        else:
+            with ProcessPoolExecutor(workers) as ex:
+                list(ex.map(_fill_worker, tasks))
+        src = np.ndarray(shape, dtype=np.float32, buffer=shm.buf)
+        if out is None:
+            out = np.empty(shape, dtype=np.float32)
+        np.copyto(out.reshape(shape), src)
+        del src
+    finally:
+        shm.close()
+        shm.unlink()
+    return out

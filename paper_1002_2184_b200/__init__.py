@@ -1,0 +1,382 @@
+"""B200-native Fast Haar Wavelet Transform (arXiv 1002.2184) — thin Python binding.
+
+Every function here only marshals arguments (tensor -> device pointer, current CUDA stream ->
+cudaStream_t, status -> exception) and calls the C ABI of ``libfhwt.so`` (include/fhwt.h),
+whose sm_100a kernels do all of the arithmetic.  There is no CPU or PyTorch fallback: inputs
+must be contiguous float32 CUDA tensors, and a missing library raises ``FhwtLibraryError``.
+
+Names follow the C ABI: analyze_1d / synthesize_1d / analyze_2d / synthesize_2d, Plan1d / Plan2d
+(plan handles), pack_ll_2d, roundtrip_2d_host / roundtrip_1d_host, band_offset_1d/2d.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "FhwtError", "FhwtLibraryError", "OddLength", "EmptySignal", "InvalidLevels", "InsufficientLength",
+    "ShapeMismatch", "UnsupportedFilter", "Misaligned", "CudaError", "NoDevice", "InvalidArgument",
+    "lib", "lib_path", "haar_filter_bank", "launch_count", "version",
+    "analyze_1d", "synthesize_1d", "analyze_2d", "synthesize_2d", "Plan1d", "Plan2d",
+    "pack_ll_2d", "roundtrip_2d_host", "roundtrip_1d_host", "band_offset_1d", "band_offset_2d",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libfhwt.so")
+
+
+class FhwtError(RuntimeError):
+    status = -1
+
+
+class FhwtLibraryError(FhwtError):
+    pass
+
+
+class InvalidArgument(FhwtError, ValueError):
+    status = 1
+
+
+class EmptySignal(FhwtError, ValueError):
+    status = 2
+
+
+class OddLength(FhwtError, ValueError):
+    status = 3
+
+
+class InvalidLevels(FhwtError, ValueError):
+    status = 4
+
+
+class InsufficientLength(FhwtError, ValueError):
+    status = 5
+
+
+class ShapeMismatch(FhwtError, ValueError):
+    status = 6
+
+
+LengthMismatch = DimensionMismatch = ShapeMismatch
+
+
+class UnsupportedFilter(FhwtError, ValueError):
+    status = 7
+
+
+class Misaligned(FhwtError, ValueError):
+    status = 8
+
+
+class CudaError(FhwtError):
+    status = 9
+
+
+class NoDevice(FhwtError):
+    status = 10
+
+
+_BY_STATUS = {c.status: c for c in (InvalidArgument, EmptySignal, OddLength, InvalidLevels, InsufficientLength,
+                                      ShapeMismatch, UnsupportedFilter, Misaligned, CudaError, NoDevice)}
+
+
+class FilterBank(ctypes.Structure):
+    """fhwt_filter_bank: the paper's problem statement (b0, b1, a0, a1, M) — PAPER.md:54, :88."""
+    _fields_ = [("b0", ctypes.c_double * 2), ("b1", ctypes.c_double * 2), ("a0", ctypes.c_double * 2),
+                ("a1", ctypes.c_double * 2), ("M", ctypes.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """Load (building in-tree first if the sources are newer) libfhwt.so."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    try:
+        from . import _build
+        if _build.stale():
+            _build.build()
+    except Exception as e:  # noqa: BLE001 - surface as a library error below if the .so is unusable
+        if not os.path.exists(lib_path):
+            raise FhwtLibraryError(f"libfhwt.so is missing and could not be built: {e}") from e
+    if not os.path.exists(lib_path):
+        raise FhwtLibraryError(f"{lib_path} not found; run `python -m paper_1002_2184_b200._build`")
+    L = ctypes.CDLL(lib_path)
+    i64, c_int, vp, st = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_int
+    sig = {
+        "fhwt_haar_filter_bank": (st, [ctypes.POINTER(FilterBank)]),
+        "fhwt_status_string": (ctypes.c_char_p, [st]),
+        "fhwt_last_error_message": (ctypes.c_char_p, []),
+        "fhwt_version": (c_int, []),
+        "fhwt_launch_count": (ctypes.c_uint64, []),
+        "fhwt_plan_1d": (st, [ctypes.POINTER(vp), i64, i64, c_int, ctypes.POINTER(FilterBank)]),
+        "fhwt_plan_2d": (st, [ctypes.POINTER(vp), i64, i64, i64, c_int, ctypes.POINTER(FilterBank)]),
+        "fhwt_plan_destroy": (st, [vp]),
+        "fhwt_plan_workspace_bytes": (ctypes.c_size_t, [vp]),
+        "fhwt_plan_analyze": (st, [vp, vp, vp, vp, vp]),
+        "fhwt_plan_synthesize": (st, [vp, vp, vp, vp, vp]),
+        "fhwt_analyze_1d": (st, [vp, vp, i64, i64, c_int, vp]),
+        "fhwt_synthesize_1d": (st, [vp, vp, i64, i64, c_int, vp]),
+        "fhwt_analyze_2d": (st, [vp, vp, i64, i64, i64, c_int, vp]),
+        "fhwt_synthesize_2d": (st, [vp, vp, i64, i64, i64, c_int, vp]),
+        "fhwt_band_offset_1d": (i64, [i64, c_int, c_int, ctypes.POINTER(i64)]),
+        "fhwt_band_offset_2d": (i64, [i64, i64, c_int, c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "fhwt_pack_ll_2d": (st, [vp, vp, i64, i64, i64, c_int, vp]),
+        "fhwt_roundtrip_2d_host": (st, [vp, vp, vp, i64, i64, i64, c_int, i64]),
+        "fhwt_roundtrip_1d_host": (st, [vp, vp, vp, i64, i64, c_int, i64]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status == 0:
+        return
+    L = lib()
+    msg = L.fhwt_last_error_message().decode(errors="replace")
+    name = L.fhwt_status_string(status).decode()
+    raise _BY_STATUS.get(status, FhwtError)(f"{name}: {msg}")
+
+
+def version() -> int:
+    return lib().fhwt_version()
+
+
+def launch_count() -> int:
+    """Number of kernels libfhwt.so has launched in this process."""
+    return int(lib().fhwt_launch_count())
+
+
+def haar_filter_bank() -> FilterBank:
+    fb = FilterBank()
+    _check(lib().fhwt_haar_filter_bank(ctypes.byref(fb)))
+    return fb
+
+
+# ------------------------------------------------------------------ tensor marshalling
+def _stream(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev_f32(t, what):
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{what} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise InvalidArgument(f"{what} must be a CUDA tensor (this library has no CPU path)")
+    if t.dtype != torch.float32:
+        raise InvalidArgument(f"{what} must be float32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise InvalidArgument(f"{what} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _out_like(x, out):
+    import torch
+    if out is None:
+        return torch.empty_like(x)
+    if out.shape != x.shape:
+        raise ShapeMismatch(f"out has shape {tuple(out.shape)}, expected {tuple(x.shape)}")
+    return out
+
+
+def _shape_1d(x):
+    if x.dim() < 1:
+        raise InvalidArgument("1-D transform needs at least one dimension")
+    n = x.shape[-1]
+    return n, (x.numel() // n if n else 0)
+
+
+def _shape_2d(x):
+    if x.dim() < 2:
+        raise InvalidArgument("2-D transform needs at least two dimensions")
+    h, w = x.shape[-2], x.shape[-1]
+    return h, w, (x.numel() // (h * w) if h * w else 0)
+
+
+def _guard_device(x):
+    import torch
+    _dev_f32(x, "input")          # validate (CUDA, float32, contiguous) before touching the device
+    return torch.cuda.device(x.device)
+
+
+def analyze_1d(d, levels: int, out=None, stream=None):
+    """fhwt_analyze_1d: multi-level Fast Haar analysis along the last axis -> Mallat layout."""
+    n, batch = _shape_1d(d)
+    out = _out_like(d, out)
+    with _guard_device(d):
+        _check(lib().fhwt_analyze_1d(_dev_f32(d, "d"), _dev_f32(out, "coeffs"), n, batch, int(levels), _stream(stream)))
+    return out
+
+
+def synthesize_1d(coeffs, levels: int, out=None, stream=None):
+    """fhwt_synthesize_1d: inverse of analyze_1d (perfect reconstruction)."""
+    n, batch = _shape_1d(coeffs)
+    out = _out_like(coeffs, out)
+    with _guard_device(coeffs):
+        _check(lib().fhwt_synthesize_1d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"), n, batch, int(levels),
+                                        _stream(stream)))
+    return out
+
+
+def analyze_2d(d, levels: int, out=None, stream=None):
+    """fhwt_analyze_2d: separable multi-level Fast Haar analysis of [..., h, w] -> Mallat quadrants."""
+    h, w, batch = _shape_2d(d)
+    out = _out_like(d, out)
+    with _guard_device(d):
+        _check(lib().fhwt_analyze_2d(_dev_f32(d, "d"), _dev_f32(out, "coeffs"), h, w, batch, int(levels),
+                                     _stream(stream)))
+    return out
+
+
+def synthesize_2d(coeffs, levels: int, out=None, stream=None):
+    """fhwt_synthesize_2d: inverse of analyze_2d."""
+    h, w, batch = _shape_2d(coeffs)
+    out = _out_like(coeffs, out)
+    with _guard_device(coeffs):
+        _check(lib().fhwt_synthesize_2d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"), h, w, batch, int(levels),
+                                        _stream(stream)))
+    return out
+
+
+class _Plan:
+    _kind = 0
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.fhwt_plan_destroy(h)
+            self._h = None
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(lib().fhwt_plan_workspace_bytes(self._h))
+
+    def _ws(self, like, workspace):
+        import torch
+        nb = self.workspace_bytes
+        if nb == 0:
+            return ctypes.c_void_p(0)
+        if workspace is None:
+            ws = getattr(self, "_ws_cache", None)
+            if ws is None or ws.device != like.device:
+                ws = torch.empty(nb, dtype=torch.uint8, device=like.device)
+                self._ws_cache = ws
+            workspace = ws
+        if workspace.numel() * workspace.element_size() < nb or not workspace.is_cuda:
+            raise InvalidArgument(f"workspace must be a CUDA buffer of >= {nb} bytes")
+        return ctypes.c_void_p(workspace.data_ptr())
+
+    def _check_shape(self, x):
+        if tuple(x.shape[-self._kind:]) != self._tail or x.numel() != self._numel:
+            raise ShapeMismatch(f"tensor shape {tuple(x.shape)} does not match the plan {self._tail} x {self.batch}")
+
+    def analyze(self, d, out=None, workspace=None, stream=None):
+        self._check_shape(d)
+        out = _out_like(d, out)
+        with _guard_device(d):
+            _check(lib().fhwt_plan_analyze(self._h, _dev_f32(d, "d"), _dev_f32(out, "coeffs"), self._ws(d, workspace),
+                                           _stream(stream)))
+        return out
+
+    def synthesize(self, coeffs, out=None, workspace=None, stream=None):
+        self._check_shape(coeffs)
+        out = _out_like(coeffs, out)
+        with _guard_device(coeffs):
+            _check(lib().fhwt_plan_synthesize(self._h, _dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"),
+                                              self._ws(coeffs, workspace), _stream(stream)))
+        return out
+
+
+class Plan1d(_Plan):
+    """fhwt_plan_1d handle: batch signals of n samples, `levels` levels, filter bank (default §II)."""
+    _kind = 1
+
+    def __init__(self, n: int, batch: int, levels: int, filter_bank: FilterBank | None = None):
+        h = ctypes.c_void_p()
+        _check(lib().fhwt_plan_1d(ctypes.byref(h), int(n), int(batch), int(levels),
+                                  ctypes.byref(filter_bank) if filter_bank is not None else None))
+        self._h = h
+        self.n, self.batch, self.levels = int(n), int(batch), int(levels)
+        self._tail = (self.n,)
+        self._numel = self.n * self.batch
+
+
+class Plan2d(_Plan):
+    """fhwt_plan_2d handle: batch images of h x w, `levels` separable levels."""
+    _kind = 2
+
+    def __init__(self, h: int, w: int, batch: int, levels: int, filter_bank: FilterBank | None = None):
+        hd = ctypes.c_void_p()
+        _check(lib().fhwt_plan_2d(ctypes.byref(hd), int(h), int(w), int(batch), int(levels),
+                                  ctypes.byref(filter_bank) if filter_bank is not None else None))
+        self._h = hd
+        self.h, self.w, self.batch, self.levels = int(h), int(w), int(batch), int(levels)
+        self._tail = (self.h, self.w)
+        self._numel = self.h * self.w * self.batch
+
+
+def pack_ll_2d(coeffs, levels: int, out=None, stream=None):
+    """fhwt_pack_ll_2d: contiguous copy of every image's coarsest LL band ([..., h>>L, w>>L])."""
+    import torch
+    h, w, batch = _shape_2d(coeffs)
+    shape = tuple(coeffs.shape[:-2]) + (h >> levels, w >> levels)
+    if out is None:
+        out = torch.empty(shape, dtype=coeffs.dtype, device=coeffs.device)
+    with _guard_device(coeffs):
+        _check(lib().fhwt_pack_ll_2d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "ll"), h, w, batch, int(levels),
+                                     _stream(stream)))
+    return out
+
+
+def _host_f32(t, what):
+    import torch
+    if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+        raise InvalidArgument(f"{what} must be a contiguous float32 host tensor (pinned recommended)")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def roundtrip_2d_host(d, levels: int, coeffs_out=None, out=None, chunk: int = 0):
+    """fhwt_roundtrip_2d_host: DWT + IDWT of HOST images, streamed through the current device."""
+    import torch
+    h, w, batch = _shape_2d(d)
+    if out is None:
+        out = torch.empty_like(d, pin_memory=d.is_pinned())
+    _check(lib().fhwt_roundtrip_2d_host(_host_f32(d, "d"), _host_f32(coeffs_out, "coeffs") if coeffs_out is not None else None,
+                                        _host_f32(out, "d_R"), h, w, batch, int(levels), int(chunk)))
+    return out
+
+
+def roundtrip_1d_host(d, levels: int, coeffs_out=None, out=None, chunk: int = 0):
+    import torch
+    n, batch = _shape_1d(d)
+    if out is None:
+        out = torch.empty_like(d, pin_memory=d.is_pinned())
+    _check(lib().fhwt_roundtrip_1d_host(_host_f32(d, "d"), _host_f32(coeffs_out, "coeffs") if coeffs_out is not None else None,
+                                        _host_f32(out, "d_R"), n, batch, int(levels), int(chunk)))
+    return out
+
+
+def band_offset_1d(n: int, level: int, band: int):
+    ln = ctypes.c_int64()
+    off = lib().fhwt_band_offset_1d(int(n), int(level), int(band), ctypes.byref(ln))
+    if off < 0:
+        raise InvalidArgument(f"bad band query n={n} level={level} band={band}")
+    return int(off), int(ln.value)
+
+
+def band_offset_2d(h: int, w: int, level: int, band: int):
+    r, c = ctypes.c_int64(), ctypes.c_int64()
+    off = lib().fhwt_band_offset_2d(int(h), int(w), int(level), int(band), ctypes.byref(r), ctypes.byref(c))
+    if off < 0:
+        raise InvalidArgument(f"bad band query {h}x{w} level={level} band={band}")
+    return int(off), int(r.value), int(c.value)
+

@@ -1,0 +1,704 @@
+// C ABI of the Fast Haar library (include/fhwt.h): validation, plans, kernel-pass scheduling,
+// TMA descriptor encoding, workspace, host-buffer streaming.  No torch types cross this boundary.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fhwt.h"
+#include "fhwt_internal.cuh"
+
+using namespace fhwt;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+fhwt_status fail(fhwt_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+fhwt_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(FHWT_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define FHWT_CUDA(call, what)                 \
+  do {                                        \
+    cudaError_t e_ = (call);                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+#define FHWT_TRY(call)                   \
+  do {                                   \
+    fhwt_status st_ = (call);            \
+    if (st_ != FHWT_OK) return st_;      \
+  } while (0)
+
+int64_t pitch4(int64_t x) { return (x + 3) & ~int64_t(3); }
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Pass {
+  int g0, Lp;
+};
+
+std::vector<Pass> make_passes(int levels, int per_pass) {
+  std::vector<Pass> v;
+  for (int g = 0; g < levels; g += per_pass) v.push_back({g, std::min(per_pass, levels - g)});
+  return v;
+}
+
+// ------------------------------------------------------------------ device info / TMA encode
+struct DevInfo {
+  int sms = 0;
+  int major = 0;
+  bool ok = false;
+};
+
+fhwt_status device_info(DevInfo* out) {
+  static std::mutex mu;
+  static DevInfo cache[64];
+  int dev = 0;
+  FHWT_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return fail(FHWT_ERR_NO_DEVICE, "device index %d", dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!cache[dev].ok) {
+    FHWT_CUDA(cudaDeviceGetAttribute(&cache[dev].sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+    FHWT_CUDA(cudaDeviceGetAttribute(&cache[dev].major, cudaDevAttrComputeCapabilityMajor, dev), "cc");
+    cache[dev].ok = true;
+  }
+  if (cache[dev].major != 10)
+    return fail(FHWT_ERR_NO_DEVICE, "device %d has compute capability %d.x; this library is built for sm_100a",
+                dev, cache[dev].major);
+  *out = cache[dev];
+  return FHWT_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D row-major tensor view: `cols` x `rows` elements, row pitch `pitch_elems`, box bw x bh.
+fhwt_status encode_2d(CUtensorMap* m, const void* base, bool f64, int64_t cols, int64_t rows, int64_t pitch_elems,
+                      int bw, int bh) {
+  auto fn = get_encode();
+  if (!fn) return fail(FHWT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  const size_t es = f64 ? 8 : 4;
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(pitch_elems) * es};
+  cuuint32_t box[2] = {cuuint32_t(bw), cuuint32_t(bh)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(FHWT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): dims %lld x %lld pitch %lld box %d x %d", int(r),
+                (long long)cols, (long long)rows, (long long)pitch_elems, bw, bh);
+  return FHWT_OK;
+}
+
+// occupancy cache: (kind, smem) -> blocks per SM
+fhwt_status occupancy(int kind, size_t smem, int* bps) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, size_t>, int>> cache;
+  int dev = 0;
+  FHWT_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  const int key = kind * 64 + dev;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : cache)
+      if (e.first.first == key && e.first.second == smem) {
+        *bps = e.second;
+        return FHWT_OK;
+      }
+  }
+  cudaError_t e = kind == 2 ? syn2d_occupancy(smem, bps) : ana2d_occupancy(kind == 1, smem, bps);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+  if (*bps < 1) return fail(FHWT_ERR_CUDA, "kernel does not fit on an SM with %zu B shared memory", smem);
+  std::lock_guard<std::mutex> lk(mu);
+  cache.push_back({{key, smem}, *bps});
+  return FHWT_OK;
+}
+
+// ------------------------------------------------------------------ validation
+fhwt_status check_bank(const fhwt_filter_bank* fb) {
+  if (!fb) return FHWT_OK;
+  const double s = 1.0 / std::sqrt(2.0);
+  const double ref[8] = {s, s, -s, s, s, s, s, -s};
+  const double got[8] = {fb->b0[0], fb->b0[1], fb->b1[0], fb->b1[1], fb->a0[0], fb->a0[1], fb->a1[0], fb->a1[1]};
+  for (int i = 0; i < 8; ++i)
+    if (!(std::fabs(got[i] - ref[i]) <= 1e-12))
+      return fail(FHWT_ERR_UNSUPPORTED_FILTER, "tap %d = %.17g differs from the section II Haar set", i, got[i]);
+  if (fb->M != 2) return fail(FHWT_ERR_UNSUPPORTED_FILTER, "decimation factor M = %d (Haar needs M = 2)", fb->M);
+  return FHWT_OK;
+}
+
+fhwt_status check_1d(int64_t n, int64_t batch, int levels) {
+  if (n < 0 || batch < 0) return fail(FHWT_ERR_INVALID_ARG, "negative size n=%lld batch=%lld", (long long)n, (long long)batch);
+  if (n == 0 || batch == 0) return fail(FHWT_ERR_EMPTY, "empty input n=%lld batch=%lld", (long long)n, (long long)batch);
+  if (levels < 1 || levels > 62) return fail(FHWT_ERR_INVALID_LEVELS, "levels=%d", levels);
+  if (n % 2) return fail(FHWT_ERR_ODD_LENGTH, "odd length n=%lld", (long long)n);
+  if (n % (int64_t(1) << levels)) return fail(FHWT_ERR_INSUFFICIENT_LENGTH, "n=%lld not divisible by 2^%d", (long long)n, levels);
+  return FHWT_OK;
+}
+
+fhwt_status check_2d(int64_t h, int64_t w, int64_t batch, int levels) {
+  if (h < 0 || w < 0 || batch < 0) return fail(FHWT_ERR_INVALID_ARG, "negative size");
+  if (h == 0 || w == 0 || batch == 0) return fail(FHWT_ERR_EMPTY, "empty input %lldx%lld batch %lld", (long long)h, (long long)w, (long long)batch);
+  if (levels < 1 || levels > 62) return fail(FHWT_ERR_INVALID_LEVELS, "levels=%d", levels);
+  if (h % 2 || w % 2) return fail(FHWT_ERR_ODD_LENGTH, "odd dimension %lldx%lld", (long long)h, (long long)w);
+  if (h % (int64_t(1) << levels) || w % (int64_t(1) << levels))
+    return fail(FHWT_ERR_INSUFFICIENT_LENGTH, "%lldx%lld not divisible by 2^%d", (long long)h, (long long)w, levels);
+  if (batch * h >= (int64_t(1) << 31) || w >= (int64_t(1) << 31))
+    return fail(FHWT_ERR_INVALID_ARG, "batch*h=%lld or w=%lld exceeds the 2^31 TMA coordinate range",
+                (long long)(batch * h), (long long)w);
+  return FHWT_OK;
+}
+
+fhwt_status check_ptrs(const void* in, const void* out, size_t bytes) {
+  if (!in || !out) return fail(FHWT_ERR_INVALID_ARG, "null buffer pointer");
+  const char* a = static_cast<const char*>(in);
+  const char* b = static_cast<const char*>(out);
+  if (a < b + bytes && b < a + bytes) return fail(FHWT_ERR_INVALID_ARG, "input and output buffers overlap (no in-place transform)");
+  if ((reinterpret_cast<uintptr_t>(in) & 3) || (reinterpret_cast<uintptr_t>(out) & 3))
+    return fail(FHWT_ERR_MISALIGNED, "buffers must be at least 4-byte aligned");
+  return FHWT_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+namespace fhwt {
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace fhwt
+
+// ---------------------------------------------------------------------- plan object
+struct fhwt_plan_s {
+  int kind;  // 1 or 2
+  int64_t n, h, w, batch;
+  int levels;
+  std::vector<Pass> passes;
+  std::vector<size_t> ws_off;  // per pass boundary k (after pass k, k < passes-1)
+  size_t ws_bytes;
+};
+
+namespace {
+
+void plan_layout(fhwt_plan_s* p) {
+  p->passes = make_passes(p->levels, p->kind == 2 ? kMaxLevels2dPass : kMaxLevels1dPass);
+  p->ws_off.clear();
+  size_t off = 0;
+  for (size_t k = 0; k + 1 < p->passes.size(); ++k) {
+    const int g = p->passes[k].g0 + p->passes[k].Lp;
+    size_t elems = p->kind == 2 ? size_t(p->batch) * size_t(p->h >> g) * size_t(pitch4(p->w >> g))
+                                : size_t(p->batch) * size_t(pitch4(p->n >> g));
+    p->ws_off.push_back(off);
+    off = align_up(off + elems * sizeof(double), 256);
+  }
+  p->ws_bytes = off;
+}
+
+int choose_tr(int64_t rows, int Lp) {
+  int tr = 32;
+  while (tr > 1 && rows % tr) tr >>= 1;
+  return std::max(tr, 1 << Lp);
+}
+
+// ------------------------------------------------------------------ 2-D execution
+fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char* ws, cudaStream_t s) {
+  const int64_t H = pl->h, W = pl->w, B = pl->batch;
+  if (W % 4 != 0 || !aligned16(d) || !aligned16(coeffs)) {
+    if (pl->levels != 1)
+      return fail(FHWT_ERR_MISALIGNED, "multi-level 2-D transform needs 16-byte aligned buffers and w %% 4 == 0");
+    FHWT_CUDA(launch_ana2d_l1_scalar(d, coeffs, H, W, B, s), "ana2d_l1_scalar launch");
+    return FHWT_OK;
+  }
+  DevInfo di;
+  FHWT_TRY(device_info(&di));
+  const size_t np = pl->passes.size();
+  for (size_t k = 0; k < np; ++k) {
+    const Pass ps = pl->passes[k];
+    const bool in64 = k > 0;
+    const bool final_pass = k + 1 == np;
+    Ana2dParams p{};
+    p.out = coeffs;
+    p.H = H;
+    p.W = W;
+    p.Hin = H >> ps.g0;
+    p.Win = W >> ps.g0;
+    p.batch = B;
+    p.Lp = ps.Lp;
+    p.g0 = ps.g0;
+    p.TR = choose_tr(p.Hin, ps.Lp);
+    p.TC = int(std::min<int64_t>(in64 ? 128 : 256, p.Win));
+    p.tiles_r = p.Hin / p.TR;
+    p.tiles_c = (p.Win + p.TC - 1) / p.TC;
+    p.ntiles = B * p.tiles_r * p.tiles_c;
+    p.final_pass = final_pass;
+    p.ws_out = final_pass ? nullptr : reinterpret_cast<double*>(ws + pl->ws_off[k]);
+    const void* in = k == 0 ? static_cast<const void*>(d) : static_cast<const void*>(ws + pl->ws_off[k - 1]);
+    const int64_t in_pitch = k == 0 ? W : pitch4(p.Win);
+    CUtensorMap map;
+    FHWT_TRY(encode_2d(&map, in, in64, p.Win, B * p.Hin, in_pitch, p.TC, p.TR));
+    // shared memory layout: stages | P[0] | P[1] | barriers
+    const size_t es = in64 ? 8 : 4;
+    p.stages = in64 ? 2 : 3;
+    p.stage_bytes = uint32_t(align_up(size_t(p.TR) * p.TC * es, 1024));
+    size_t pb[2] = {0, 0};
+    for (int j = 1; j < ps.Lp; ++j) {
+      const size_t sz = (in64 || ps.g0 + j >= kFirstF64Level) ? 8 : 4;
+      pb[j & 1] = std::max(pb[j & 1], size_t(p.TR >> j) * size_t(p.TC >> j) * sz);
+    }
+    size_t off = size_t(p.stages) * p.stage_bytes;
+    p.p_off[0] = uint32_t(off);
+    off = align_up(off + pb[0], 128);
+    p.p_off[1] = uint32_t(off);
+    off = align_up(off + pb[1], 128);
+    p.bar_off = uint32_t(off);
+    const size_t smem = off + 8 * size_t(p.stages);
+    int bps = 0;
+    FHWT_TRY(occupancy(in64 ? 1 : 0, smem, &bps));
+    const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
+    FHWT_CUDA(launch_ana2d(p, map, in64, int(grid), smem, s), "ana2d launch");
+  }
+  return FHWT_OK;
+}
+
+fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, char* ws, cudaStream_t s) {
+  const int64_t H = pl->h, W = pl->w, B = pl->batch;
+  if (W % 4 != 0 || !aligned16(coeffs) || !aligned16(dR)) {
+    if (pl->levels != 1)
+      return fail(FHWT_ERR_MISALIGNED, "multi-level 2-D transform needs 16-byte aligned buffers and w %% 4 == 0");
+    FHWT_CUDA(launch_syn2d_l1_scalar(coeffs, dR, H, W, B, s), "syn2d_l1_scalar launch");
+    return FHWT_OK;
+  }
+  DevInfo di;
+  FHWT_TRY(device_info(&di));
+  const size_t np = pl->passes.size();
+  for (size_t kk = np; kk-- > 0;) {
+    const Pass ps = pl->passes[kk];
+    Syn2dParams p{};
+    p.H = H;
+    p.W = W;
+    p.Hin = H >> ps.g0;
+    p.Win = W >> ps.g0;
+    p.batch = B;
+    p.Lp = ps.Lp;
+    p.g0 = ps.g0;
+    p.TR = choose_tr(p.Hin, ps.Lp);
+    p.TC = int(std::min<int64_t>(256, p.Win));
+    p.tiles_r = p.Hin / p.TR;
+    p.tiles_c = (p.Win + p.TC - 1) / p.TC;
+    p.ntiles = B * p.tiles_r * p.tiles_c;
+    if (kk == 0) {
+      p.out = dR;
+      p.out_pitch = W;
+    } else {
+      p.out = reinterpret_cast<float*>(ws + pl->ws_off[kk - 1]);
+      p.out_pitch = pitch4(p.Win);
+    }
+    TmaMaps2d maps;
+    std::memset(&maps, 0, sizeof maps);
+    int bw[6] = {0, 0, 0, 0, 0, 0};
+    for (int j = 1; j <= ps.Lp; ++j) {
+      bw[j] = int(pitch4(p.TC >> j));
+      p.box_pitch[j] = bw[j];
+      FHWT_TRY(encode_2d(&maps.level[j], coeffs, false, W, B * H, W, bw[j], p.TR >> j));
+    }
+    if (kk + 1 == np) {
+      p.ll_from_ws = 0;
+      maps.ll = maps.level[ps.Lp];
+    } else {
+      p.ll_from_ws = 1;
+      const int64_t wl = p.Win >> ps.Lp, hl = p.Hin >> ps.Lp;
+      FHWT_TRY(encode_2d(&maps.ll, ws + pl->ws_off[kk], false, wl, B * hl, pitch4(wl), bw[ps.Lp], p.TR >> ps.Lp));
+    }
+    // stage layout: LL box, then per level j three boxes
+    size_t off = 0, tx = 0;
+    {
+      const size_t bytes = size_t(p.TR >> ps.Lp) * bw[ps.Lp] * 4;
+      p.box_off[0][0] = uint32_t(off);
+      off = align_up(off + bytes, 128);
+      tx += bytes;
+    }
+    for (int j = 1; j <= ps.Lp; ++j) {
+      const size_t bytes = size_t(p.TR >> j) * bw[j] * 4;
+      for (int q = 0; q < 3; ++q) {
+        p.box_off[j][q] = uint32_t(off);
+        off = align_up(off + bytes, 128);
+        tx += bytes;
+      }
+    }
+    p.tx_bytes = uint32_t(tx);
+    p.stage_bytes = uint32_t(align_up(off, 1024));
+    p.stages = 3;
+    size_t pb[2] = {0, 0};
+    for (int j = 2; j <= ps.Lp; ++j) {
+      const int jj = j - 1;
+      pb[jj & 1] = std::max(pb[jj & 1], size_t(p.TR >> jj) * size_t(p.TC >> jj) * 4);
+    }
+    off = size_t(p.stages) * p.stage_bytes;
+    p.p_off[0] = uint32_t(off);
+    off = align_up(off + pb[0], 128);
+    p.p_off[1] = uint32_t(off);
+    off = align_up(off + pb[1], 128);
+    p.bar_off = uint32_t(off);
+    const size_t smem = off + 8 * size_t(p.stages);
+    int bps = 0;
+    FHWT_TRY(occupancy(2, smem, &bps));
+    const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
+    FHWT_CUDA(launch_syn2d(p, maps, int(grid), smem, s), "syn2d launch");
+  }
+  return FHWT_OK;
+}
+
+// ------------------------------------------------------------------ 1-D execution
+fhwt_status run_ana1d(const fhwt_plan_s* pl, const float* d, float* coeffs, char* ws, cudaStream_t s) {
+  const int64_t n = pl->n, B = pl->batch;
+  if (n % 4 != 0 || !aligned16(d) || !aligned16(coeffs)) {
+    if (pl->levels != 1)
+      return fail(FHWT_ERR_MISALIGNED, "multi-level 1-D transform needs 16-byte aligned buffers and n %% 4 == 0");
+    FHWT_CUDA(launch_ana1d_l1_scalar(d, coeffs, n, B, s), "ana1d_l1_scalar launch");
+    return FHWT_OK;
+  }
+  const size_t np = pl->passes.size();
+  for (size_t k = 0; k < np; ++k) {
+    const Pass ps = pl->passes[k];
+    Haar1dParams p{};
+    p.n = n;
+    p.nin = n >> ps.g0;
+    p.batch = B;
+    p.Lp = ps.Lp;
+    p.g0 = ps.g0;
+    p.chunks = (p.nin + kChunk1d - 1) / kChunk1d;
+    p.nwarps = B * p.chunks;
+    p.coeffs_out = coeffs;
+    p.final_pass = k + 1 == np;
+    p.in = k == 0 ? static_cast<const void*>(d) : static_cast<const void*>(ws + pl->ws_off[k - 1]);
+    p.in_pitch = k == 0 ? n : pitch4(p.nin);
+    p.out = p.final_pass ? nullptr : static_cast<void*>(ws + pl->ws_off[k]);
+    p.out_pitch = p.final_pass ? 0 : pitch4(p.nin >> ps.Lp);
+    FHWT_CUDA(launch_ana1d(p, k > 0, s), "ana1d launch");
+  }
+  return FHWT_OK;
+}
+
+fhwt_status run_syn1d(const fhwt_plan_s* pl, const float* coeffs, float* dR, char* ws, cudaStream_t s) {
+  const int64_t n = pl->n, B = pl->batch;
+  if (n % 4 != 0 || !aligned16(coeffs) || !aligned16(dR)) {
+    if (pl->levels != 1)
+      return fail(FHWT_ERR_MISALIGNED, "multi-level 1-D transform needs 16-byte aligned buffers and n %% 4 == 0");
+    FHWT_CUDA(launch_syn1d_l1_scalar(coeffs, dR, n, B, s), "syn1d_l1_scalar launch");
+    return FHWT_OK;
+  }
+  const size_t np = pl->passes.size();
+  for (size_t kk = np; kk-- > 0;) {
+    const Pass ps = pl->passes[kk];
+    Haar1dParams p{};
+    p.n = n;
+    p.nin = n >> ps.g0;
+    p.batch = B;
+    p.Lp = ps.Lp;
+    p.g0 = ps.g0;
+    p.chunks = (p.nin + kChunk1d - 1) / kChunk1d;
+    p.nwarps = B * p.chunks;
+    p.coeffs_in = coeffs;
+    p.final_pass = kk == 0;
+    if (kk + 1 == np) {
+      p.in = coeffs;
+      p.in_pitch = n;
+    } else {
+      p.in = ws + pl->ws_off[kk];
+      p.in_pitch = pitch4(p.nin >> ps.Lp);
+    }
+    if (kk == 0) {
+      p.out = dR;
+      p.out_pitch = n;
+    } else {
+      p.out = ws + pl->ws_off[kk - 1];
+      p.out_pitch = pitch4(p.nin);
+    }
+    FHWT_CUDA(launch_syn1d(p, s), "syn1d launch");
+  }
+  return FHWT_OK;
+}
+
+size_t data_bytes(const fhwt_plan_s* p) {
+  return size_t(p->batch) * (p->kind == 2 ? size_t(p->h) * size_t(p->w) : size_t(p->n)) * sizeof(float);
+}
+
+fhwt_status run(fhwt_plan p, const float* in, float* out, void* workspace, fhwt_stream_t st, bool analysis) {
+  if (!p) return fail(FHWT_ERR_INVALID_ARG, "null plan");
+  FHWT_TRY(check_ptrs(in, out, data_bytes(p)));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  char* ws = static_cast<char*>(workspace);
+  bool owned = false;
+  if (p->ws_bytes && !ws) {
+    void* t = nullptr;
+    FHWT_CUDA(cudaMallocAsync(&t, p->ws_bytes, s), "workspace cudaMallocAsync");
+    ws = static_cast<char*>(t);
+    owned = true;
+  }
+  fhwt_status st_ = FHWT_OK;
+  if (p->kind == 2)
+    st_ = analysis ? run_ana2d(p, in, out, ws, s) : run_syn2d(p, in, out, ws, s);
+  else
+    st_ = analysis ? run_ana1d(p, in, out, ws, s) : run_syn1d(p, in, out, ws, s);
+  if (owned) {
+    cudaError_t e = cudaFreeAsync(ws, s);
+    if (st_ == FHWT_OK && e != cudaSuccess) return cuda_fail(e, "workspace cudaFreeAsync");
+  }
+  return st_;
+}
+
+}  // namespace
+
+// ======================================================================= exported C ABI
+extern "C" {
+
+int fhwt_version(void) { return 10000; }
+
+uint64_t fhwt_launch_count(void) { return g_launches.load(); }
+
+const char* fhwt_last_error_message(void) { return g_last_error.c_str(); }
+
+const char* fhwt_status_string(fhwt_status st) {
+  switch (st) {
+    case FHWT_OK: return "FHWT_OK";
+    case FHWT_ERR_INVALID_ARG: return "FHWT_ERR_INVALID_ARG";
+    case FHWT_ERR_EMPTY: return "FHWT_ERR_EMPTY";
+    case FHWT_ERR_ODD_LENGTH: return "FHWT_ERR_ODD_LENGTH";
+    case FHWT_ERR_INVALID_LEVELS: return "FHWT_ERR_INVALID_LEVELS";
+    case FHWT_ERR_INSUFFICIENT_LENGTH: return "FHWT_ERR_INSUFFICIENT_LENGTH";
+    case FHWT_ERR_SHAPE_MISMATCH: return "FHWT_ERR_SHAPE_MISMATCH";
+    case FHWT_ERR_UNSUPPORTED_FILTER: return "FHWT_ERR_UNSUPPORTED_FILTER";
+    case FHWT_ERR_MISALIGNED: return "FHWT_ERR_MISALIGNED";
+    case FHWT_ERR_CUDA: return "FHWT_ERR_CUDA";
+    case FHWT_ERR_NO_DEVICE: return "FHWT_ERR_NO_DEVICE";
+  }
+  return "FHWT_ERR_UNKNOWN";
+}
+
+fhwt_status fhwt_haar_filter_bank(fhwt_filter_bank* out) {
+  if (!out) return fail(FHWT_ERR_INVALID_ARG, "null output");
+  const double s = 1.0 / std::sqrt(2.0);
+  out->b0[0] = s;  out->b0[1] = s;
+  out->b1[0] = -s; out->b1[1] = s;
+  out->a0[0] = s;  out->a0[1] = s;
+  out->a1[0] = s;  out->a1[1] = -s;
+  out->M = 2;
+  return FHWT_OK;
+}
+
+fhwt_status fhwt_plan_1d(fhwt_plan* p, int64_t n, int64_t batch, int levels, const fhwt_filter_bank* fb) {
+  if (!p) return fail(FHWT_ERR_INVALID_ARG, "null plan pointer");
+  *p = nullptr;
+  FHWT_TRY(check_1d(n, batch, levels));
+  FHWT_TRY(check_bank(fb));
+  auto* pl = new fhwt_plan_s{};
+  pl->kind = 1;
+  pl->n = n;
+  pl->batch = batch;
+  pl->levels = levels;
+  plan_layout(pl);
+  *p = pl;
+  return FHWT_OK;
+}
+
+fhwt_status fhwt_plan_2d(fhwt_plan* p, int64_t h, int64_t w, int64_t batch, int levels, const fhwt_filter_bank* fb) {
+  if (!p) return fail(FHWT_ERR_INVALID_ARG, "null plan pointer");
+  *p = nullptr;
+  FHWT_TRY(check_2d(h, w, batch, levels));
+  FHWT_TRY(check_bank(fb));
+  auto* pl = new fhwt_plan_s{};
+  pl->kind = 2;
+  pl->h = h;
+  pl->w = w;
+  pl->batch = batch;
+  pl->levels = levels;
+  plan_layout(pl);
+  *p = pl;
+  return FHWT_OK;
+}
+
+fhwt_status fhwt_plan_destroy(fhwt_plan p) {
+  delete p;
+  return FHWT_OK;
+}
+
+size_t fhwt_plan_workspace_bytes(fhwt_plan p) { return p ? p->ws_bytes : 0; }
+
+fhwt_status fhwt_plan_analyze(fhwt_plan p, const float* d, float* coeffs, void* workspace, fhwt_stream_t s) {
+  return run(p, d, coeffs, workspace, s, true);
+}
+
+fhwt_status fhwt_plan_synthesize(fhwt_plan p, const float* coeffs, float* dR, void* workspace, fhwt_stream_t s) {
+  return run(p, coeffs, dR, workspace, s, false);
+}
+
+fhwt_status fhwt_analyze_1d(const float* d, float* coeffs, int64_t n, int64_t batch, int levels, fhwt_stream_t s) {
+  fhwt_plan p;
+  FHWT_TRY(fhwt_plan_1d(&p, n, batch, levels, nullptr));
+  fhwt_status st = run(p, d, coeffs, nullptr, s, true);
+  delete p;
+  return st;
+}
+
+fhwt_status fhwt_synthesize_1d(const float* coeffs, float* dR, int64_t n, int64_t batch, int levels, fhwt_stream_t s) {
+  fhwt_plan p;
+  FHWT_TRY(fhwt_plan_1d(&p, n, batch, levels, nullptr));
+  fhwt_status st = run(p, coeffs, dR, nullptr, s, false);
+  delete p;
+  return st;
+}
+
+fhwt_status fhwt_analyze_2d(const float* d, float* coeffs, int64_t h, int64_t w, int64_t batch, int levels,
+                            fhwt_stream_t s) {
+  fhwt_plan p;
+  FHWT_TRY(fhwt_plan_2d(&p, h, w, batch, levels, nullptr));
+  fhwt_status st = run(p, d, coeffs, nullptr, s, true);
+  delete p;
+  return st;
+}
+
+fhwt_status fhwt_synthesize_2d(const float* coeffs, float* dR, int64_t h, int64_t w, int64_t batch, int levels,
+                               fhwt_stream_t s) {
+  fhwt_plan p;
+  FHWT_TRY(fhwt_plan_2d(&p, h, w, batch, levels, nullptr));
+  fhwt_status st = run(p, coeffs, dR, nullptr, s, false);
+  delete p;
+  return st;
+}
+
+int64_t fhwt_band_offset_1d(int64_t n, int level, int band, int64_t* len) {
+  if (n <= 0 || level < 1 || level > 62 || (band != 0 && band != 1) || n % (int64_t(1) << level)) return -1;
+  const int64_t l = n >> level;
+  if (len) *len = l;
+  return band == 0 ? 0 : l;
+}
+
+int64_t fhwt_band_offset_2d(int64_t h, int64_t w, int level, int band, int64_t* rows, int64_t* cols) {
+  if (h <= 0 || w <= 0 || level < 1 || level > 62 || band < 0 || band > 3) return -1;
+  if (h % (int64_t(1) << level) || w % (int64_t(1) << level)) return -1;
+  const int64_t hl = h >> level, wl = w >> level;
+  if (rows) *rows = hl;
+  if (cols) *cols = wl;
+  const int64_t r = (band & 2) ? hl : 0, c = (band & 1) ? wl : 0;
+  return r * w + c;
+}
+
+fhwt_status fhwt_pack_ll_2d(const float* coeffs, float* ll_packed, int64_t h, int64_t w, int64_t batch, int levels,
+                            fhwt_stream_t s) {
+  FHWT_TRY(check_2d(h, w, batch, levels));
+  if (!coeffs || !ll_packed) return fail(FHWT_ERR_INVALID_ARG, "null buffer pointer");
+  FHWT_CUDA(launch_pack_ll(coeffs, ll_packed, h, w, batch, levels, reinterpret_cast<cudaStream_t>(s)), "pack_ll launch");
+  return FHWT_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------- host-buffer streaming
+namespace {
+
+fhwt_status roundtrip_host(fhwt_plan_s* full, const float* h_d, float* h_c, float* h_r, int64_t unit_elems,
+                           int64_t chunk) {
+  const int64_t B = full->batch;
+  if (!h_d || !h_r) return fail(FHWT_ERR_INVALID_ARG, "null host buffer");
+  const int64_t unit_bytes = unit_elems * int64_t(sizeof(float));
+  if (chunk <= 0) chunk = std::max<int64_t>(1, (int64_t(256) << 20) / std::max<int64_t>(unit_bytes, 1));
+  chunk = std::min(chunk, B);
+  // chunk-sized plan (same shape, fewer units)
+  fhwt_plan_s cp = *full;
+  cp.batch = chunk;
+  plan_layout(&cp);
+  cudaStream_t st[2];
+  FHWT_CUDA(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking), "stream create");
+  FHWT_CUDA(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking), "stream create");
+  const size_t cbytes = size_t(chunk) * size_t(unit_bytes);
+  const size_t wsb = align_up(cp.ws_bytes, 256);
+  char* buf[2] = {nullptr, nullptr};
+  fhwt_status rs = FHWT_OK;
+  for (int i = 0; i < 2 && rs == FHWT_OK; ++i) {
+    void* t = nullptr;
+    cudaError_t e = cudaMallocAsync(&t, 3 * align_up(cbytes, 256) + wsb, st[i]);
+    if (e != cudaSuccess) rs = cuda_fail(e, "staging cudaMallocAsync");
+    buf[i] = static_cast<char*>(t);
+  }
+  for (int64_t u0 = 0, it = 0; u0 < B && rs == FHWT_OK; u0 += chunk, ++it) {
+    const int k = int(it & 1);
+    const int64_t cnt = std::min(chunk, B - u0);
+    cudaStream_t s = st[k];
+    float* dd = reinterpret_cast<float*>(buf[k]);
+    float* dc = reinterpret_cast<float*>(buf[k] + align_up(cbytes, 256));
+    float* dr = reinterpret_cast<float*>(buf[k] + 2 * align_up(cbytes, 256));
+    char* ws = buf[k] + 3 * align_up(cbytes, 256);
+    const size_t bytes = size_t(cnt) * size_t(unit_bytes);
+    fhwt_plan_s pp = cp;
+    if (cnt != chunk) {
+      pp.batch = cnt;
+      plan_layout(&pp);
+    }
+    cudaError_t e = cudaMemcpyAsync(dd, h_d + u0 * unit_elems, bytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) { rs = cuda_fail(e, "H2D copy"); break; }
+    rs = run(&pp, dd, dc, ws, reinterpret_cast<fhwt_stream_t>(s), true);
+    if (rs != FHWT_OK) break;
+    if (h_c) {
+      e = cudaMemcpyAsync(h_c + u0 * unit_elems, dc, bytes, cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) { rs = cuda_fail(e, "D2H copy"); break; }
+    }
+    rs = run(&pp, dc, dr, ws, reinterpret_cast<fhwt_stream_t>(s), false);
+    if (rs != FHWT_OK) break;
+    e = cudaMemcpyAsync(h_r + u0 * unit_elems, dr, bytes, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) { rs = cuda_fail(e, "D2H copy"); break; }
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (buf[i]) cudaFreeAsync(buf[i], st[i]);
+    cudaError_t e = cudaStreamSynchronize(st[i]);
+    if (rs == FHWT_OK && e != cudaSuccess) rs = cuda_fail(e, "stream synchronize");
+    cudaStreamDestroy(st[i]);
+  }
+  return rs;
+}
+
+}  // namespace
+
+extern "C" fhwt_status fhwt_roundtrip_2d_host(const float* h_d, float* h_coeffs, float* h_dR, int64_t h, int64_t w,
+                                              int64_t batch, int levels, int64_t chunk) {
+  fhwt_plan p;
+  FHWT_TRY(fhwt_plan_2d(&p, h, w, batch, levels, nullptr));
+  fhwt_status st = roundtrip_host(p, h_d, h_coeffs, h_dR, h * w, chunk);
+  delete p;
+  return st;
+}
+
+extern "C" fhwt_status fhwt_roundtrip_1d_host(const float* h_d, float* h_coeffs, float* h_dR, int64_t n, int64_t batch,
+                                              int levels, int64_t chunk) {
+  fhwt_plan p;
+  FHWT_TRY(fhwt_plan_1d(&p, n, batch, levels, nullptr));
+  fhwt_status st = roundtrip_host(p, h_d, h_coeffs, h_dR, n, chunk);
+  delete p;
+  return st;
+}

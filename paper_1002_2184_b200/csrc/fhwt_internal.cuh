@@ -1,0 +1,185 @@
+// Internal declarations shared by the fhwt CUDA translation units (not part of the C ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fhwt {
+
+// fl(1/√2): the polyphase component b00 = a00.
+constexpr float kS32 = 0.70710678118654752440f;
+constexpr double kS64 = 0.70710678118654752440;
+
+// Levels per fused pass: 2-D tiles of 32 rows cover 5 levels, 1-D warp
+// chunks of 1024 samples cover 10 levels.
+constexpr int kMaxLevels2dPass = 5;
+constexpr int kMaxLevels1dPass = 10;
+constexpr int kChunk1d = 1024;
+constexpr int kThreads2d = 256;
+constexpr int kThreads1d = 256;
+
+// First global level computed in fp64 (levels 1..3 fp32).  DESIGN.md "Precision".
+constexpr int kFirstF64Level = 4;
+
+// ------------------------------------------------------------------ 2-D pass parameters
+struct Ana2dParams {
+  float* out;            // Mallat coefficients, image 0, row pitch W (fp32)
+  double* ws_out;        // LL_{g0+Lp} hand-off (fp64) when !final_pass; pitch Win >> Lp
+  int64_t H, W;          // full image dims (output layout)
+  int64_t Hin, Win;      // this pass's input dims per image (= H >> g0, W >> g0)
+  int64_t batch;
+  int Lp, g0;            // levels in this pass, global level offset
+  int TR, TC;            // tile rows / cols (input coordinates)
+  int64_t tiles_r;       // row tiles per image
+  int64_t tiles_c;       // column tiles
+  int64_t ntiles;
+  int stages;
+  uint32_t stage_bytes, p_off[2], bar_off;
+  int final_pass;
+};
+
+struct Syn2dParams {
+  float* out;            // d_R (final pass, pitch W) or the LL_{g0} hand-off (pitch Win)
+  int64_t out_pitch;
+  int64_t H, W;          // full image dims (coefficient layout)
+  int64_t Hin, Win;      // this pass's OUTPUT dims per image (= H >> g0, W >> g0)
+  int64_t batch;
+  int Lp, g0;
+  int TR, TC;
+  int64_t tiles_r, tiles_c, ntiles;
+  int stages;
+  uint32_t stage_bytes, bar_off;
+  uint32_t box_off[6][3];  // per pass-level j (1..Lp): offsets of HL, LH, HH boxes; [0][0] = LL box
+  int box_pitch[6];        // smem pitch (elements) of level-j boxes; [0] unused
+  uint32_t p_off[2];
+  uint32_t tx_bytes;       // bytes landed per stage
+  int ll_from_ws;          // LL_{g0+Lp} comes from the workspace map (else from coeffs)
+};
+
+struct TmaMaps2d {
+  CUtensorMap level[6];  // coeff view box for pass-level j = 1..Lp ([0] unused)
+  CUtensorMap ll;        // LL_{g0+Lp} source box
+};
+
+// ------------------------------------------------------------------ 1-D pass parameters
+struct Haar1dParams {
+  const void* in;        // analysis: pass input (fp32 d or fp64 ws); synthesis: approx source
+  int64_t in_pitch;      // elements between signals of `in`
+  float* coeffs_out;     // analysis: coefficient array (pitch n)
+  const float* coeffs_in;  // synthesis: coefficient array (pitch n)
+  void* out;             // analysis: approx hand-off (fp64 ws) / synthesis: output (fp32)
+  int64_t out_pitch;
+  int64_t n;             // full signal length (coefficient pitch)
+  int64_t nin;           // this pass's signal length (= n >> g0)
+  int64_t batch;
+  int64_t chunks;        // chunks per signal
+  int64_t nwarps;
+  int Lp, g0;
+  int final_pass;        // analysis: approx goes to coeffs; synthesis: output is d_R
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool in_f64, int grid,
+                         size_t smem, cudaStream_t s);
+cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int grid, size_t smem, cudaStream_t s);
+cudaError_t ana2d_occupancy(bool in_f64, size_t smem, int* blocks_per_sm);
+cudaError_t syn2d_occupancy(size_t smem, int* blocks_per_sm);
+cudaError_t launch_ana1d(const Haar1dParams& p, bool in_f64, cudaStream_t s);
+cudaError_t launch_syn1d(const Haar1dParams& p, cudaStream_t s);
+cudaError_t launch_ana2d_l1_scalar(const float* d, float* c, int64_t h, int64_t w, int64_t batch, cudaStream_t s);
+cudaError_t launch_syn2d_l1_scalar(const float* c, float* d, int64_t h, int64_t w, int64_t batch, cudaStream_t s);
+cudaError_t launch_ana1d_l1_scalar(const float* d, float* c, int64_t n, int64_t batch, cudaStream_t s);
+cudaError_t launch_syn1d_l1_scalar(const float* c, float* d, int64_t n, int64_t batch, cudaStream_t s);
+cudaError_t launch_pack_ll(const float* c, float* ll, int64_t h, int64_t w, int64_t batch, int levels,
+                           cudaStream_t s);
+
+void count_launch();
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_LOOP:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra WAIT_DONE;\n"
+      "bra WAIT_LOOP;\n"
+      "WAIT_DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// TMA 2-D tile load global -> shared, completion counted on `bar` (complete_tx bytes).
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// streaming global accesses (read once / written once: do not allocate in L1)
+__device__ __forceinline__ float4 ldg_stream4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float2 ldg_stream2(const float* p) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ldg_stream1(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg_stream4(float* p, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void stg_stream2(float* p, float2 v) {
+  asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void stg_stream1(float* p, float v) {
+  asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+}  // namespace fhwt

@@ -1,0 +1,433 @@
+// Fused multi-level 2-D Fast Haar analysis / synthesis kernels for sm_100a.
+//
+// Method: the polyphase "Fast Haar" banks of arXiv 1002.2184 (analysis: §III
+// Fig. 4; synthesis: §IV Figs. 6-7, Eq. (19)) applied separably, rows then
+// columns (reading R8).  Per 2x2 input block [[a, b], [c, d]] the row
+// butterflies (x_e ± x_o)/√2 followed by the column butterflies fold to one exact ×½:
+//     LL = ½((a+b)+(c+d))  LH = ½((a+b)−(c+d))  HL = ½((a−b)+(c−d))  HH = ½((a−b)−(c−d))
+// and the synthesis bank (Eq. (19), A00 = A01 = 1/√2) folds to
+//     a = ½((LL+LH)+(HL+HH))  b = ½((LL+LH)−(HL+HH))  c = ½((LL−LH)+(HL−HH))  d = ½((LL−LH)−(HL−HH)).
+//
+// B200 design: persistent CTAs (2 per SM) stream TR x TC tiles
+// (32 x 256 fp32 = 32 KB) through a 3-stage TMA (cp.async.bulk.tensor) + mbarrier ring; all
+// Lp <= 5 levels of a tile run in shared memory / registers; every detail band is written once,
+// coalesced (float2 per thread, >= 32 B per row segment at the coarsest level), so HBM sees one
+// read and one write of each sample.  Levels g >= 4 are computed in fp64.
+#include "fhwt_internal.cuh"
+
+namespace fhwt {
+
+namespace {
+
+// band codes: 1 = HL (right half), 2 = LH (bottom half), 3 = HH (both)
+__device__ __forceinline__ float* band_row_ptr(const Ana2dParams& p, int64_t b, int g, int band, int64_t r) {
+  const int64_t hg = p.H >> g, wg = p.W >> g;
+  const int64_t row = ((band & 2) ? hg : 0) + r;
+  const int64_t col = (band & 1) ? wg : 0;
+  return p.out + (b * p.H + row) * p.W + col;
+}
+
+// stores V consecutive floats at p[0..V) of which the first `nvalid` are inside the band
+template <int V>
+__device__ __forceinline__ void store_row(float* ptr, const float (&v)[V], int64_t nvalid) {
+  if constexpr (V == 2) {
+    if (nvalid >= 2 && (reinterpret_cast<uintptr_t>(ptr) & 7) == 0) {
+      stg_stream2(ptr, make_float2(v[0], v[1]));
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < V; ++i)
+    if (i < nvalid) stg_stream1(ptr + i, v[i]);
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void load_row(const T* src, T (&v)[N]) {
+  if constexpr (sizeof(T) == 4 && N == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(src);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else if constexpr (sizeof(T) == 4 && N == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(src);
+    v[0] = t.x; v[1] = t.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(src + i);
+      v[i] = t.x; v[i + 1] = t.y;
+    }
+  }
+}
+
+// One analysis level of one tile.  Source: R x C region (smem, pitch C) of LL_{g-1} (or the input
+// tile); V output columns per thread unit.  Writes HL/LH/HH of global level g to HBM and LL_g to
+// smem (lldst, pitch C/2) or, on the pass's last level, to HBM (coeffs LL region or fp64 ws).
+template <typename TS, typename TC, int V>
+__device__ __forceinline__ void ana_level(const Ana2dParams& p, const TS* __restrict__ src, int R, int C, int j,
+                                          int64_t b, int64_t row0, int64_t col0, TC* __restrict__ lldst,
+                                          bool last) {
+  const int g = p.g0 + j;
+  const int OC = C >> 1;
+  const int upr = OC / V;
+  const int nunits = (R >> 1) * upr;
+  const int64_t brow = row0 >> j, bcol = col0 >> j;
+  const int64_t nvalid_row = (p.Win >> j) - bcol;  // valid output cols of this tile at this level
+  const TC half = TC(0.5);
+  for (int u = threadIdx.x; u < nunits; u += blockDim.x) {
+    const int orow = u / upr;
+    const int oc = (u - orow * upr) * V;
+    TS t0[2 * V], t1[2 * V];
+    load_row<TS, 2 * V>(src + (2 * orow) * C + 2 * oc, t0);
+    load_row<TS, 2 * V>(src + (2 * orow + 1) * C + 2 * oc, t1);
+    float hl[V], lh[V], hh[V];
+    TC ll[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const TC a = TC(t0[2 * v]), bb = TC(t0[2 * v + 1]), c = TC(t1[2 * v]), d = TC(t1[2 * v + 1]);
+      const TC s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+      ll[v] = (s1 + s2) * half;
+      lh[v] = float((s1 - s2) * half);
+      hl[v] = float((d1 + d2) * half);
+      hh[v] = float((d1 - d2) * half);
+    }
+    const int64_t nv = nvalid_row - oc;
+    const int64_t r = brow + orow, cc = bcol + oc;
+    store_row<V>(band_row_ptr(p, b, g, 1, r) + cc, hl, nv);
+    store_row<V>(band_row_ptr(p, b, g, 2, r) + cc, lh, nv);
+    store_row<V>(band_row_ptr(p, b, g, 3, r) + cc, hh, nv);
+    if (!last) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) lldst[orow * OC + oc + v] = ll[v];
+    } else if (p.final_pass) {
+      float llf[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) llf[v] = float(ll[v]);
+      store_row<V>(p.out + (b * p.H + r) * p.W + cc, llf, nv);
+    } else {
+      // fp64 hand-off of LL_{g} to the next pass (pitch = padded Win >> Lp, see fhwt_api.cu)
+      const int64_t wpitch = ((p.Win >> j) + 3) & ~int64_t(3);
+      double* w = p.ws_out + (b * (p.Hin >> j) + r) * wpitch + cc;
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (v < nv) w[v] = double(ll[v]);
+    }
+  }
+}
+
+template <typename TS, typename TC>
+__device__ __forceinline__ void ana_level_v(const Ana2dParams& p, const TS* src, int R, int C, int j, int64_t b,
+                                            int64_t row0, int64_t col0, TC* lldst, bool last) {
+  if (((C >> 1) & 1) == 0)
+    ana_level<TS, TC, 2>(p, src, R, C, j, b, row0, col0, lldst, last);
+  else
+    ana_level<TS, TC, 1>(p, src, R, C, j, b, row0, col0, lldst, last);
+}
+
+template <typename TIn>
+__device__ __forceinline__ void ana_tile(const Ana2dParams& p, const TIn* stage, unsigned char* smem, int64_t b,
+                                         int64_t row0, int64_t col0) {
+  int R = p.TR, C = p.TC;
+  const void* src = stage;
+  bool src64 = sizeof(TIn) == 8;
+  for (int j = 1; j <= p.Lp; ++j) {
+    const bool cmp64 = src64 || (p.g0 + j) >= kFirstF64Level;
+    const bool last = j == p.Lp;
+    void* dst = smem + p.p_off[j & 1];
+    if (!src64 && !cmp64)
+      ana_level_v<float, float>(p, (const float*)src, R, C, j, b, row0, col0, (float*)dst, last);
+    else if (!src64)
+      ana_level_v<float, double>(p, (const float*)src, R, C, j, b, row0, col0, (double*)dst, last);
+    else
+      ana_level_v<double, double>(p, (const double*)src, R, C, j, b, row0, col0, (double*)dst, last);
+    if (!last) __syncthreads();
+    src = dst;
+    src64 = cmp64;
+    R >>= 1;
+    C >>= 1;
+  }
+}
+
+template <typename TIn>
+__global__ void __launch_bounds__(kThreads2d) ana2d_kernel(const __grid_constant__ Ana2dParams p,
+                                                           const __grid_constant__ CUtensorMap in_map) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    prefetch_tmap(&in_map);
+    for (int s = 0; s < p.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t tile_bytes = uint32_t(p.TR) * uint32_t(p.TC) * uint32_t(sizeof(TIn));
+  uint64_t pol = 0;
+  if (tid == 0) {
+    pol = policy_evict_first();
+    for (int s = 0; s < p.stages; ++s) {
+      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
+      if (t < p.ntiles) {
+        const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+        mbar_arrive_expect_tx(&bars[s], tile_bytes);
+        tma_load_2d(smem + s * p.stage_bytes, &in_map, int(ct * p.TC), int(rt * p.TR), &bars[s], pol);
+      }
+    }
+  }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+    const int s = it % p.stages;
+    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
+    const int64_t b = rt / p.tiles_r;
+    const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
+    ana_tile<TIn>(p, reinterpret_cast<const TIn*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC);
+    __syncthreads();  // stage s and the LL buffers are free again
+    if (tid == 0) {
+      const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
+      if (nt < p.ntiles) {
+        const int64_t nrt = nt / p.tiles_c, nct = nt - nrt * p.tiles_c;
+        mbar_arrive_expect_tx(&bars[s], tile_bytes);
+        tma_load_2d(smem + s * p.stage_bytes, &in_map, int(nct * p.TC), int(nrt * p.TR), &bars[s], pol);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------ synthesis
+template <int V>
+__device__ __forceinline__ void store_out_row(float* ptr, const float (&v)[2 * V], int64_t nvalid) {
+  if constexpr (V == 2) {
+    if (nvalid >= 4 && (reinterpret_cast<uintptr_t>(ptr) & 15) == 0) {
+      stg_stream4(ptr, make_float4(v[0], v[1], v[2], v[3]));
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2 * V; ++i)
+    if (i < nvalid) stg_stream1(ptr + i, v[i]);
+}
+
+// One synthesis level: coefficient block R x C (tile rows/cols at level j) -> LL_{j-1} (2R x 2C).
+template <int V>
+__device__ __forceinline__ void syn_level(const Syn2dParams& p, const float* __restrict__ ll, int llp,
+                                          const float* __restrict__ hl, const float* __restrict__ lh,
+                                          const float* __restrict__ hh, int bp, int R, int C, int j, int64_t b,
+                                          int64_t row0, int64_t col0, float* __restrict__ dst) {
+  const int upr = C / V;
+  const int nunits = R * upr;
+  const int OC = 2 * C;  // dst pitch when dst is smem
+  for (int u = threadIdx.x; u < nunits; u += blockDim.x) {
+    const int r = u / upr;
+    const int c = (u - r * upr) * V;
+    float vll[V], vhl[V], vlh[V], vhh[V];
+    load_row<float, V>(ll + r * llp + c, vll);
+    load_row<float, V>(hl + r * bp + c, vhl);
+    load_row<float, V>(lh + r * bp + c, vlh);
+    load_row<float, V>(hh + r * bp + c, vhh);
+    float top[2 * V], bot[2 * V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const float s = vll[v] + vlh[v], t = vhl[v] + vhh[v];
+      const float s2 = vll[v] - vlh[v], t2 = vhl[v] - vhh[v];
+      top[2 * v] = (s + t) * 0.5f;
+      top[2 * v + 1] = (s - t) * 0.5f;
+      bot[2 * v] = (s2 + t2) * 0.5f;
+      bot[2 * v + 1] = (s2 - t2) * 0.5f;
+    }
+    if (j > 1) {
+#pragma unroll
+      for (int k = 0; k < 2 * V; ++k) {
+        dst[(2 * r) * OC + 2 * c + k] = top[k];
+        dst[(2 * r + 1) * OC + 2 * c + k] = bot[k];
+      }
+    } else {
+      const int64_t nv = p.Win - (col0 + 2 * c);
+      float* o = p.out + (b * p.Hin + row0 + 2 * r) * p.out_pitch + col0 + 2 * c;
+      store_out_row<V>(o, top, nv);
+      store_out_row<V>(o + p.out_pitch, bot, nv);
+    }
+  }
+}
+
+__device__ __forceinline__ void syn_tile(const Syn2dParams& p, unsigned char* stage, unsigned char* smem, int64_t b,
+                                         int64_t row0, int64_t col0) {
+  const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]);
+  int llp = p.box_pitch[p.Lp];
+  for (int j = p.Lp; j >= 1; --j) {
+    const int R = p.TR >> j, C = p.TC >> j;
+    const float* hl = reinterpret_cast<const float*>(stage + p.box_off[j][0]);
+    const float* lh = reinterpret_cast<const float*>(stage + p.box_off[j][1]);
+    const float* hh = reinterpret_cast<const float*>(stage + p.box_off[j][2]);
+    float* dst = reinterpret_cast<float*>(smem + p.p_off[(j - 1) & 1]);
+    if ((C & 1) == 0)
+      syn_level<2>(p, ll, llp, hl, lh, hh, p.box_pitch[j], R, C, j, b, row0, col0, dst);
+    else
+      syn_level<1>(p, ll, llp, hl, lh, hh, p.box_pitch[j], R, C, j, b, row0, col0, dst);
+    if (j > 1) __syncthreads();
+    ll = dst;
+    llp = 2 * C;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads2d) syn2d_kernel(const __grid_constant__ Syn2dParams p,
+                                                           const __grid_constant__ TmaMaps2d maps) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int j = 1; j <= p.Lp; ++j) prefetch_tmap(&maps.level[j]);
+    prefetch_tmap(&maps.ll);
+    for (int s = 0; s < p.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint64_t pol = 0;
+  auto issue = [&](int64_t t, int s) {
+    const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+    const int64_t b = rt / p.tiles_r;
+    const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = ct * p.TC;
+    unsigned char* base = smem + s * p.stage_bytes;
+    mbar_arrive_expect_tx(&bars[s], p.tx_bytes);
+    const int L = p.Lp;
+    if (p.ll_from_ws)
+      tma_load_2d(base + p.box_off[0][0], &maps.ll, int(col0 >> L), int(b * (p.Hin >> L) + (row0 >> L)), &bars[s], pol);
+    else
+      tma_load_2d(base + p.box_off[0][0], &maps.ll, int(col0 >> L), int(b * p.H + (row0 >> L)), &bars[s], pol);
+    for (int j = L; j >= 1; --j) {
+      const int g = p.g0 + j;
+      const int64_t hg = p.H >> g, wg = p.W >> g;
+      const int64_t br = b * p.H + (row0 >> j), bc = col0 >> j;
+      tma_load_2d(base + p.box_off[j][0], &maps.level[j], int(wg + bc), int(br), &bars[s], pol);
+      tma_load_2d(base + p.box_off[j][1], &maps.level[j], int(bc), int(br + hg), &bars[s], pol);
+      tma_load_2d(base + p.box_off[j][2], &maps.level[j], int(wg + bc), int(br + hg), &bars[s], pol);
+    }
+  };
+  if (tid == 0) {
+    pol = policy_evict_first();
+    for (int s = 0; s < p.stages; ++s) {
+      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
+      if (t < p.ntiles) issue(t, s);
+    }
+  }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+    const int s = it % p.stages;
+    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
+    const int64_t b = rt / p.tiles_r;
+    const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
+    syn_tile(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC);
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
+      if (nt < p.ntiles) issue(nt, s);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ single-level scalar kernels
+// Used only when the row length is not a multiple of 4 (then levels == 1, since w % 2^levels == 0),
+// where 16-byte vector / TMA access is impossible.  One thread per 2x2 block.
+__global__ void ana2d_l1_scalar_kernel(const float* __restrict__ d, float* __restrict__ c, int64_t h, int64_t w,
+                                       int64_t batch) {
+  const int64_t hw = (h / 2) * (w / 2);
+  const int64_t total = batch * hw;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / hw, rem = i - b * hw;
+    const int64_t r = rem / (w / 2), q = rem - r * (w / 2);
+    const float* x = d + b * h * w + (2 * r) * w + 2 * q;
+    const float a = x[0], bb = x[1], cc = x[w], dd = x[w + 1];
+    const float s1 = a + bb, s2 = cc + dd, d1 = a - bb, d2 = cc - dd;
+    float* o = c + b * h * w;
+    o[r * w + q] = (s1 + s2) * 0.5f;
+    o[r * w + w / 2 + q] = (d1 + d2) * 0.5f;
+    o[(h / 2 + r) * w + q] = (s1 - s2) * 0.5f;
+    o[(h / 2 + r) * w + w / 2 + q] = (d1 - d2) * 0.5f;
+  }
+}
+
+__global__ void syn2d_l1_scalar_kernel(const float* __restrict__ c, float* __restrict__ d, int64_t h, int64_t w,
+                                       int64_t batch) {
+  const int64_t hw = (h / 2) * (w / 2);
+  const int64_t total = batch * hw;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / hw, rem = i - b * hw;
+    const int64_t r = rem / (w / 2), q = rem - r * (w / 2);
+    const float* o = c + b * h * w;
+    const float ll = o[r * w + q], hl = o[r * w + w / 2 + q];
+    const float lh = o[(h / 2 + r) * w + q], hh = o[(h / 2 + r) * w + w / 2 + q];
+    const float s = ll + lh, t = hl + hh, s2 = ll - lh, t2 = hl - hh;
+    float* x = d + b * h * w + (2 * r) * w + 2 * q;
+    x[0] = (s + t) * 0.5f;
+    x[1] = (s - t) * 0.5f;
+    x[w] = (s2 + t2) * 0.5f;
+    x[w + 1] = (s2 - t2) * 0.5f;
+  }
+}
+
+__global__ void pack_ll_kernel(const float* __restrict__ c, float* __restrict__ ll, int64_t h, int64_t w,
+                               int64_t batch, int levels) {
+  const int64_t hl = h >> levels, wl = w >> levels;
+  const int64_t total = batch * hl * wl;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / (hl * wl), rem = i - b * hl * wl;
+    const int64_t r = rem / wl, q = rem - r * wl;
+    ll[i] = c[b * h * w + r * w + q];
+  }
+}
+
+int grid_for(int64_t total, int threads) {
+  int64_t g = (total + threads - 1) / threads;
+  if (g > 148 * 32) g = 148 * 32;
+  return int(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+cudaError_t ana2d_occupancy(bool in_f64, size_t smem, int* blocks_per_sm) {
+  const void* fn = in_f64 ? (const void*)ana2d_kernel<double> : (const void*)ana2d_kernel<float>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kThreads2d, smem);
+}
+
+cudaError_t syn2d_occupancy(size_t smem, int* blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute((const void*)syn2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (const void*)syn2d_kernel, kThreads2d, smem);
+}
+
+cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool in_f64, int grid, size_t smem,
+                         cudaStream_t s) {
+  count_launch();
+  if (in_f64)
+    ana2d_kernel<double><<<grid, kThreads2d, smem, s>>>(p, in_map);
+  else
+    ana2d_kernel<float><<<grid, kThreads2d, smem, s>>>(p, in_map);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int grid, size_t smem, cudaStream_t s) {
+  count_launch();
+  syn2d_kernel<<<grid, kThreads2d, smem, s>>>(p, maps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ana2d_l1_scalar(const float* d, float* c, int64_t h, int64_t w, int64_t batch, cudaStream_t s) {
+  count_launch();
+  ana2d_l1_scalar_kernel<<<grid_for(batch * (h / 2) * (w / 2), 256), 256, 0, s>>>(d, c, h, w, batch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_syn2d_l1_scalar(const float* c, float* d, int64_t h, int64_t w, int64_t batch, cudaStream_t s) {
+  count_launch();
+  syn2d_l1_scalar_kernel<<<grid_for(batch * (h / 2) * (w / 2), 256), 256, 0, s>>>(c, d, h, w, batch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_ll(const float* c, float* ll, int64_t h, int64_t w, int64_t batch, int levels,
+                           cudaStream_t s) {
+  count_launch();
+  pack_ll_kernel<<<grid_for(batch * (h >> levels) * (w >> levels), 256), 256, 0, s>>>(c, ll, h, w, batch, levels);
+  return cudaGetLastError();
+}
+
+}  // namespace fhwt

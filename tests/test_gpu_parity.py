@@ -1,0 +1,199 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the fp64 oracle (oracle/).
+
+Tolerance (BASELINE.json north_star): for every coefficient and for the
+round trip, |gpu - oracle| <= 1e-5 * max|d| with max|d| taken per transform unit (signal for
+1-D, image for 2-D; reading A9).  Integer images (c3) must be bit-exact (IEEE ==) against the
+exact closed form.
+"""
+import numpy as np
+import pytest
+
+import datagen
+import oracle as o
+from oracle.closed_form import closed_form_2d
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - the -m gpu suite runs on a B200
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1002_2184_b200 as fhwt  # noqa: E402
+
+TOL = 1e-5
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.double().cpu().numpy()
+
+
+def unit_max(x, ndim):
+    axes = tuple(range(x.ndim - ndim, x.ndim))
+    return np.max(np.abs(x), axis=axes, keepdims=True)
+
+
+def assert_close(got, ref, scale_src, ndim, tol=TOL, what=""):
+    """Per-unit max error <= tol * max|d_unit|."""
+    scale = np.maximum(unit_max(np.asarray(scale_src, dtype=np.float64), ndim), 1e-30)
+    err = np.abs(np.asarray(got, np.float64) - np.asarray(ref, np.float64)) / scale
+    worst = float(err.max()) if err.size else 0.0
+    assert worst <= tol, f"{what}: max err {worst:.3e} x max|d| > {tol:g}"
+    return worst
+
+
+def check_1d(x, levels):
+    xd = dev(x)
+    c = fhwt.analyze_1d(xd, levels)
+    ref = o.decompose_1d(x, levels)
+    assert_close(host(c), ref, x, 1, what=f"1-D analysis n={x.shape[-1]} J={levels}")
+    # synthesis alone, from the oracle's coefficients rounded to fp32
+    c32 = ref.astype(np.float32)
+    r = fhwt.synthesize_1d(dev(c32), levels)
+    assert_close(host(r), o.reconstruct_1d(c32, levels), x, 1, what="1-D synthesis")
+    # round trip through the GPU coefficients
+    rr = fhwt.synthesize_1d(c, levels)
+    assert_close(host(rr), x, x, 1, what="1-D round trip")
+
+
+def check_2d(x, levels):
+    xd = dev(x)
+    c = fhwt.analyze_2d(xd, levels)
+    ref = o.analyze_2d(x, levels)
+    assert_close(host(c), ref, x, 2, what=f"2-D analysis {x.shape} L={levels}")
+    c32 = ref.astype(np.float32)
+    r = fhwt.synthesize_2d(dev(c32), levels)
+    assert_close(host(r), o.synthesize_2d(c32, levels), x, 2, what="2-D synthesis")
+    rr = fhwt.synthesize_2d(c, levels)
+    assert_close(host(rr), x, x, 2, what="2-D round trip")
+    return c
+
+
+# ------------------------------------------------------------------ 1-D
+def test_c1_full():
+    """BASELINE configs[0]: 1 x 1024, J=1."""
+    check_1d(datagen.c1_signal()[None], 1)
+
+
+@pytest.mark.parametrize("n,batch,levels", [
+    (2, 3, 1), (6, 2, 1),                      # n % 4 != 0: scalar single-level path
+    (4, 3, 1), (4, 3, 2), (8, 2, 3), (12, 2, 2), (64, 5, 6), (256, 2, 8),
+    (1024, 4, 10), (2048, 3, 10), (3072, 2, 10),
+    (1536, 2, 9), (1040, 3, 4),                # ragged last chunk
+    (1 << 11, 2, 11), (1 << 14, 3, 14),        # > 10 levels: fp64 hand-off, second pass
+    (12288, 2, 12),                            # second pass on 12-sample signals
+    (4096, 2, 1), (4096, 2, 3), (4096, 2, 5), (4096, 2, 7),
+])
+def test_1d_shapes(n, batch, levels):
+    check_1d(datagen.uniform((batch, n), seed=n * 31 + levels), levels)
+
+
+def test_c2_reduced():
+    """BASELINE configs[1] generator and length, 64 of the 4096 signals, J=10."""
+    check_1d(datagen.c2_batch(0, 64), 10)
+
+
+# ------------------------------------------------------------------ 2-D
+def test_c3_bit_exact():
+    """BASELINE configs[2]: 512^2 uint8 image, L=3; exact dyadic coefficients (C6)."""
+    x = datagen.c3_image()
+    c = host(fhwt.analyze_2d(dev(x), 3))
+    exact = closed_form_2d(x, 3, exact_int=True)
+    assert np.array_equal(c, exact), f"{np.count_nonzero(c != exact)} coefficients differ from the exact value"
+    assert_close(c, o.analyze_2d(x, 3), x, 2, tol=1e-12, what="c3 vs oracle")
+    r = host(fhwt.synthesize_2d(dev(c.astype(np.float32)), 3))
+    assert np.array_equal(r, x.astype(np.float64)), "c3 round trip is not exact"
+    check_2d(x, 3)
+
+
+@pytest.mark.parametrize("h,w,batch,levels", [
+    (2, 2, 1, 1), (6, 6, 2, 1), (6, 10, 1, 1),   # w % 4 != 0: scalar single-level path
+    (4, 4, 3, 2), (8, 8, 2, 3), (32, 4, 2, 2), (16, 24, 1, 3), (32, 32, 1, 5),
+    (96, 320, 2, 5),                              # ragged column tile
+    (64, 64, 2, 6), (64, 192, 1, 6), (128, 128, 1, 7), (256, 512, 1, 8),   # two passes
+    (1024, 1024, 1, 10), (512, 2048, 1, 9),
+    (64, 1024, 3, 1), (64, 1024, 3, 2), (64, 1024, 3, 4),
+])
+def test_2d_shapes(h, w, batch, levels):
+    check_2d(datagen.uniform((batch, h, w), seed=h * 7 + w + levels), levels)
+
+
+def test_c4_reduced():
+    """BASELINE configs[3] generator and size, 4 of the 256 images, L=5."""
+    check_2d(datagen.c4_batch(0, 4), 5)
+
+
+def test_c5_reduced():
+    """BASELINE configs[4] generator at 2048^2 with L=8 (two kernel passes, fp64 hand-off)."""
+    check_2d(datagen.c5_rows(0, 2048, size=2048), 8)
+
+
+# ------------------------------------------------------------------ API behaviour
+def test_plans_workspace_and_side_stream():
+    x = datagen.uniform((2, 256, 512), seed=3)
+    plan = fhwt.Plan2d(256, 512, 2, 8)
+    assert plan.workspace_bytes > 0
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    xd = dev(x)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        c = plan.analyze(xd, workspace=ws)
+        r = plan.synthesize(c, workspace=ws)
+    s.synchronize()
+    c1 = fhwt.analyze_2d(xd, 8)
+    assert torch.equal(c, c1)
+    assert_close(host(r), x, x, 2)
+    p1 = fhwt.Plan1d(1 << 14, 2, 14)
+    y = datagen.uniform((2, 1 << 14), seed=4)
+    cy = p1.analyze(dev(y))
+    assert torch.equal(cy, fhwt.analyze_1d(dev(y), 14))
+
+
+def test_deterministic_and_launch_count():
+    x = dev(datagen.uniform((3, 512, 512), seed=5))
+    n0 = fhwt.launch_count()
+    a = fhwt.analyze_2d(x, 7)
+    b = fhwt.analyze_2d(x, 7)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert fhwt.launch_count() - n0 == 4      # two passes per call
+
+
+def test_misaligned_and_cpu_inputs_fail_loudly():
+    buf = torch.zeros(1 + 64 * 64, device="cuda")
+    x = buf[1:].view(64, 64)                   # 4-byte aligned, not 16
+    with pytest.raises(fhwt.Misaligned):
+        fhwt.analyze_2d(x, 3)
+    c = fhwt.analyze_2d(x, 1)                  # single level: scalar path accepts it
+    assert_close(host(c), o.analyze_2d(np.zeros((64, 64)), 1), np.ones((64, 64)), 2)
+    with pytest.raises(fhwt.InvalidArgument):
+        fhwt.analyze_1d(torch.zeros(16), 2)
+    with pytest.raises(fhwt.InvalidArgument):
+        fhwt.analyze_1d(torch.zeros(16, device="cuda", dtype=torch.float64), 2)
+    with pytest.raises(fhwt.InsufficientLength):
+        fhwt.analyze_2d(torch.zeros(24, 24, device="cuda"), 4)
+
+
+def test_pack_ll_matches_band():
+    x = dev(datagen.uniform((3, 256, 128), seed=6))
+    c = fhwt.analyze_2d(x, 4)
+    ll = fhwt.pack_ll_2d(c, 4)
+    assert torch.equal(ll, c[:, :16, :8])
+
+
+def test_host_roundtrip_api():
+    x = torch.from_numpy(datagen.uniform((5, 128, 256), seed=7)).pin_memory()
+    coeffs = torch.empty_like(x).pin_memory()
+    r = fhwt.roundtrip_2d_host(x, 6, coeffs_out=coeffs, chunk=2)
+    assert_close(coeffs.double().numpy(), o.analyze_2d(x.numpy(), 6), x.numpy(), 2)
+    assert_close(r.double().numpy(), x.numpy(), x.numpy(), 2)
+    y = torch.from_numpy(datagen.uniform((7, 4096), seed=8)).pin_memory()
+    cy = torch.empty_like(y).pin_memory()
+    ry = fhwt.roundtrip_1d_host(y, 12, coeffs_out=cy, chunk=3)
+    assert_close(cy.double().numpy(), o.decompose_1d(y.numpy(), 12), y.numpy(), 1)
+    assert_close(ry.double().numpy(), y.numpy(), y.numpy(), 1)
