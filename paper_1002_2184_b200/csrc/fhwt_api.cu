@@ -324,7 +324,10 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     std::memset(&maps, 0, sizeof maps);
     int bw[6] = {0, 0, 0, 0, 0, 0};
     for (int j = 1; j <= ps.Lp; ++j) {
-      bw[j] = int(pitch4(p.TC >> j));
+      // TMA box starts must be 16-byte aligned: LH boxes start at col0 >> j (a multiple of 4),
+      // HL/HH boxes at (W >> g) + (col0 >> j), so they start hoff = (W >> g) & 3 columns early.
+      p.hoff[j] = int((W >> (ps.g0 + j)) & 3);
+      bw[j] = int(pitch4((p.TC >> j) + p.hoff[j]));
       p.box_pitch[j] = bw[j];
       FHWT_TRY(encode_2d(&maps.level[j], coeffs, false, W, B * H, W, bw[j], p.TR >> j));
     }

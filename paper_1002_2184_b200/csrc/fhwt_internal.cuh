@@ -52,6 +52,8 @@ struct Syn2dParams {
   uint32_t stage_bytes, bar_off;
   uint32_t box_off[6][3];  // per pass-level j (1..Lp): offsets of HL, LH, HH boxes; [0][0] = LL box
   int box_pitch[6];        // smem pitch (elements) of level-j boxes; [0] unused
+  int hoff[6];             // HL/HH boxes start hoff[j] columns left of the band block (TMA box
+                           // starts must be 16-B aligned; hoff = (W >> g) & 3)
   uint32_t p_off[2];
   uint32_t tx_bytes;       // bytes landed per stage
   int ll_from_ws;          // LL_{g0+Lp} comes from the workspace map (else from coeffs)

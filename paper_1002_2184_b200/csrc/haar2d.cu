@@ -47,9 +47,16 @@ __device__ __forceinline__ void load_row(const T* src, T (&v)[N]) {
     const float4 t = *reinterpret_cast<const float4*>(src);
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   } else if constexpr (sizeof(T) == 4 && N == 2) {
-    const float2 t = *reinterpret_cast<const float2*>(src);
-    v[0] = t.x; v[1] = t.y;
+    if ((reinterpret_cast<uintptr_t>(src) & 7) == 0) {
+      const float2 t = *reinterpret_cast<const float2*>(src);
+      v[0] = t.x; v[1] = t.y;
+    } else {  // HL/HH boxes shifted by an odd hoff
+      v[0] = src[0]; v[1] = src[1];
+    }
+  } else if constexpr (sizeof(T) == 4 && N == 1) {
+    v[0] = src[0];
   } else {
+    static_assert(sizeof(T) == 8 && N % 2 == 0, "double rows are loaded as double2");
 #pragma unroll
     for (int i = 0; i < N; i += 2) {
       const double2 t = *reinterpret_cast<const double2*>(src + i);
@@ -253,9 +260,9 @@ __device__ __forceinline__ void syn_tile(const Syn2dParams& p, unsigned char* st
   int llp = p.box_pitch[p.Lp];
   for (int j = p.Lp; j >= 1; --j) {
     const int R = p.TR >> j, C = p.TC >> j;
-    const float* hl = reinterpret_cast<const float*>(stage + p.box_off[j][0]);
+    const float* hl = reinterpret_cast<const float*>(stage + p.box_off[j][0]) + p.hoff[j];
     const float* lh = reinterpret_cast<const float*>(stage + p.box_off[j][1]);
-    const float* hh = reinterpret_cast<const float*>(stage + p.box_off[j][2]);
+    const float* hh = reinterpret_cast<const float*>(stage + p.box_off[j][2]) + p.hoff[j];
     float* dst = reinterpret_cast<float*>(smem + p.p_off[(j - 1) & 1]);
     if ((C & 1) == 0)
       syn_level<2>(p, ll, llp, hl, lh, hh, p.box_pitch[j], R, C, j, b, row0, col0, dst);
@@ -295,9 +302,10 @@ __global__ void __launch_bounds__(kThreads2d) syn2d_kernel(const __grid_constant
       const int g = p.g0 + j;
       const int64_t hg = p.H >> g, wg = p.W >> g;
       const int64_t br = b * p.H + (row0 >> j), bc = col0 >> j;
-      tma_load_2d(base + p.box_off[j][0], &maps.level[j], int(wg + bc), int(br), &bars[s], pol);
+      const int hc = int(wg + bc) - p.hoff[j];   // 16-B aligned box start
+      tma_load_2d(base + p.box_off[j][0], &maps.level[j], hc, int(br), &bars[s], pol);
       tma_load_2d(base + p.box_off[j][1], &maps.level[j], int(bc), int(br + hg), &bars[s], pol);
-      tma_load_2d(base + p.box_off[j][2], &maps.level[j], int(wg + bc), int(br + hg), &bars[s], pol);
+      tma_load_2d(base + p.box_off[j][2], &maps.level[j], hc, int(br + hg), &bars[s], pol);
     }
   };
   if (tid == 0) {
@@ -382,15 +390,25 @@ int grid_for(int64_t total, int threads) {
 
 }  // namespace
 
+// The dynamic-smem cap is raised to the device's opt-in maximum (not to `smem`), so a cached
+// occupancy answer for a small configuration never leaves the cap below a later, larger launch.
+static cudaError_t raise_smem_cap(const void* fn) {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  return e;
+}
+
 cudaError_t ana2d_occupancy(bool in_f64, size_t smem, int* blocks_per_sm) {
   const void* fn = in_f64 ? (const void*)ana2d_kernel<double> : (const void*)ana2d_kernel<float>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t e = raise_smem_cap(fn);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kThreads2d, smem);
 }
 
 cudaError_t syn2d_occupancy(size_t smem, int* blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute((const void*)syn2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t e = raise_smem_cap((const void*)syn2d_kernel);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (const void*)syn2d_kernel, kThreads2d, smem);
 }
