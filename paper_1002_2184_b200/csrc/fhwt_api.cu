@@ -119,7 +119,8 @@ fhwt_status encode_2d(CUtensorMap* m, const void* base, bool f64, int64_t cols, 
   return FHWT_OK;
 }
 
-// occupancy cache: (kind, smem) -> blocks per SM
+// occupancy cache: (kind, smem) -> blocks per SM.  kind = 0/1 ana2d f32/f64 generic,
+// 2 syn2d generic, 10 + LP ana2d fast, 20 + LP syn2d fast.
 fhwt_status occupancy(int kind, size_t smem, int* bps) {
   static std::mutex mu;
   static std::vector<std::pair<std::pair<int, size_t>, int>> cache;
@@ -134,7 +135,10 @@ fhwt_status occupancy(int kind, size_t smem, int* bps) {
         return FHWT_OK;
       }
   }
-  cudaError_t e = kind == 2 ? syn2d_occupancy(smem, bps) : ana2d_occupancy(kind == 1, smem, bps);
+  cudaError_t e = kind == 2    ? syn2d_occupancy(0, smem, bps)
+                  : kind >= 20 ? syn2d_occupancy(kind - 20, smem, bps)
+                  : kind >= 10 ? ana2d_occupancy(false, kind - 10, smem, bps)
+                               : ana2d_occupancy(kind == 1, 0, smem, bps);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
   if (*bps < 1) return fail(FHWT_ERR_CUDA, "kernel does not fit on an SM with %zu B shared memory", smem);
   std::lock_guard<std::mutex> lk(mu);
@@ -279,10 +283,12 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     off = align_up(off + pb[1], 128);
     p.bar_off = uint32_t(off);
     const size_t smem = off + 8 * size_t(p.stages);
+    // compile-time 32 x 256 variant: first pass, full tiles (then every band offset is 8-B aligned)
+    const int fast = (!in64 && ps.g0 == 0 && p.TR == 32 && p.TC == 256 && p.Win % 256 == 0) ? ps.Lp : 0;
     int bps = 0;
-    FHWT_TRY(occupancy(in64 ? 1 : 0, smem, &bps));
+    FHWT_TRY(occupancy(fast ? 10 + fast : (in64 ? 1 : 0), smem, &bps));
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
-    FHWT_CUDA(launch_ana2d(p, map, in64, int(grid), smem, s), "ana2d launch");
+    FHWT_CUDA(launch_ana2d(p, map, in64, fast, int(grid), smem, s), "ana2d launch");
   }
   return FHWT_OK;
 }
@@ -370,10 +376,12 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     off = align_up(off + pb[1], 128);
     p.bar_off = uint32_t(off);
     const size_t smem = off + 8 * size_t(p.stages);
+    bool fast = p.TR == 32 && p.TC == 256 && p.Win % 256 == 0 && p.out_pitch % 4 == 0;
+    for (int j = 1; j <= ps.Lp; ++j) fast = fast && p.hoff[j] == 0 && bw[j] == (256 >> j);
     int bps = 0;
-    FHWT_TRY(occupancy(2, smem, &bps));
+    FHWT_TRY(occupancy(fast ? 20 + ps.Lp : 2, smem, &bps));
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
-    FHWT_CUDA(launch_syn2d(p, maps, int(grid), smem, s), "syn2d launch");
+    FHWT_CUDA(launch_syn2d(p, maps, fast ? ps.Lp : 0, int(grid), smem, s), "syn2d launch");
   }
   return FHWT_OK;
 }

@@ -82,11 +82,13 @@ struct Haar1dParams {
 };
 
 // launchers (return cudaError_t of the launch)
-cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool in_f64, int grid,
+// fast_lp > 0 selects the compile-time 32 x 256 full-tile variant with that many levels
+cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool in_f64, int fast_lp, int grid,
                          size_t smem, cudaStream_t s);
-cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int grid, size_t smem, cudaStream_t s);
-cudaError_t ana2d_occupancy(bool in_f64, size_t smem, int* blocks_per_sm);
-cudaError_t syn2d_occupancy(size_t smem, int* blocks_per_sm);
+cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int fast_lp, int grid, size_t smem,
+                         cudaStream_t s);
+cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm);
+cudaError_t syn2d_occupancy(int fast_lp, size_t smem, int* blocks_per_sm);
 cudaError_t launch_ana1d(const Haar1dParams& p, bool in_f64, cudaStream_t s);
 cudaError_t launch_syn1d(const Haar1dParams& p, cudaStream_t s);
 cudaError_t launch_ana2d_l1_scalar(const float* d, float* c, int64_t h, int64_t w, int64_t batch, cudaStream_t s);

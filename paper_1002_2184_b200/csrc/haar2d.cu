@@ -13,41 +13,36 @@
 // Lp <= 5 levels of a tile run in shared memory / registers; every detail band is written once,
 // coalesced (float2 per thread, >= 32 B per row segment at the coarsest level), so HBM sees one
 // read and one write of each sample.  Levels g >= 4 are computed in fp64.
+#include <type_traits>
+
 #include "fhwt_internal.cuh"
 
 namespace fhwt {
 
 namespace {
 
-// band codes: 1 = HL (right half), 2 = LH (bottom half), 3 = HH (both)
-__device__ __forceinline__ float* band_row_ptr(const Ana2dParams& p, int64_t b, int g, int band, int64_t r) {
-  const int64_t hg = p.H >> g, wg = p.W >> g;
-  const int64_t row = ((band & 2) ? hg : 0) + r;
-  const int64_t col = (band & 1) ? wg : 0;
-  return p.out + (b * p.H + row) * p.W + col;
-}
-
-// stores V consecutive floats at p[0..V) of which the first `nvalid` are inside the band
-template <int V>
+// Stores V consecutive floats at ptr[0..V) of which the first `nvalid` lie inside the band.
+// ALIGNED: the caller guarantees an 8-B aligned ptr and a full vector (fast tiles).
+template <int V, bool ALIGNED>
 __device__ __forceinline__ void store_row(float* ptr, const float (&v)[V], int64_t nvalid) {
   if constexpr (V == 2) {
-    if (nvalid >= 2 && (reinterpret_cast<uintptr_t>(ptr) & 7) == 0) {
+    if (ALIGNED || (nvalid >= 2 && (reinterpret_cast<uintptr_t>(ptr) & 7) == 0)) {
       stg_stream2(ptr, make_float2(v[0], v[1]));
       return;
     }
   }
 #pragma unroll
   for (int i = 0; i < V; ++i)
-    if (i < nvalid) stg_stream1(ptr + i, v[i]);
+    if (ALIGNED || i < nvalid) stg_stream1(ptr + i, v[i]);
 }
 
-template <typename T, int N>
+template <typename T, int N, bool ALIGNED = false>
 __device__ __forceinline__ void load_row(const T* src, T (&v)[N]) {
   if constexpr (sizeof(T) == 4 && N == 4) {
     const float4 t = *reinterpret_cast<const float4*>(src);
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   } else if constexpr (sizeof(T) == 4 && N == 2) {
-    if ((reinterpret_cast<uintptr_t>(src) & 7) == 0) {
+    if (ALIGNED || (reinterpret_cast<uintptr_t>(src) & 7) == 0) {
       const float2 t = *reinterpret_cast<const float2*>(src);
       v[0] = t.x; v[1] = t.y;
     } else {  // HL/HH boxes shifted by an odd hoff
@@ -65,26 +60,49 @@ __device__ __forceinline__ void load_row(const T* src, T (&v)[N]) {
   }
 }
 
-// One analysis level of one tile.  Source: R x C region (smem, pitch C) of LL_{g-1} (or the input
-// tile); V output columns per thread unit.  Writes HL/LH/HH of global level g to HBM and LL_g to
-// smem (lldst, pitch C/2) or, on the pass's last level, to HBM (coeffs LL region or fp64 ws).
-template <typename TS, typename TC, int V>
-__device__ __forceinline__ void ana_level(const Ana2dParams& p, const TS* __restrict__ src, int R, int C, int j,
+// LL_g of a unit -> shared memory (vector store: lanes write consecutive 8/16-B words, no conflicts)
+template <typename TC, int V>
+__device__ __forceinline__ void store_ll_smem(TC* dst, const TC (&ll)[V]) {
+  if constexpr (V == 2 && sizeof(TC) == 4) {
+    *reinterpret_cast<float2*>(dst) = make_float2(ll[0], ll[1]);
+  } else if constexpr (V == 2) {
+    *reinterpret_cast<double2*>(dst) = make_double2(ll[0], ll[1]);
+  } else {
+    dst[0] = ll[0];
+  }
+}
+
+// One analysis level of one tile.  Source: the R x C region (smem, pitch C) of LL_{g-1} (or the
+// input tile); V output columns per thread unit (one 2 x 2V input block).  Writes HL/LH/HH of global
+// level g to HBM and LL_g to smem (lldst, pitch C/2) or, on the pass's last level, to HBM (coeffs
+// LL region or the fp64 workspace).
+// RC, CC: compile-time R, C (0 = runtime).  FAST: full, 8-B aligned tile (no masks, no checks).
+template <typename TS, typename TC, int V, int RC, int CC, bool FAST>
+__device__ __forceinline__ void ana_level(const Ana2dParams& p, const TS* __restrict__ src, int R_, int C_, int j,
                                           int64_t b, int64_t row0, int64_t col0, TC* __restrict__ lldst,
                                           bool last) {
-  const int g = p.g0 + j;
+  const int R = RC ? RC : R_;
+  const int C = CC ? CC : C_;
   const int OC = C >> 1;
   const int upr = OC / V;
   const int nunits = (R >> 1) * upr;
+  const int g = p.g0 + j;
+  const int64_t W = p.W;
+  const int64_t wg = W >> g, hgW = (p.H >> g) * W;
   const int64_t brow = row0 >> j, bcol = col0 >> j;
-  const int64_t nvalid_row = (p.Win >> j) - bcol;  // valid output cols of this tile at this level
+  float* const base = p.out + (b * p.H + brow) * W + bcol;  // (orow, oc) = (0, 0) of LL_g in this tile
+  const int64_t nvalid_row = FAST ? int64_t(OC) : (p.Win >> j) - bcol;
   const TC half = TC(0.5);
-  for (int u = threadIdx.x; u < nunits; u += blockDim.x) {
+  const int iters = (nunits + kThreads2d - 1) / kThreads2d;
+#pragma unroll
+  for (int it = 0; it < iters; ++it) {
+    const int u = int(threadIdx.x) + it * kThreads2d;
+    if ((nunits % kThreads2d) != 0 && u >= nunits) break;
     const int orow = u / upr;
     const int oc = (u - orow * upr) * V;
     TS t0[2 * V], t1[2 * V];
-    load_row<TS, 2 * V>(src + (2 * orow) * C + 2 * oc, t0);
-    load_row<TS, 2 * V>(src + (2 * orow + 1) * C + 2 * oc, t1);
+    load_row<TS, 2 * V, true>(src + (2 * orow) * C + 2 * oc, t0);
+    load_row<TS, 2 * V, true>(src + (2 * orow + 1) * C + 2 * oc, t1);
     float hl[V], lh[V], hh[V];
     TC ll[V];
 #pragma unroll
@@ -97,22 +115,21 @@ __device__ __forceinline__ void ana_level(const Ana2dParams& p, const TS* __rest
       hh[v] = float((d1 - d2) * half);
     }
     const int64_t nv = nvalid_row - oc;
-    const int64_t r = brow + orow, cc = bcol + oc;
-    store_row<V>(band_row_ptr(p, b, g, 1, r) + cc, hl, nv);
-    store_row<V>(band_row_ptr(p, b, g, 2, r) + cc, lh, nv);
-    store_row<V>(band_row_ptr(p, b, g, 3, r) + cc, hh, nv);
+    float* const pr = base + int64_t(orow) * W + oc;
+    store_row<V, FAST>(pr + wg, hl, nv);
+    store_row<V, FAST>(pr + hgW, lh, nv);
+    store_row<V, FAST>(pr + hgW + wg, hh, nv);
     if (!last) {
-#pragma unroll
-      for (int v = 0; v < V; ++v) lldst[orow * OC + oc + v] = ll[v];
+      store_ll_smem<TC, V>(lldst + orow * OC + oc, ll);
     } else if (p.final_pass) {
       float llf[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) llf[v] = float(ll[v]);
-      store_row<V>(p.out + (b * p.H + r) * p.W + cc, llf, nv);
+      store_row<V, FAST>(pr, llf, nv);
     } else {
-      // fp64 hand-off of LL_{g} to the next pass (pitch = padded Win >> Lp, see fhwt_api.cu)
+      // fp64 hand-off of LL_g to the next pass (pitch = padded Win >> Lp, see fhwt_api.cu)
       const int64_t wpitch = ((p.Win >> j) + 3) & ~int64_t(3);
-      double* w = p.ws_out + (b * (p.Hin >> j) + r) * wpitch + cc;
+      double* w = p.ws_out + (b * (p.Hin >> j) + brow + orow) * wpitch + bcol + oc;
 #pragma unroll
       for (int v = 0; v < V; ++v)
         if (v < nv) w[v] = double(ll[v]);
@@ -124,11 +141,12 @@ template <typename TS, typename TC>
 __device__ __forceinline__ void ana_level_v(const Ana2dParams& p, const TS* src, int R, int C, int j, int64_t b,
                                             int64_t row0, int64_t col0, TC* lldst, bool last) {
   if (((C >> 1) & 1) == 0)
-    ana_level<TS, TC, 2>(p, src, R, C, j, b, row0, col0, lldst, last);
+    ana_level<TS, TC, 2, 0, 0, false>(p, src, R, C, j, b, row0, col0, lldst, last);
   else
-    ana_level<TS, TC, 1>(p, src, R, C, j, b, row0, col0, lldst, last);
+    ana_level<TS, TC, 1, 0, 0, false>(p, src, R, C, j, b, row0, col0, lldst, last);
 }
 
+// Generic tile: any TR/TC, ragged right edge, runtime level count, fp32 or fp64 input.
 template <typename TIn>
 __device__ __forceinline__ void ana_tile(const Ana2dParams& p, const TIn* stage, unsigned char* smem, int64_t b,
                                          int64_t row0, int64_t col0) {
@@ -153,7 +171,25 @@ __device__ __forceinline__ void ana_tile(const Ana2dParams& p, const TIn* stage,
   }
 }
 
-template <typename TIn>
+// Fast tile: first pass (g0 = 0, fp32 input), 32 x 256 full tiles, LP levels known at compile
+// time, so every index is a shift/constant and levels g >= 4 are fp64 by construction.
+template <int J, int LP>
+__device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* src, unsigned char* smem, int64_t b,
+                                              int64_t row0, int64_t col0) {
+  constexpr int R = 32 >> (J - 1), C = 256 >> (J - 1);
+  constexpr bool src64 = J - 1 >= kFirstF64Level;
+  constexpr bool cmp64 = J >= kFirstF64Level;
+  using TS = typename std::conditional<src64, double, float>::type;
+  using TC = typename std::conditional<cmp64, double, float>::type;
+  ana_level<TS, TC, 2, R, C, true>(p, static_cast<const TS*>(src), R, C, J, b, row0, col0,
+                                   reinterpret_cast<TC*>(smem + p.p_off[J & 1]), J == LP);
+  if constexpr (J < LP) {
+    __syncthreads();
+    ana_fast_step<J + 1, LP>(p, smem + p.p_off[J & 1], smem, b, row0, col0);
+  }
+}
+
+template <typename TIn, int LPFAST>
 __global__ void __launch_bounds__(kThreads2d) ana2d_kernel(const __grid_constant__ Ana2dParams p,
                                                            const __grid_constant__ CUtensorMap in_map) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -185,7 +221,10 @@ __global__ void __launch_bounds__(kThreads2d) ana2d_kernel(const __grid_constant
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
     const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
-    ana_tile<TIn>(p, reinterpret_cast<const TIn*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC);
+    if constexpr (LPFAST > 0)
+      ana_fast_step<1, LPFAST>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC);
+    else
+      ana_tile<TIn>(p, reinterpret_cast<const TIn*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC);
     __syncthreads();  // stage s and the LL buffers are free again
     if (tid == 0) {
       const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
@@ -199,36 +238,44 @@ __global__ void __launch_bounds__(kThreads2d) ana2d_kernel(const __grid_constant
 }
 
 // ------------------------------------------------------------------------------------ synthesis
-template <int V>
+template <int V, bool ALIGNED>
 __device__ __forceinline__ void store_out_row(float* ptr, const float (&v)[2 * V], int64_t nvalid) {
   if constexpr (V == 2) {
-    if (nvalid >= 4 && (reinterpret_cast<uintptr_t>(ptr) & 15) == 0) {
+    if (ALIGNED || (nvalid >= 4 && (reinterpret_cast<uintptr_t>(ptr) & 15) == 0)) {
       stg_stream4(ptr, make_float4(v[0], v[1], v[2], v[3]));
       return;
     }
   }
 #pragma unroll
   for (int i = 0; i < 2 * V; ++i)
-    if (i < nvalid) stg_stream1(ptr + i, v[i]);
+    if (ALIGNED || i < nvalid) stg_stream1(ptr + i, v[i]);
 }
 
-// One synthesis level: coefficient block R x C (tile rows/cols at level j) -> LL_{j-1} (2R x 2C).
-template <int V>
+// One synthesis level: coefficient block R x C (tile rows/cols at level j) -> LL_{j-1} (2R x 2C),
+// into smem (to_smem, pitch 2C) or, for pass-level 1, into HBM.
+template <int V, int RC, int CC, bool FAST>
 __device__ __forceinline__ void syn_level(const Syn2dParams& p, const float* __restrict__ ll, int llp,
                                           const float* __restrict__ hl, const float* __restrict__ lh,
-                                          const float* __restrict__ hh, int bp, int R, int C, int j, int64_t b,
-                                          int64_t row0, int64_t col0, float* __restrict__ dst) {
+                                          const float* __restrict__ hh, int bp, int R_, int C_, bool to_smem,
+                                          int64_t b, int64_t row0, int64_t col0, float* __restrict__ dst) {
+  const int R = RC ? RC : R_;
+  const int C = CC ? CC : C_;
   const int upr = C / V;
   const int nunits = R * upr;
   const int OC = 2 * C;  // dst pitch when dst is smem
-  for (int u = threadIdx.x; u < nunits; u += blockDim.x) {
+  const int iters = (nunits + kThreads2d - 1) / kThreads2d;
+  float* const obase = p.out + (b * p.Hin + row0) * p.out_pitch + col0;
+#pragma unroll
+  for (int it = 0; it < iters; ++it) {
+    const int u = int(threadIdx.x) + it * kThreads2d;
+    if ((nunits % kThreads2d) != 0 && u >= nunits) break;
     const int r = u / upr;
     const int c = (u - r * upr) * V;
     float vll[V], vhl[V], vlh[V], vhh[V];
-    load_row<float, V>(ll + r * llp + c, vll);
-    load_row<float, V>(hl + r * bp + c, vhl);
-    load_row<float, V>(lh + r * bp + c, vlh);
-    load_row<float, V>(hh + r * bp + c, vhh);
+    load_row<float, V, FAST>(ll + r * llp + c, vll);
+    load_row<float, V, FAST>(hl + r * bp + c, vhl);
+    load_row<float, V, FAST>(lh + r * bp + c, vlh);
+    load_row<float, V, FAST>(hh + r * bp + c, vhh);
     float top[2 * V], bot[2 * V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -239,17 +286,20 @@ __device__ __forceinline__ void syn_level(const Syn2dParams& p, const float* __r
       bot[2 * v] = (s2 + t2) * 0.5f;
       bot[2 * v + 1] = (s2 - t2) * 0.5f;
     }
-    if (j > 1) {
-#pragma unroll
-      for (int k = 0; k < 2 * V; ++k) {
-        dst[(2 * r) * OC + 2 * c + k] = top[k];
-        dst[(2 * r + 1) * OC + 2 * c + k] = bot[k];
+    if (to_smem) {
+      float* d0 = dst + (2 * r) * OC + 2 * c;
+      if constexpr (V == 2) {  // 16-B vector stores: conflict-free across the warp
+        *reinterpret_cast<float4*>(d0) = make_float4(top[0], top[1], top[2], top[3]);
+        *reinterpret_cast<float4*>(d0 + OC) = make_float4(bot[0], bot[1], bot[2], bot[3]);
+      } else {
+        d0[0] = top[0]; d0[1] = top[1];
+        d0[OC] = bot[0]; d0[OC + 1] = bot[1];
       }
     } else {
-      const int64_t nv = p.Win - (col0 + 2 * c);
-      float* o = p.out + (b * p.Hin + row0 + 2 * r) * p.out_pitch + col0 + 2 * c;
-      store_out_row<V>(o, top, nv);
-      store_out_row<V>(o + p.out_pitch, bot, nv);
+      const int64_t nv = FAST ? int64_t(2 * V) : p.Win - (col0 + 2 * c);
+      float* o = obase + int64_t(2 * r) * p.out_pitch + 2 * c;
+      store_out_row<V, FAST>(o, top, nv);
+      store_out_row<V, FAST>(o + p.out_pitch, bot, nv);
     }
   }
 }
@@ -265,15 +315,32 @@ __device__ __forceinline__ void syn_tile(const Syn2dParams& p, unsigned char* st
     const float* hh = reinterpret_cast<const float*>(stage + p.box_off[j][2]) + p.hoff[j];
     float* dst = reinterpret_cast<float*>(smem + p.p_off[(j - 1) & 1]);
     if ((C & 1) == 0)
-      syn_level<2>(p, ll, llp, hl, lh, hh, p.box_pitch[j], R, C, j, b, row0, col0, dst);
+      syn_level<2, 0, 0, false>(p, ll, llp, hl, lh, hh, p.box_pitch[j], R, C, j > 1, b, row0, col0, dst);
     else
-      syn_level<1>(p, ll, llp, hl, lh, hh, p.box_pitch[j], R, C, j, b, row0, col0, dst);
+      syn_level<1, 0, 0, false>(p, ll, llp, hl, lh, hh, p.box_pitch[j], R, C, j > 1, b, row0, col0, dst);
     if (j > 1) __syncthreads();
     ll = dst;
     llp = 2 * C;
   }
 }
 
+// Fast tile: 32 x 256 full tiles, hoff = 0, LP known at compile time (box pitch = 256 >> j).
+template <int J>
+__device__ __forceinline__ void syn_fast_step(const Syn2dParams& p, unsigned char* stage, unsigned char* smem,
+                                              const float* ll, int64_t b, int64_t row0, int64_t col0) {
+  constexpr int R = 32 >> J, C = 256 >> J;
+  const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]);
+  const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]);
+  const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]);
+  float* dst = reinterpret_cast<float*>(smem + p.p_off[(J - 1) & 1]);
+  syn_level<2, R, C, true>(p, ll, C, hl, lh, hh, C, R, C, J > 1, b, row0, col0, dst);
+  if constexpr (J > 1) {
+    __syncthreads();
+    syn_fast_step<J - 1>(p, stage, smem, dst, b, row0, col0);
+  }
+}
+
+template <int LPFAST>
 __global__ void __launch_bounds__(kThreads2d) syn2d_kernel(const __grid_constant__ Syn2dParams p,
                                                            const __grid_constant__ TmaMaps2d maps) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -322,7 +389,12 @@ __global__ void __launch_bounds__(kThreads2d) syn2d_kernel(const __grid_constant
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
     const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
-    syn_tile(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC);
+    unsigned char* stage = smem + s * p.stage_bytes;
+    if constexpr (LPFAST > 0)
+      syn_fast_step<LPFAST>(p, stage, smem, reinterpret_cast<const float*>(stage + p.box_off[0][0]), b, row0,
+                            ct * p.TC);
+    else
+      syn_tile(p, stage, smem, b, row0, ct * p.TC);
     __syncthreads();
     if (tid == 0) {
       const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
@@ -400,33 +472,55 @@ static cudaError_t raise_smem_cap(const void* fn) {
   return e;
 }
 
-cudaError_t ana2d_occupancy(bool in_f64, size_t smem, int* blocks_per_sm) {
-  const void* fn = in_f64 ? (const void*)ana2d_kernel<double> : (const void*)ana2d_kernel<float>;
+static const void* ana2d_fn(bool in_f64, int fast_lp) {
+  if (in_f64) return (const void*)ana2d_kernel<double, 0>;
+  switch (fast_lp) {
+    case 1: return (const void*)ana2d_kernel<float, 1>;
+    case 2: return (const void*)ana2d_kernel<float, 2>;
+    case 3: return (const void*)ana2d_kernel<float, 3>;
+    case 4: return (const void*)ana2d_kernel<float, 4>;
+    case 5: return (const void*)ana2d_kernel<float, 5>;
+    default: return (const void*)ana2d_kernel<float, 0>;
+  }
+}
+
+static const void* syn2d_fn(int fast_lp) {
+  switch (fast_lp) {
+    case 1: return (const void*)syn2d_kernel<1>;
+    case 2: return (const void*)syn2d_kernel<2>;
+    case 3: return (const void*)syn2d_kernel<3>;
+    case 4: return (const void*)syn2d_kernel<4>;
+    case 5: return (const void*)syn2d_kernel<5>;
+    default: return (const void*)syn2d_kernel<0>;
+  }
+}
+
+cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm) {
+  const void* fn = ana2d_fn(in_f64, fast_lp);
   cudaError_t e = raise_smem_cap(fn);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kThreads2d, smem);
 }
 
-cudaError_t syn2d_occupancy(size_t smem, int* blocks_per_sm) {
-  cudaError_t e = raise_smem_cap((const void*)syn2d_kernel);
+cudaError_t syn2d_occupancy(int fast_lp, size_t smem, int* blocks_per_sm) {
+  const void* fn = syn2d_fn(fast_lp);
+  cudaError_t e = raise_smem_cap(fn);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (const void*)syn2d_kernel, kThreads2d, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kThreads2d, smem);
 }
 
-cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool in_f64, int grid, size_t smem,
+cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool in_f64, int fast_lp, int grid,
+                         size_t smem, cudaStream_t s) {
+  count_launch();
+  void* args[] = {const_cast<Ana2dParams*>(&p), const_cast<CUtensorMap*>(&in_map)};
+  return cudaLaunchKernel(ana2d_fn(in_f64, fast_lp), dim3(grid), dim3(kThreads2d), args, smem, s);
+}
+
+cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int fast_lp, int grid, size_t smem,
                          cudaStream_t s) {
   count_launch();
-  if (in_f64)
-    ana2d_kernel<double><<<grid, kThreads2d, smem, s>>>(p, in_map);
-  else
-    ana2d_kernel<float><<<grid, kThreads2d, smem, s>>>(p, in_map);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int grid, size_t smem, cudaStream_t s) {
-  count_launch();
-  syn2d_kernel<<<grid, kThreads2d, smem, s>>>(p, maps);
-  return cudaGetLastError();
+  void* args[] = {const_cast<Syn2dParams*>(&p), const_cast<TmaMaps2d*>(&maps)};
+  return cudaLaunchKernel(syn2d_fn(fast_lp), dim3(grid), dim3(kThreads2d), args, smem, s);
 }
 
 cudaError_t launch_ana2d_l1_scalar(const float* d, float* c, int64_t h, int64_t w, int64_t batch, cudaStream_t s) {
