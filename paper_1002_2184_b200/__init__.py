@@ -22,7 +22,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libfhwt.so")
+lib_path = os.environ.get("FHWT_LIB") or os.path.join(_HERE, "libfhwt.so")   # FHWT_LIB: tuning sweeps only
 
 
 class FhwtError(RuntimeError):

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -119,14 +120,21 @@ fhwt_status encode_2d(CUtensorMap* m, const void* base, bool f64, int64_t cols, 
   return FHWT_OK;
 }
 
+// Tuning knobs (defaults chosen by measurement); env overrides exist only
+// for the tile/stage sweeps in tools/.
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
 // occupancy cache: (kind, smem) -> blocks per SM.  kind = 0/1 ana2d f32/f64 generic,
-// 2 syn2d generic, 10 + LP ana2d fast, 20 + LP syn2d fast.
+// 2 syn2d generic, 1e6 + fast_lp ana2d fast, 2e6 + fast_lp syn2d fast.
 fhwt_status occupancy(int kind, size_t smem, int* bps) {
   static std::mutex mu;
-  static std::vector<std::pair<std::pair<int, size_t>, int>> cache;
+  static std::vector<std::pair<std::pair<int64_t, size_t>, int>> cache;
   int dev = 0;
   FHWT_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
-  const int key = kind * 64 + dev;
+  const int64_t key = int64_t(kind) * 64 + dev;
   {
     std::lock_guard<std::mutex> lk(mu);
     for (auto& e : cache)
@@ -135,10 +143,10 @@ fhwt_status occupancy(int kind, size_t smem, int* bps) {
         return FHWT_OK;
       }
   }
-  cudaError_t e = kind == 2    ? syn2d_occupancy(0, smem, bps)
-                  : kind >= 20 ? syn2d_occupancy(kind - 20, smem, bps)
-                  : kind >= 10 ? ana2d_occupancy(false, kind - 10, smem, bps)
-                               : ana2d_occupancy(kind == 1, 0, smem, bps);
+  cudaError_t e = kind == 2         ? syn2d_occupancy(0, smem, bps)
+                  : kind >= 2000000 ? syn2d_occupancy(kind - 2000000, smem, bps)
+                  : kind >= 1000000 ? ana2d_occupancy(false, kind - 1000000, smem, bps)
+                                    : ana2d_occupancy(kind == 1, 0, smem, bps);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
   if (*bps < 1) return fail(FHWT_ERR_CUDA, "kernel does not fit on an SM with %zu B shared memory", smem);
   std::lock_guard<std::mutex> lk(mu);
@@ -257,7 +265,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     p.Lp = ps.Lp;
     p.g0 = ps.g0;
     p.TR = choose_tr(p.Hin, ps.Lp);
-    p.TC = int(std::min<int64_t>(in64 ? 128 : 256, p.Win));
+    p.TC = int(std::min<int64_t>(in64 ? 128 : env_int("FHWT_ANA_TC", 256), p.Win));
     p.tiles_r = p.Hin / p.TR;
     p.tiles_c = (p.Win + p.TC - 1) / p.TC;
     p.ntiles = B * p.tiles_r * p.tiles_c;
@@ -266,10 +274,15 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     const void* in = k == 0 ? static_cast<const void*>(d) : static_cast<const void*>(ws + pl->ws_off[k - 1]);
     const int64_t in_pitch = k == 0 ? W : pitch4(p.Win);
     CUtensorMap map;
-    FHWT_TRY(encode_2d(&map, in, in64, p.Win, B * p.Hin, in_pitch, p.TC, p.TR));
+    // One-row boxes when a row is >= 1 KB (and a 128-B multiple): the kernel then issues TR of
+    // them per tile from one thread.  B200 (tools/membench.py, tools/sweep_2d.py): 32 one-row
+    // 1-KB boxes stream at 6.9 TB/s where one 32-row box stops at 6.1 TB/s; smaller row boxes
+    // are request-bound and slower than multi-row boxes.
+    p.row_boxes = size_t(p.TC) * (in64 ? 8 : 4) >= 1024 && (size_t(p.TC) * (in64 ? 8 : 4)) % 128 == 0;
+    FHWT_TRY(encode_2d(&map, in, in64, p.Win, B * p.Hin, in_pitch, p.TC, p.row_boxes ? 1 : p.TR));
     // shared memory layout: stages | P[0] | P[1] | barriers
     const size_t es = in64 ? 8 : 4;
-    p.stages = in64 ? 2 : 3;
+    p.stages = in64 ? 2 : env_int("FHWT_ANA_STAGES", 2);
     p.stage_bytes = uint32_t(align_up(size_t(p.TR) * p.TC * es, 1024));
     size_t pb[2] = {0, 0};
     for (int j = 1; j < ps.Lp; ++j) {
@@ -284,9 +297,10 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     p.bar_off = uint32_t(off);
     const size_t smem = off + 8 * size_t(p.stages);
     // compile-time 32 x 256 variant: first pass, full tiles (then every band offset is 8-B aligned)
-    const int fast = (!in64 && ps.g0 == 0 && p.TR == 32 && p.TC == 256 && p.Win % 256 == 0) ? ps.Lp : 0;
+    const bool fast_ok = !in64 && ps.g0 == 0 && p.TR == 32 && (p.TC == 256 || p.TC == 128) && p.Win % p.TC == 0;
+    const int fast = fast_ok ? (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
-    FHWT_TRY(occupancy(fast ? 10 + fast : (in64 ? 1 : 0), smem, &bps));
+    FHWT_TRY(occupancy(fast ? 1000000 + fast : (in64 ? 1 : 0), smem, &bps));
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
     FHWT_CUDA(launch_ana2d(p, map, in64, fast, int(grid), smem, s), "ana2d launch");
   }
@@ -315,7 +329,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     p.Lp = ps.Lp;
     p.g0 = ps.g0;
     p.TR = choose_tr(p.Hin, ps.Lp);
-    p.TC = int(std::min<int64_t>(256, p.Win));
+    p.TC = int(std::min<int64_t>(env_int("FHWT_SYN_TC", 256), p.Win));
     p.tiles_r = p.Hin / p.TR;
     p.tiles_c = (p.Win + p.TC - 1) / p.TC;
     p.ntiles = B * p.tiles_r * p.tiles_c;
@@ -326,6 +340,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       p.out = reinterpret_cast<float*>(ws + pl->ws_off[kk - 1]);
       p.out_pitch = pitch4(p.Win);
     }
+    p.coeffs = coeffs;
     TmaMaps2d maps;
     std::memset(&maps, 0, sizeof maps);
     int bw[6] = {0, 0, 0, 0, 0, 0};
@@ -335,35 +350,48 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       p.hoff[j] = int((W >> (ps.g0 + j)) & 3);
       bw[j] = int(pitch4((p.TC >> j) + p.hoff[j]));
       p.box_pitch[j] = bw[j];
-      FHWT_TRY(encode_2d(&maps.level[j], coeffs, false, W, B * H, W, bw[j], p.TR >> j));
+      p.row_boxes[j] = bw[j] * 4 >= 1024 && (bw[j] * 4) % 128 == 0;   // see the analysis note
+      FHWT_TRY(encode_2d(&maps.level[j], coeffs, false, W, B * H, W, bw[j], p.row_boxes[j] ? 1 : p.TR >> j));
     }
     if (kk + 1 == np) {
       p.ll_from_ws = 0;
       maps.ll = maps.level[ps.Lp];
     } else {
       p.ll_from_ws = 1;
+      p.ll_ws = reinterpret_cast<const float*>(ws + pl->ws_off[kk]);
       const int64_t wl = p.Win >> ps.Lp, hl = p.Hin >> ps.Lp;
-      FHWT_TRY(encode_2d(&maps.ll, ws + pl->ws_off[kk], false, wl, B * hl, pitch4(wl), bw[ps.Lp], p.TR >> ps.Lp));
+      FHWT_TRY(encode_2d(&maps.ll, ws + pl->ws_off[kk], false, wl, B * hl, pitch4(wl), bw[ps.Lp],
+                         p.row_boxes[ps.Lp] ? 1 : p.TR >> ps.Lp));
     }
-    // stage layout: LL box, then per level j three boxes
+    // Fast variant: 32 x TC full aligned tiles.
+    bool fast = p.TR == 32 && (p.TC == 256 || p.TC == 128) && p.Win % p.TC == 0 && p.out_pitch % 4 == 0 &&
+                (W >> (ps.g0 + 1)) % 2 == 0;
+    for (int j = 1; j <= ps.Lp; ++j) fast = fast && p.hoff[j] == 0 && bw[j] == (p.TC >> j);
+    // load path of the fast variant: 0 TMA boxes, 1 LDG level-1 bands, 2 cp.async (LDGSTS) for all
+    // boxes.  Measured on B200 (tools/sweep_syn.py): 2 = 6.10 TB/s, 0 = 5.86, 1 = 5.19.
+    const int mode = fast ? env_int("FHWT_SYN_MODE", 2) : 0;
+    p.l1_ldg = mode == 1;
+    // stage layout: LL box, then per level j three boxes (128-B aligned: TMA destinations need it;
+    // with cp.async a 16-B packing would admit a 3rd CTA/SM, which measured slower: 5.54 vs 6.10 TB/s)
+    const size_t balign = 128;
     size_t off = 0, tx = 0;
     {
       const size_t bytes = size_t(p.TR >> ps.Lp) * bw[ps.Lp] * 4;
       p.box_off[0][0] = uint32_t(off);
-      off = align_up(off + bytes, 128);
+      off = align_up(off + bytes, balign);
       tx += bytes;
     }
-    for (int j = 1; j <= ps.Lp; ++j) {
+    for (int j = p.l1_ldg ? 2 : 1; j <= ps.Lp; ++j) {
       const size_t bytes = size_t(p.TR >> j) * bw[j] * 4;
       for (int q = 0; q < 3; ++q) {
         p.box_off[j][q] = uint32_t(off);
-        off = align_up(off + bytes, 128);
+        off = align_up(off + bytes, balign);
         tx += bytes;
       }
     }
     p.tx_bytes = uint32_t(tx);
     p.stage_bytes = uint32_t(align_up(off, 1024));
-    p.stages = 3;
+    p.stages = env_int("FHWT_SYN_STAGES", 2);   // 2 stages -> 3 CTAs/SM (measured best, tools/sweep_2d.py)
     size_t pb[2] = {0, 0};
     for (int j = 2; j <= ps.Lp; ++j) {
       const int jj = j - 1;
@@ -376,12 +404,11 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     off = align_up(off + pb[1], 128);
     p.bar_off = uint32_t(off);
     const size_t smem = off + 8 * size_t(p.stages);
-    bool fast = p.TR == 32 && p.TC == 256 && p.Win % 256 == 0 && p.out_pitch % 4 == 0;
-    for (int j = 1; j <= ps.Lp; ++j) fast = fast && p.hoff[j] == 0 && bw[j] == (256 >> j);
+    const int fast_lp = fast ? (mode << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
-    FHWT_TRY(occupancy(fast ? 20 + ps.Lp : 2, smem, &bps));
+    FHWT_TRY(occupancy(fast ? 2000000 + fast_lp : 2, smem, &bps));
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
-    FHWT_CUDA(launch_syn2d(p, maps, fast ? ps.Lp : 0, int(grid), smem, s), "syn2d launch");
+    FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
   }
   return FHWT_OK;
 }

@@ -37,9 +37,15 @@ struct Ana2dParams {
   int stages;
   uint32_t stage_bytes, p_off[2], bar_off;
   int final_pass;
+  int row_boxes;         // 1: the map's box is one row and TR boxes are issued per tile (rows of
+                         // 128-B multiples; TMA smem destinations must be 128-B aligned); 0: one TR-row box
 };
 
 struct Syn2dParams {
+  const float* coeffs;   // Mallat coefficients (pitch W): level-1 bands are read from here by LDG
+                         // in the fast variant (l1_ldg), everything else arrives by TMA
+  int l1_ldg;
+  const float* ll_ws;    // LL_{g0+Lp} source in the workspace (cp.async variant; pitch pitch4(Win >> Lp))
   float* out;            // d_R (final pass, pitch W) or the LL_{g0} hand-off (pitch Win)
   int64_t out_pitch;
   int64_t H, W;          // full image dims (coefficient layout)
@@ -57,6 +63,7 @@ struct Syn2dParams {
   uint32_t p_off[2];
   uint32_t tx_bytes;       // bytes landed per stage
   int ll_from_ws;          // LL_{g0+Lp} comes from the workspace map (else from coeffs)
+  int row_boxes[6];        // per pass-level j: one-row boxes (1) or one (TR >> j)-row box (0); see Ana2dParams
 };
 
 struct TmaMaps2d {
@@ -82,7 +89,7 @@ struct Haar1dParams {
 };
 
 // launchers (return cudaError_t of the launch)
-// fast_lp > 0 selects the compile-time 32 x 256 full-tile variant with that many levels
+// fast_lp > 0 selects the compile-time full-tile variant: fast_lp = (tile cols << 4) | levels
 cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool in_f64, int fast_lp, int grid,
                          size_t smem, cudaStream_t s);
 cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int fast_lp, int grid, size_t smem,
@@ -145,6 +152,14 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+
+// Ampere-style async copy (LDGSTS): 16 B global -> shared, completion tracked per thread by groups.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;

@@ -17,6 +17,14 @@
 
 #include "fhwt_internal.cuh"
 
+// Minimum resident CTAs per SM the 2-D kernels are compiled for (register cap 65536 / (256 * n)).
+#ifndef FHWT_MINB_ANA
+#define FHWT_MINB_ANA 2
+#endif
+#ifndef FHWT_MINB_SYN
+#define FHWT_MINB_SYN 3   // measured: synthesis 6.10 TB/s at 3 CTAs/SM vs 6.02 at 2; analysis best at 2
+#endif
+
 namespace fhwt {
 
 namespace {
@@ -171,12 +179,45 @@ __device__ __forceinline__ void ana_tile(const Ana2dParams& p, const TIn* stage,
   }
 }
 
-// Fast tile: first pass (g0 = 0, fp32 input), 32 x 256 full tiles, LP levels known at compile
+// Loads input tile `t` into a stage: TR one-row TMA boxes issued by the 32 lanes of warp 0.
+// (Measured on B200, tools/membench: 32 one-row boxes stream at 6.9 TB/s where one 32-row box
+// of the same bytes stops at 6.1 TB/s.)  Must be called by all of warp 0.
+__device__ __forceinline__ void ana_issue_tile(const Ana2dParams& p, const CUtensorMap* map, unsigned char* dst,
+                                               uint64_t* bar, int64_t t, uint32_t bytes, uint32_t row_bytes,
+                                               uint64_t pol) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+  if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+  __syncwarp();
+  if (p.row_boxes) {
+    if (lane == 0)
+      for (int r = 0; r < p.TR; ++r)
+        tma_load_2d(dst + r * row_bytes, map, int(ct * p.TC), int(rt * p.TR + r), bar, pol);
+  } else if (lane == 0) {
+    tma_load_2d(dst, map, int(ct * p.TC), int(rt * p.TR), bar, pol);
+  }
+}
+
+// Re-arms stage s of the TMA ring with the CTA's tile `next` (warp 0; no-op past the end).
+struct Refill {
+  const Ana2dParams* p;
+  const CUtensorMap* map;
+  unsigned char* dst;
+  uint64_t* bar;
+  int64_t next;
+  uint32_t bytes, row_bytes;
+  uint64_t pol;
+  __device__ __forceinline__ void operator()() const {
+    if (threadIdx.x < 32 && next < p->ntiles) ana_issue_tile(*p, map, dst, bar, next, bytes, row_bytes, pol);
+  }
+};
+
+// Fast tile: first pass (g0 = 0, fp32 input), 32 x TCF full tiles, LP levels known at compile
 // time, so every index is a shift/constant and levels g >= 4 are fp64 by construction.
-template <int J, int LP>
+template <int J, int LP, int TCF>
 __device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* src, unsigned char* smem, int64_t b,
-                                              int64_t row0, int64_t col0) {
-  constexpr int R = 32 >> (J - 1), C = 256 >> (J - 1);
+                                              int64_t row0, int64_t col0, const Refill& refill) {
+  constexpr int R = 32 >> (J - 1), C = TCF >> (J - 1);
   constexpr bool src64 = J - 1 >= kFirstF64Level;
   constexpr bool cmp64 = J >= kFirstF64Level;
   using TS = typename std::conditional<src64, double, float>::type;
@@ -185,12 +226,13 @@ __device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* 
                                    reinterpret_cast<TC*>(smem + p.p_off[J & 1]), J == LP);
   if constexpr (J < LP) {
     __syncthreads();
-    ana_fast_step<J + 1, LP>(p, smem + p.p_off[J & 1], smem, b, row0, col0);
+    if constexpr (J == 1) refill();   // level 1 was the last reader of the TMA stage
+    ana_fast_step<J + 1, LP, TCF>(p, smem + p.p_off[J & 1], smem, b, row0, col0, refill);
   }
 }
 
-template <typename TIn, int LPFAST>
-__global__ void __launch_bounds__(kThreads2d) ana2d_kernel(const __grid_constant__ Ana2dParams p,
+template <typename TIn, int LPFAST, int TCF>
+__global__ void __launch_bounds__(kThreads2d, FHWT_MINB_ANA) ana2d_kernel(const __grid_constant__ Ana2dParams p,
                                                            const __grid_constant__ CUtensorMap in_map) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
@@ -201,17 +243,15 @@ __global__ void __launch_bounds__(kThreads2d) ana2d_kernel(const __grid_constant
     fence_mbar_init();
   }
   __syncthreads();
-  const uint32_t tile_bytes = uint32_t(p.TR) * uint32_t(p.TC) * uint32_t(sizeof(TIn));
+  const uint32_t row_bytes = uint32_t(p.TC) * uint32_t(sizeof(TIn));
+  const uint32_t tile_bytes = uint32_t(p.TR) * row_bytes;
   uint64_t pol = 0;
-  if (tid == 0) {
+  if (tid < 32) {
     pol = policy_evict_first();
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
-      if (t < p.ntiles) {
-        const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
-        mbar_arrive_expect_tx(&bars[s], tile_bytes);
-        tma_load_2d(smem + s * p.stage_bytes, &in_map, int(ct * p.TC), int(rt * p.TR), &bars[s], pol);
-      }
+      if (t < p.ntiles)
+        ana_issue_tile(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, tile_bytes, row_bytes, pol);
     }
   }
   int it = 0;
@@ -221,18 +261,16 @@ __global__ void __launch_bounds__(kThreads2d) ana2d_kernel(const __grid_constant
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
     const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
-    if constexpr (LPFAST > 0)
-      ana_fast_step<1, LPFAST>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC);
-    else
+    const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
+                        tile_bytes, row_bytes, pol};
+    if constexpr (LPFAST > 0) {
+      ana_fast_step<1, LPFAST, TCF>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC, refill);
+      __syncthreads();  // LL buffers free again
+      if constexpr (LPFAST == 1) refill();
+    } else {
       ana_tile<TIn>(p, reinterpret_cast<const TIn*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC);
-    __syncthreads();  // stage s and the LL buffers are free again
-    if (tid == 0) {
-      const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
-      if (nt < p.ntiles) {
-        const int64_t nrt = nt / p.tiles_c, nct = nt - nrt * p.tiles_c;
-        mbar_arrive_expect_tx(&bars[s], tile_bytes);
-        tma_load_2d(smem + s * p.stage_bytes, &in_map, int(nct * p.TC), int(nrt * p.TR), &bars[s], pol);
-      }
+      __syncthreads();  // stage s and the LL buffers are free again
+      refill();
     }
   }
 }
@@ -324,11 +362,27 @@ __device__ __forceinline__ void syn_tile(const Syn2dParams& p, unsigned char* st
   }
 }
 
-// Fast tile: 32 x 256 full tiles, hoff = 0, LP known at compile time (box pitch = 256 >> j).
-template <int J>
+// Fast tile: 32 x TCF full tiles, hoff = 0, LP known at compile time (box pitch = TCF >> j).
+// Coarse levels J..2 from the TMA stage; leaves LL_1 in P[1].
+template <int J, int TCF>
+__device__ __forceinline__ void syn_fast_coarse(const Syn2dParams& p, unsigned char* stage, unsigned char* smem,
+                                                const float* ll, int64_t b, int64_t row0, int64_t col0) {
+  static_assert(J >= 2, "level 1 runs from registers");
+  constexpr int R = 32 >> J, C = TCF >> J;
+  const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]);
+  const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]);
+  const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]);
+  float* dst = reinterpret_cast<float*>(smem + p.p_off[(J - 1) & 1]);
+  syn_level<2, R, C, true>(p, ll, C, hl, lh, hh, C, R, C, true, b, row0, col0, dst);
+  __syncthreads();
+  if constexpr (J > 2) syn_fast_coarse<J - 1, TCF>(p, stage, smem, dst, b, row0, col0);
+}
+
+// All levels J..1 from the TMA stage (level 1 writes the output tile).
+template <int J, int TCF>
 __device__ __forceinline__ void syn_fast_step(const Syn2dParams& p, unsigned char* stage, unsigned char* smem,
                                               const float* ll, int64_t b, int64_t row0, int64_t col0) {
-  constexpr int R = 32 >> J, C = 256 >> J;
+  constexpr int R = 32 >> J, C = TCF >> J;
   const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]);
   const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]);
   const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]);
@@ -336,12 +390,125 @@ __device__ __forceinline__ void syn_fast_step(const Syn2dParams& p, unsigned cha
   syn_level<2, R, C, true>(p, ll, C, hl, lh, hh, C, R, C, J > 1, b, row0, col0, dst);
   if constexpr (J > 1) {
     __syncthreads();
-    syn_fast_step<J - 1>(p, stage, smem, dst, b, row0, col0);
+    syn_fast_step<J - 1, TCF>(p, stage, smem, dst, b, row0, col0);
   }
 }
 
-template <int LPFAST>
-__global__ void __launch_bounds__(kThreads2d) syn2d_kernel(const __grid_constant__ Syn2dParams p,
+// cp.async variant: every thread copies 16-B chunks of tile t (all boxes of all levels, same smem
+// layout as the TMA boxes) and commits one group.  Chunk q = tid + 256 i enumerates, level by
+// level, the rows of HL, LH, HH (and the LL block of level LP).
+template <int LP, int TCF>
+__device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned char* base, int64_t t) {
+  const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+  const int64_t b = rt / p.tiles_r;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = ct * p.TC;
+  int q0 = 0;
+#pragma unroll
+  for (int j = 1; j <= LP; ++j) {
+    const int rows = 32 >> j, cpr = (TCF >> j) / 4, nb = rows * cpr;   // chunks per band block
+    const int g = p.g0 + j;
+    const int64_t hg = p.H >> g, wg = p.W >> g;
+    const float* gb = p.coeffs + (b * p.H + (row0 >> j)) * p.W + (col0 >> j);
+#pragma unroll
+    for (int q = int(threadIdx.x); q < 3 * nb; q += kThreads2d) {
+      const int band = q / nb, rem = q - band * nb, r = rem / cpr, c = (rem - r * cpr) * 4;
+      // band 0 = HL (right half), 1 = LH (bottom half), 2 = HH (both)
+      const float* src = gb + (band >= 1 ? hg * p.W : 0) + (band != 1 ? wg : 0) + int64_t(r) * p.W + c;
+      cp_async16(base + p.box_off[j][band] + (r * (TCF >> j) + c) * 4, src);
+    }
+    q0 += 3 * nb;
+  }
+  {
+    const int rows = 32 >> LP, cpr = (TCF >> LP) / 4;
+    const float* lsrc;
+    int64_t lpitch;
+    if (p.ll_from_ws) {
+      lpitch = (((p.Win >> LP) + 3) & ~int64_t(3));
+      lsrc = p.ll_ws + (b * (p.Hin >> LP) + (row0 >> LP)) * lpitch + (col0 >> LP);
+    } else {
+      lpitch = p.W;
+      lsrc = p.coeffs + (b * p.H + (row0 >> LP)) * p.W + (col0 >> LP);
+    }
+    for (int q = int(threadIdx.x); q < rows * cpr; q += kThreads2d) {
+      const int r = q / cpr, c = (q - r * cpr) * 4;
+      cp_async16(base + p.box_off[0][0] + (r * (TCF >> LP) + c) * 4, lsrc + int64_t(r) * lpitch + c);
+    }
+  }
+  cp_async_commit();
+}
+
+// Level-1 band values of one tile, held in registers (fast synthesis): unit k of this thread is
+// row r = u / UPR, cols 2c, 2c+1 with u = tid + 256 k (same mapping as syn_level<2>).
+template <int TCF>
+struct L1Bands {
+  static constexpr int C1 = TCF / 2, UPR = C1 / 2, N = 16 * UPR / kThreads2d;
+  float2 hl[N], lh[N], hh[N];
+  __device__ __forceinline__ void load(const Syn2dParams& p, int64_t t) {
+    const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+    const int64_t b = rt / p.tiles_r;
+    const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = ct * p.TC;
+    const int g = p.g0 + 1;
+    const int64_t hgW = (p.H >> g) * p.W, wg = p.W >> g;
+    const float* base = p.coeffs + (b * p.H + (row0 >> 1)) * p.W + (col0 >> 1);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int u = int(threadIdx.x) + k * kThreads2d;
+      const int r = u / UPR, c = (u % UPR) * 2;
+      const float* q = base + int64_t(r) * p.W + c;
+      hl[k] = ldg_stream2(q + wg);
+      lh[k] = ldg_stream2(q + hgW);
+      hh[k] = ldg_stream2(q + hgW + wg);
+    }
+  }
+};
+
+// Issues the TMA loads of tile t into one stage (LL box + 3 band boxes per level; level 1 is
+// skipped when it is read by LDG).  Called by all of warp 0; lane 0 issues.
+__device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* base,
+                                               uint64_t* bar, int64_t t, uint64_t pol) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+  const int64_t b = rt / p.tiles_r;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = ct * p.TC;
+  if (lane == 0) mbar_arrive_expect_tx(bar, p.tx_bytes);
+  __syncwarp();
+  if (lane != 0) return;
+  const int L = p.Lp;
+  const int64_t llrow = p.ll_from_ws ? b * (p.Hin >> L) + (row0 >> L) : b * p.H + (row0 >> L);
+  const int llrows = p.row_boxes[L] ? (p.TR >> L) : 1;
+  for (int r = 0; r < llrows; ++r)
+    tma_load_2d(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int(col0 >> L), int(llrow + r), bar, pol);
+  for (int j = L; j >= (p.l1_ldg ? 2 : 1); --j) {
+    const int g = p.g0 + j;
+    const int64_t hg = p.H >> g, wg = p.W >> g;
+    const int64_t br = b * p.H + (row0 >> j), bc = col0 >> j;
+    const int hc = int(wg + bc) - p.hoff[j];   // 16-B aligned box start
+    const int rb = p.box_pitch[j] * 4;
+    const int nrows = p.row_boxes[j] ? (p.TR >> j) : 1;
+    for (int r = 0; r < nrows; ++r) {
+      tma_load_2d(base + p.box_off[j][0] + r * rb, &maps.level[j], hc, int(br + r), bar, pol);
+      tma_load_2d(base + p.box_off[j][1] + r * rb, &maps.level[j], int(bc), int(br + hg + r), bar, pol);
+      tma_load_2d(base + p.box_off[j][2] + r * rb, &maps.level[j], hc, int(br + hg + r), bar, pol);
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait_rt(int n) {  // runtime-N wrapper (n in [0, N])
+  if constexpr (N > 0) {
+    if (n >= N) {
+      cp_async_wait<N>();
+      return;
+    }
+    cp_async_wait_rt<N - 1>(n);
+  } else {
+    cp_async_wait<0>();
+  }
+}
+
+// MODE 0: all boxes by TMA; 1: level-1 bands by register LDG; 2: everything by cp.async (LDGSTS)
+template <int LPFAST, int TCF, int MODE>
+__global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const __grid_constant__ Syn2dParams p,
                                                            const __grid_constant__ TmaMaps2d maps) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
@@ -354,50 +521,86 @@ __global__ void __launch_bounds__(kThreads2d) syn2d_kernel(const __grid_constant
   }
   __syncthreads();
   uint64_t pol = 0;
-  auto issue = [&](int64_t t, int s) {
-    const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
-    const int64_t b = rt / p.tiles_r;
-    const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = ct * p.TC;
-    unsigned char* base = smem + s * p.stage_bytes;
-    mbar_arrive_expect_tx(&bars[s], p.tx_bytes);
-    const int L = p.Lp;
-    if (p.ll_from_ws)
-      tma_load_2d(base + p.box_off[0][0], &maps.ll, int(col0 >> L), int(b * (p.Hin >> L) + (row0 >> L)), &bars[s], pol);
-    else
-      tma_load_2d(base + p.box_off[0][0], &maps.ll, int(col0 >> L), int(b * p.H + (row0 >> L)), &bars[s], pol);
-    for (int j = L; j >= 1; --j) {
-      const int g = p.g0 + j;
-      const int64_t hg = p.H >> g, wg = p.W >> g;
-      const int64_t br = b * p.H + (row0 >> j), bc = col0 >> j;
-      const int hc = int(wg + bc) - p.hoff[j];   // 16-B aligned box start
-      tma_load_2d(base + p.box_off[j][0], &maps.level[j], hc, int(br), &bars[s], pol);
-      tma_load_2d(base + p.box_off[j][1], &maps.level[j], int(bc), int(br + hg), &bars[s], pol);
-      tma_load_2d(base + p.box_off[j][2], &maps.level[j], hc, int(br + hg), &bars[s], pol);
+  auto issue = [&](int64_t t, int s) { syn_issue_tile(p, maps, smem + s * p.stage_bytes, &bars[s], t, pol); };
+  constexpr bool L1LDG = MODE == 1, CPASYNC = MODE == 2 && LPFAST > 0;
+  if constexpr (CPASYNC) {
+    for (int s = 0; s < p.stages; ++s) {
+      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
+      if (t < p.ntiles)
+        syn_cp_async_tile<LPFAST, TCF>(p, smem + s * p.stage_bytes, t);
+      else
+        cp_async_commit();
     }
-  };
-  if (tid == 0) {
+  } else if (tid < 32) {
     pol = policy_evict_first();
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
       if (t < p.ntiles) issue(t, s);
     }
   }
+  [[maybe_unused]] L1Bands<(LPFAST > 0 ? TCF : 256)> l1;
+  if constexpr (LPFAST > 0 && L1LDG)
+    if (blockIdx.x < p.ntiles) l1.load(p, blockIdx.x);
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
     const int s = it % p.stages;
-    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    if constexpr (CPASYNC) {
+      cp_async_wait_rt<3>(p.stages - 1);   // this thread's copies of the oldest stage have landed
+      __syncthreads();                     // ... and everyone else's
+    } else {
+      mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    }
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
     const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
     unsigned char* stage = smem + s * p.stage_bytes;
-    if constexpr (LPFAST > 0)
-      syn_fast_step<LPFAST>(p, stage, smem, reinterpret_cast<const float*>(stage + p.box_off[0][0]), b, row0,
-                            ct * p.TC);
-    else
+    if constexpr (LPFAST > 0 && !L1LDG) {
+      syn_fast_step<LPFAST, TCF>(p, stage, smem, reinterpret_cast<const float*>(stage + p.box_off[0][0]), b, row0,
+                                 ct * p.TC);
+    } else if constexpr (LPFAST > 0) {
+      const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]);
+      if constexpr (LPFAST >= 2) {
+        syn_fast_coarse<LPFAST, TCF>(p, stage, smem, ll, b, row0, ct * p.TC);
+        ll = reinterpret_cast<const float*>(smem + p.p_off[1]);
+      }
+      // level 1: LL_1 from smem, bands from registers; the next tile's bands are requested as soon
+      // as these registers are consumed, so their HBM latency overlaps the next tile's coarse levels.
+      using B1 = L1Bands<TCF>;
+      float4 top[B1::N], bot[B1::N];
+#pragma unroll
+      for (int k = 0; k < B1::N; ++k) {
+        const int u = tid + k * kThreads2d;
+        const int r = u / B1::UPR, c = (u % B1::UPR) * 2;
+        const float2 vll = *reinterpret_cast<const float2*>(ll + r * B1::C1 + c);
+        const float s0 = vll.x + l1.lh[k].x, t0 = l1.hl[k].x + l1.hh[k].x;
+        const float u0 = vll.x - l1.lh[k].x, w0 = l1.hl[k].x - l1.hh[k].x;
+        const float s1 = vll.y + l1.lh[k].y, t1 = l1.hl[k].y + l1.hh[k].y;
+        const float u1 = vll.y - l1.lh[k].y, w1 = l1.hl[k].y - l1.hh[k].y;
+        top[k] = make_float4((s0 + t0) * 0.5f, (s0 - t0) * 0.5f, (s1 + t1) * 0.5f, (s1 - t1) * 0.5f);
+        bot[k] = make_float4((u0 + w0) * 0.5f, (u0 - w0) * 0.5f, (u1 + w1) * 0.5f, (u1 - w1) * 0.5f);
+      }
+      const int64_t next = tile + gridDim.x;
+      if (next < p.ntiles) l1.load(p, next);
+      float* obase = p.out + (b * p.Hin + row0) * p.out_pitch + ct * p.TC;
+#pragma unroll
+      for (int k = 0; k < B1::N; ++k) {
+        const int u = tid + k * kThreads2d;
+        const int r = u / B1::UPR, c = (u % B1::UPR) * 2;
+        float* o = obase + int64_t(2 * r) * p.out_pitch + 2 * c;
+        stg_stream4(o, top[k]);
+        stg_stream4(o + p.out_pitch, bot[k]);
+      }
+    } else {
       syn_tile(p, stage, smem, b, row0, ct * p.TC);
+    }
     __syncthreads();
-    if (tid == 0) {
-      const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
+    const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
+    if constexpr (CPASYNC) {
+      if (nt < p.ntiles)
+        syn_cp_async_tile<LPFAST, TCF>(p, smem + s * p.stage_bytes, nt);
+      else
+        cp_async_commit();
+    } else if (tid < 32) {
       if (nt < p.ntiles) issue(nt, s);
     }
   }
@@ -472,27 +675,45 @@ static cudaError_t raise_smem_cap(const void* fn) {
   return e;
 }
 
-static const void* ana2d_fn(bool in_f64, int fast_lp) {
-  if (in_f64) return (const void*)ana2d_kernel<double, 0>;
-  switch (fast_lp) {
-    case 1: return (const void*)ana2d_kernel<float, 1>;
-    case 2: return (const void*)ana2d_kernel<float, 2>;
-    case 3: return (const void*)ana2d_kernel<float, 3>;
-    case 4: return (const void*)ana2d_kernel<float, 4>;
-    case 5: return (const void*)ana2d_kernel<float, 5>;
-    default: return (const void*)ana2d_kernel<float, 0>;
+template <int TCF>
+static const void* ana2d_fast_fn(int lp) {
+  switch (lp) {
+    case 1: return (const void*)ana2d_kernel<float, 1, TCF>;
+    case 2: return (const void*)ana2d_kernel<float, 2, TCF>;
+    case 3: return (const void*)ana2d_kernel<float, 3, TCF>;
+    case 4: return (const void*)ana2d_kernel<float, 4, TCF>;
+    default: return (const void*)ana2d_kernel<float, 5, TCF>;
   }
 }
 
-static const void* syn2d_fn(int fast_lp) {
-  switch (fast_lp) {
-    case 1: return (const void*)syn2d_kernel<1>;
-    case 2: return (const void*)syn2d_kernel<2>;
-    case 3: return (const void*)syn2d_kernel<3>;
-    case 4: return (const void*)syn2d_kernel<4>;
-    case 5: return (const void*)syn2d_kernel<5>;
-    default: return (const void*)syn2d_kernel<0>;
+template <int TCF, int MODE>
+static const void* syn2d_fast_fn(int lp) {
+  switch (lp) {
+    case 1: return (const void*)syn2d_kernel<1, TCF, MODE>;
+    case 2: return (const void*)syn2d_kernel<2, TCF, MODE>;
+    case 3: return (const void*)syn2d_kernel<3, TCF, MODE>;
+    case 4: return (const void*)syn2d_kernel<4, TCF, MODE>;
+    default: return (const void*)syn2d_kernel<5, TCF, MODE>;
   }
+}
+
+// fast_lp: 0 = generic kernel; otherwise (tile cols << 4) | LP, tile cols 256 or 128
+static const void* ana2d_fn(bool in_f64, int fast_lp) {
+  if (in_f64) return (const void*)ana2d_kernel<double, 0, 0>;
+  if (fast_lp == 0) return (const void*)ana2d_kernel<float, 0, 0>;
+  return ((fast_lp >> 4) & 0xfff) == 128 ? ana2d_fast_fn<128>(fast_lp & 15) : ana2d_fast_fn<256>(fast_lp & 15);
+}
+
+// synthesis fast_lp additionally carries the load mode (0 TMA, 1 LDG level 1, 2 cp.async) in bits 16+
+static const void* syn2d_fn(int fast_lp) {
+  if (fast_lp == 0) return (const void*)syn2d_kernel<0, 0, 0>;
+  const int mode = (fast_lp >> 16) & 3;
+  const int tc = (fast_lp >> 4) & 0xfff;
+  if (tc == 128)
+    return mode == 2 ? syn2d_fast_fn<128, 2>(fast_lp & 15)
+         : mode == 1 ? syn2d_fast_fn<128, 1>(fast_lp & 15) : syn2d_fast_fn<128, 0>(fast_lp & 15);
+  return mode == 2 ? syn2d_fast_fn<256, 2>(fast_lp & 15)
+       : mode == 1 ? syn2d_fast_fn<256, 1>(fast_lp & 15) : syn2d_fast_fn<256, 0>(fast_lp & 15);
 }
 
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm) {
