@@ -136,23 +136,19 @@ def make_inputs(name, cfg, ws, rank):
     import torch
 
     import datagen
-    if cfg["shard"] == "image":      # weak scaling: rank r owns images [r*B, (r+1)*B)
-        shape = (cfg["batch"], cfg["h"], cfg["w"])
+    from paper_1002_2184_b200 import dist as fdist
+    if cfg["shard"] in ("image", "signal"):   # weak scaling: rank r owns units [r*B, (r+1)*B)
+        first, count = fdist.unit_shard(cfg["batch"], rank)
+        shape = (count, cfg["h"], cfg["w"]) if cfg["shard"] == "image" else (count, cfg["n"])
         host = torch.empty(shape, dtype=torch.float32).pin_memory()
-        datagen.generate("c4", first=rank * cfg["batch"], count=cfg["batch"], size=cfg["h"], out=host.numpy())
-        units = f"images [{rank * cfg['batch']}, {(rank + 1) * cfg['batch']})"
-    elif cfg["shard"] == "signal":   # weak scaling: rank r owns signals [r*B, (r+1)*B)
-        shape = (cfg["batch"], cfg["n"])
-        host = torch.empty(shape, dtype=torch.float32).pin_memory()
-        datagen.generate("c2", first=rank * cfg["batch"], count=cfg["batch"], size=cfg["n"], out=host.numpy())
-        units = f"signals [{rank * cfg['batch']}, {(rank + 1) * cfg['batch']})"
-    else:                            # strong scaling: rank r owns a 2^L-aligned row band
-        rows = cfg["h"] // ws
-        assert rows % (1 << cfg["levels"]) == 0 and rows % 256 == 0
-        shape = (rows, cfg["w"])
-        host = torch.empty(shape, dtype=torch.float32).pin_memory()
-        datagen.generate("c5", r0=rank * rows, r1=(rank + 1) * rows, size=cfg["h"], out=host.numpy())
-        units = f"rows [{rank * rows}, {(rank + 1) * rows})"
+        datagen.generate("c4" if cfg["shard"] == "image" else "c2", first=first, count=count, size=shape[-1],
+                         out=host.numpy())
+        units = f"{cfg['shard']}s [{first}, {first + count})"
+    else:                                    # strong scaling: rank r owns a 2^L-aligned row band
+        r0, r1 = fdist.row_band(cfg["h"], ws, rank, cfg["levels"])
+        host = torch.empty((r1 - r0, cfg["w"]), dtype=torch.float32).pin_memory()
+        datagen.generate("c5", r0=r0, r1=r1, size=cfg["h"], out=host.numpy())
+        units = f"rows [{r0}, {r1})"
     return host, units
 
 
@@ -190,7 +186,7 @@ def measure(name, cfg, args, ws, rank, local, pg):
             evs[1].record(stream)
         if cfg["shard"] == "rowband":
             fhwt.pack_ll_2d(coeffs, L, out=ll_local)      # K6 pack (same kernel family, counted)
-            if gather:
+            if gather:   # the only exchange (NCCL over NVLink): coarsest LL of every band
                 dist.all_gather_into_tensor(ll_all, ll_local, group=pg)
         if evs:
             evs[2].record(stream)

@@ -1,0 +1,63 @@
+"""Multi-GPU plumbing for the Fast Haar path.
+
+One process per GPU over torch.distributed (NCCL on B200, gloo in the CPU tests).  The transform
+partitions into independent units (reading R1: pairs (x[2k], x[2k+1]) make every 2^L-aligned
+block independent), so sharding needs no halo exchange:
+
+* batched signals / images (c2, c4): rank r owns units [r*B, (r+1)*B) of a global batch N*B
+  (weak scaling, no collective on the data path);
+* one large image (c5): rank r owns rows [r*h/N, (r+1)*h/N), a multiple of 2^L rows; its band
+  output equals rows [r*h/N >> j, (r+1)*h/N >> j) of every global level-j band.  The coarsest LL
+  of all bands is all-gathered (the only exchange; 64 KiB for c5).
+
+Only host arithmetic and the collective live here; the packing is the library's
+fhwt_pack_ll_2d kernel on GPU (callers pass the packed tensor).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def unit_shard(units_per_rank: int, rank: int) -> tuple[int, int]:
+    """Weak scaling: (first unit, count) owned by `rank`."""
+    return rank * units_per_rank, units_per_rank
+
+
+def row_band(h: int, world: int, rank: int, levels: int) -> tuple[int, int]:
+    """Rows [r0, r1) of an h-row image owned by `rank` (strong split into 2^levels-aligned bands)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    if h % world:
+        raise ValueError(f"h={h} does not split into {world} equal bands")
+    rows = h // world
+    if rows % (1 << levels):
+        raise ValueError(f"band of {rows} rows is not a multiple of 2^{levels}: bands would need a halo")
+    return rank * rows, (rank + 1) * rows
+
+
+def band_rows(r0: int, r1: int, level: int) -> tuple[int, int]:
+    """Rows of the global level-`level` bands that a band [r0, r1) produces."""
+    return r0 >> level, r1 >> level
+
+
+def gather_coarse_ll(ll_local: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather the packed coarsest LL of every rank's row band, concatenated along rows
+    (rank order = row order).  NCCL: all_gather_into_tensor; other backends: all_gather."""
+    world = dist.get_world_size(group)
+    out = torch.empty((world * ll_local.shape[0],) + tuple(ll_local.shape[1:]), dtype=ll_local.dtype,
+                      device=ll_local.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, ll_local.contiguous(), group=group)
+    else:
+        parts = list(out.chunk(world, dim=0))
+        dist.all_gather(parts, ll_local.contiguous(), group=group)
+        out = torch.cat(parts, dim=0)
+    return out
+
+
+def max_over_ranks(value: float, device=None, group=None) -> float:
+    """Device-timed quantities are reported as the max over ranks."""
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

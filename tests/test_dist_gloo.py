@@ -1,0 +1,116 @@
+"""World-size-2 gloo tests of the multi-GPU plumbing on CPU.
+
+The CUDA kernels are not involved: each rank transforms its shard with the fp64 oracle as a
+stand-in, so these tests check the sharding arithmetic, band-row mapping, the LL gather and the
+max-over-ranks timing reduction — the host logic bench.py runs under torchrun.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import datagen
+import oracle as o
+from paper_1002_2184_b200 import dist as fdist
+
+WORLD = 2
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, port, fn_name, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        q.put((rank, globals()[fn_name](rank)))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(fn_name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, fn_name, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(WORLD))
+    for p in procs:
+        p.join(timeout=60)
+    return res
+
+
+# ------------------------------------------------------------------ rank bodies
+H, W, L = 512, 256, 5
+
+
+def _c5_like_rank(rank):
+    r0, r1 = fdist.row_band(H, WORLD, rank, L)
+    band = datagen.c5_rows(r0, r1, size=512)[:, :W]
+    coeffs = o.analyze_2d(band, L)
+    ll = torch.from_numpy(np.ascontiguousarray(coeffs[:(r1 - r0) >> L, :W >> L]))
+    gathered = fdist.gather_coarse_ll(ll)
+    t = fdist.max_over_ranks(1.5 + rank)
+    return {"r0": r0, "r1": r1, "coeffs": coeffs, "ll_all": gathered.numpy(), "tmax": t}
+
+
+def _weak_rank(rank):
+    first, count = fdist.unit_shard(3, rank)
+    x = datagen.c4_batch(first, count, size=64)
+    return {"first": first, "count": count, "coeffs": o.analyze_2d(x, 4)}
+
+
+# ------------------------------------------------------------------ tests
+@pytest.mark.timeout(300)
+def test_row_band_sharding_and_ll_gather():
+    res = _run("_c5_like_rank")
+    full = datagen.c5_rows(0, H, size=512)[:, :W]
+    ref = o.analyze_2d(full, L)
+    for r in range(WORLD):
+        assert isinstance(res[r], dict), res[r]
+        d = res[r]
+        assert (d["r0"], d["r1"]) == (r * H // WORLD, (r + 1) * H // WORLD)
+        bh = d["r1"] - d["r0"]
+        for j in range(1, L + 1):
+            g0, g1 = fdist.band_rows(d["r0"], d["r1"], j)
+            hj, wj, bj = H >> j, W >> j, bh >> j
+            # band-local Mallat output == the corresponding rows of every global band (pin C8)
+            np.testing.assert_allclose(d["coeffs"][:bj, wj:2 * wj], ref[g0:g1, wj:2 * wj], atol=1e-12)
+            np.testing.assert_allclose(d["coeffs"][bj:2 * bj, :wj], ref[hj + g0:hj + g1, :wj], atol=1e-12)
+            np.testing.assert_allclose(d["coeffs"][bj:2 * bj, wj:2 * wj], ref[hj + g0:hj + g1, wj:2 * wj], atol=1e-12)
+        # every rank ends with the same, complete coarsest LL
+        np.testing.assert_allclose(d["ll_all"], ref[:H >> L, :W >> L], atol=1e-12)
+        assert d["tmax"] == 1.5 + WORLD - 1
+
+
+@pytest.mark.timeout(300)
+def test_weak_scaling_unit_shards():
+    res = _run("_weak_rank")
+    firsts = sorted((res[r]["first"], res[r]["count"]) for r in range(WORLD))
+    assert firsts == [(0, 3), (3, 3)]
+    allx = datagen.c4_batch(0, 6, size=64)
+    ref = o.analyze_2d(allx, 4)
+    for r in range(WORLD):
+        f, c = res[r]["first"], res[r]["count"]
+        np.testing.assert_allclose(res[r]["coeffs"], ref[f:f + c], atol=1e-12)
+
+
+def test_row_band_validation():
+    assert fdist.row_band(32768, 8, 7, 8) == (28672, 32768)
+    with pytest.raises(ValueError):
+        fdist.row_band(32768, 3, 0, 8)          # not an equal split
+    with pytest.raises(ValueError):
+        fdist.row_band(1024, 8, 0, 8)           # 128-row band < 2^8: would need a halo
+    assert fdist.band_rows(4096, 8192, 8) == (16, 32)
