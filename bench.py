@@ -367,8 +367,9 @@ def time_oracle(name, cfg, budget_s=20.0):
         units = max(1, min(cfg["h"] // 256, int(budget_s / 2.3 * cores)))
         tasks = [("c5", i, cfg["h"], min(cfg["levels"], 8)) for i in range(units)]
         sample = f"{units} of the 128 256-row bands of c5 (each band DWT+IDWT with L=8 — band-local, halo-free)"
+    import multiprocessing as mp
     t0 = time.perf_counter()
-    with ProcessPoolExecutor(cores) as ex:
+    with ProcessPoolExecutor(cores, mp_context=mp.get_context("forkserver")) as ex:
         res = list(ex.map(_oracle_unit, tasks))
     wall = time.perf_counter() - t0
     samples = sum(r[0] for r in res)

@@ -190,7 +190,9 @@ def generate(kind: str, *, first: int = 0, count: int | None = None, size: int |
             for t in tasks:
                 _fill_worker(t)
         else:
-            with ProcessPoolExecutor(workers) as ex:
+            import multiprocessing as mp
+            # forkserver: the caller may already hold CUDA / threads, where fork() is unsafe
+            with ProcessPoolExecutor(workers, mp_context=mp.get_context("forkserver")) as ex:
                 list(ex.map(_fill_worker, tasks))
         src = np.ndarray(shape, dtype=np.float32, buffer=shm.buf)
         if out is None:
