@@ -303,6 +303,56 @@ def sampled_parity(name, cfg, host, coeffs, rec, rank, ws):
             "roundtrip_err_rel": float(np.abs(r - x).max()) / scale, "tol": 1e-5}
 
 
+def measure_direct(name, cfg, d_host, steps=5):
+    """§8(f) f3: the paper's original structure (Figs. 2 and 5, full-rate filtering, materialised
+    intermediates, level by level) on the same GPU and workload, next to static op counts."""
+    import torch
+
+    import paper_1002_2184_b200 as fhwt
+    d = d_host.to("cuda")
+    c = torch.empty_like(d)
+    r = torch.empty_like(d)
+    L = cfg["levels"]
+    if cfg["kind"] == "2d":
+        shape, batch = (cfg["h"], cfg["w"]), d.shape[0]
+        ws = torch.empty(fhwt.direct_workspace_bytes(2, shape[0], shape[1], batch), dtype=torch.uint8, device="cuda")
+        ana = lambda: fhwt.direct_analyze_2d(d, L, out=c, workspace=ws)  # noqa: E731
+        syn = lambda: fhwt.direct_synthesize_2d(c, L, out=r, workspace=ws)  # noqa: E731
+    else:
+        shape, batch = (cfg["n"],), d.shape[0]
+        ws = torch.empty(fhwt.direct_workspace_bytes(1, shape[0], 0, batch), dtype=torch.uint8, device="cuda")
+        ana = lambda: fhwt.direct_analyze_1d(d, L, out=c, workspace=ws)  # noqa: E731
+        syn = lambda: fhwt.direct_synthesize_1d(c, L, out=r, workspace=ws)  # noqa: E731
+    for _ in range(2):
+        ana()
+        syn()
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    for _ in range(steps):
+        ana()
+    e[1].record()
+    for _ in range(steps):
+        syn()
+    e[2].record()
+    torch.cuda.synchronize()
+    ta, ts = e[0].elapsed_time(e[1]) / steps, e[1].elapsed_time(e[2]) / steps
+    err = float((r - d).abs().max() / d.abs().max())
+    S = d.numel()
+    ops = {}
+    for st in ("direct", "fast", "kernel"):
+        ma, aa = fhwt.op_counts(shape, L, st, batch=batch)
+        ms, as_ = fhwt.op_counts(shape, L, st, synthesis=True, batch=batch)
+        ops[st] = {"analysis_mul": ma, "analysis_add": aa, "synthesis_mul": ms, "synthesis_add": as_}
+    del d, c, r, ws
+    torch.cuda.empty_cache()
+    return {"structure": "Fig. 2 / Fig. 5 direct form, level by level, intermediates in HBM",
+            "analysis_ms": ta, "synthesis_ms": ts, "ms_per_step": ta + ts,
+            "value": 16.0 * S / ((ta + ts) * 1e-3) / 1e9, "unit": "GB/s (same 16 B/sample algorithmic bytes)",
+            "roundtrip_err_rel": err, "op_counts": ops,
+            "mul_ratio_fast_over_direct": ops["fast"]["analysis_mul"] / ops["direct"]["analysis_mul"]}
+
+
 def measure_e2e(cfg, host, steps):
     """Same metric through the public host-buffer API: every step copies the pinned input H2D,
     runs DWT+IDWT and copies coefficients and d_R back D2H (fhwt_roundtrip_*_host)."""
@@ -416,6 +466,7 @@ def main():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-breakdown", action="store_true", help="skip the c2/c5 secondary measurements")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-direct", action="store_true", help="skip the direct-form (Fig. 2/5) baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
@@ -435,6 +486,10 @@ def main():
         pg = dist.group.WORLD
     cfg = WORKLOADS[args.workload]
     res, (plan, host) = measure(args.workload, cfg, args, ws, rank, local, pg)
+    direct = None
+    if not args.no_direct and rank == 0:
+        direct = measure_direct(args.workload, cfg, host)
+        direct["fast_speedup"] = direct["ms_per_step"] / res["ms_per_step"]
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(cfg, host, args.e2e_steps)
@@ -481,6 +536,7 @@ def main():
             "clocks": res["clocks"],
             "parity": res["parity"],
             "workloads": breakdown,
+            "direct_form": direct,
         }
         print(json.dumps(out), flush=True)
     if ws > 1:

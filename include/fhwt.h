@@ -144,6 +144,32 @@ fhwt_status fhwt_roundtrip_2d_host(const float *h_d, float *h_coeffs, float *h_d
 fhwt_status fhwt_roundtrip_1d_host(const float *h_d, float *h_coeffs, float *h_dR, int64_t n, int64_t batch,
                                    int levels, int64_t chunk);
 
+/* ------------------------------------------------------------------ direct-form baseline (§8(f) f3)
+ * The paper's ORIGINAL structure, for comparison with the Fast structure on the same hardware:
+ * analysis = full-rate filtering with b0/b1 then decimation keeping n = 2k+1 (Fig. 2, Eqs. (1)-(4),
+ * PAPER.md:58-74); synthesis = zero-insertion upsampling then full-rate filtering with a0/a1 and
+ * summation (Fig. 5, Eq. (13)); level by level, rows then columns, every
+ * intermediate materialised in device memory.  Same layouts, validation and errors as the Fast entry
+ * points; workspace is REQUIRED (device, fhwt_direct_workspace_bytes bytes, caller-owned). */
+size_t fhwt_direct_workspace_bytes(int dims, int64_t n_or_h, int64_t w, int64_t batch);
+fhwt_status fhwt_direct_analyze_1d(const float *d, float *coeffs, int64_t n, int64_t batch, int levels,
+                                   void *workspace, fhwt_stream_t s);
+fhwt_status fhwt_direct_synthesize_1d(const float *coeffs, float *d_R, int64_t n, int64_t batch, int levels,
+                                      void *workspace, fhwt_stream_t s);
+fhwt_status fhwt_direct_analyze_2d(const float *d, float *coeffs, int64_t h, int64_t w, int64_t batch, int levels,
+                                   void *workspace, fhwt_stream_t s);
+fhwt_status fhwt_direct_synthesize_2d(const float *coeffs, float *d_R, int64_t h, int64_t w, int64_t batch,
+                                      int levels, void *workspace, fhwt_stream_t s);
+
+/* Static arithmetic-operation counts (multiplications, additions incl. subtractions) of one
+ * multi-level transform on sample data ("less than quarter").
+ * dims = 1 (n_or_h = n, w ignored) or 2; structure: 0 = direct (Figs. 2/5, full-rate, multiplies by
+ * inserted zeros), 1 = Fast as drawn in the paper (separable 1-D butterflies, Figs. 4/7),
+ * 2 = this library's kernels (2-D butterflies folded to one exact x1/2 per 2x2 block);
+ * synthesis = 0 analysis / 1 synthesis.  INVALID_ARG on bad arguments, plus the plan errors. */
+fhwt_status fhwt_op_counts(int dims, int64_t n_or_h, int64_t w, int64_t batch, int levels, int structure,
+                           int synthesis, uint64_t *mul, uint64_t *add);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,8 @@ __all__ = [
     "lib", "lib_path", "haar_filter_bank", "launch_count", "version",
     "analyze_1d", "synthesize_1d", "analyze_2d", "synthesize_2d", "Plan1d", "Plan2d",
     "pack_ll_2d", "roundtrip_2d_host", "roundtrip_1d_host", "band_offset_1d", "band_offset_2d",
+    "direct_workspace_bytes", "direct_analyze_1d", "direct_synthesize_1d", "direct_analyze_2d",
+    "direct_synthesize_2d", "op_counts",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -126,6 +128,13 @@ def lib():
         "fhwt_pack_ll_2d": (st, [vp, vp, i64, i64, i64, c_int, vp]),
         "fhwt_roundtrip_2d_host": (st, [vp, vp, vp, i64, i64, i64, c_int, i64]),
         "fhwt_roundtrip_1d_host": (st, [vp, vp, vp, i64, i64, c_int, i64]),
+        "fhwt_direct_workspace_bytes": (ctypes.c_size_t, [c_int, i64, i64, i64]),
+        "fhwt_direct_analyze_1d": (st, [vp, vp, i64, i64, c_int, vp, vp]),
+        "fhwt_direct_synthesize_1d": (st, [vp, vp, i64, i64, c_int, vp, vp]),
+        "fhwt_direct_analyze_2d": (st, [vp, vp, i64, i64, i64, c_int, vp, vp]),
+        "fhwt_direct_synthesize_2d": (st, [vp, vp, i64, i64, i64, c_int, vp, vp]),
+        "fhwt_op_counts": (st, [c_int, i64, i64, i64, c_int, c_int, c_int, ctypes.POINTER(ctypes.c_uint64),
+                                ctypes.POINTER(ctypes.c_uint64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -380,3 +389,70 @@ def band_offset_2d(h: int, w: int, level: int, band: int):
         raise InvalidArgument(f"bad band query {h}x{w} level={level} band={band}")
     return int(off), int(r.value), int(c.value)
 
+
+
+# ------------------------------------------------------------------ direct-form baseline (§8(f) f3)
+def direct_workspace_bytes(dims: int, n_or_h: int, w: int, batch: int) -> int:
+    return int(lib().fhwt_direct_workspace_bytes(int(dims), int(n_or_h), int(w), int(batch)))
+
+
+def _direct_ws(x, dims, n_or_h, w, batch, workspace):
+    import torch
+    nb = direct_workspace_bytes(dims, n_or_h, w, batch)
+    if workspace is None:
+        workspace = torch.empty(max(nb, 1), dtype=torch.uint8, device=x.device)
+    if not workspace.is_cuda or workspace.numel() * workspace.element_size() < nb:
+        raise InvalidArgument(f"workspace must be a CUDA buffer of >= {nb} bytes")
+    return ctypes.c_void_p(workspace.data_ptr())
+
+
+def direct_analyze_1d(d, levels: int, out=None, workspace=None, stream=None):
+    """fhwt_direct_analyze_1d: the paper's original structure (Fig. 2) on the GPU — baseline only."""
+    n, batch = _shape_1d(d)
+    out = _out_like(d, out)
+    with _guard_device(d):
+        _check(lib().fhwt_direct_analyze_1d(_dev_f32(d, "d"), _dev_f32(out, "coeffs"), n, batch, int(levels),
+                                            _direct_ws(d, 1, n, 0, batch, workspace), _stream(stream)))
+    return out
+
+
+def direct_synthesize_1d(coeffs, levels: int, out=None, workspace=None, stream=None):
+    """fhwt_direct_synthesize_1d: Fig. 5 (zero insertion + full-rate filters) — baseline only."""
+    n, batch = _shape_1d(coeffs)
+    out = _out_like(coeffs, out)
+    with _guard_device(coeffs):
+        _check(lib().fhwt_direct_synthesize_1d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"), n, batch,
+                                               int(levels), _direct_ws(coeffs, 1, n, 0, batch, workspace),
+                                               _stream(stream)))
+    return out
+
+
+def direct_analyze_2d(d, levels: int, out=None, workspace=None, stream=None):
+    h, w, batch = _shape_2d(d)
+    out = _out_like(d, out)
+    with _guard_device(d):
+        _check(lib().fhwt_direct_analyze_2d(_dev_f32(d, "d"), _dev_f32(out, "coeffs"), h, w, batch, int(levels),
+                                            _direct_ws(d, 2, h, w, batch, workspace), _stream(stream)))
+    return out
+
+
+def direct_synthesize_2d(coeffs, levels: int, out=None, workspace=None, stream=None):
+    h, w, batch = _shape_2d(coeffs)
+    out = _out_like(coeffs, out)
+    with _guard_device(coeffs):
+        _check(lib().fhwt_direct_synthesize_2d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"), h, w, batch,
+                                               int(levels), _direct_ws(coeffs, 2, h, w, batch, workspace),
+                                               _stream(stream)))
+    return out
+
+
+_STRUCTURES = {"direct": 0, "fast": 1, "kernel": 2}
+
+
+def op_counts(shape, levels: int, structure: str = "fast", synthesis: bool = False, batch: int = 1):
+    """fhwt_op_counts: static (mul, add) counts of one transform; shape = (n,) or (h, w)."""
+    m, a = ctypes.c_uint64(), ctypes.c_uint64()
+    dims = len(shape)
+    _check(lib().fhwt_op_counts(dims, int(shape[0]), int(shape[1]) if dims == 2 else 0, int(batch), int(levels),
+                                _STRUCTURES[structure], int(bool(synthesis)), ctypes.byref(m), ctypes.byref(a)))
+    return int(m.value), int(a.value)

@@ -740,3 +740,197 @@ extern "C" fhwt_status fhwt_roundtrip_1d_host(const float* h_d, float* h_coeffs,
   delete p;
   return st;
 }
+
+// ---------------------------------------------------------------------- direct-form baseline (f3)
+namespace {
+
+Lines_t lines(int64_t batch, int64_t bstride, int64_t count, int64_t sstride, int64_t len, int64_t nstride) {
+  return Lines_t{batch, bstride, count, sstride, len, nstride};
+}
+
+fhwt_status direct_common(const void* in, const void* out, const void* ws, size_t bytes) {
+  FHWT_TRY(check_ptrs(in, out, bytes));
+  if (!ws) return fail(FHWT_ERR_INVALID_ARG, "the direct-form baseline needs a workspace (fhwt_direct_workspace_bytes)");
+  return FHWT_OK;
+}
+
+}  // namespace
+
+extern "C" size_t fhwt_direct_workspace_bytes(int dims, int64_t n_or_h, int64_t w, int64_t batch) {
+  if (n_or_h <= 0 || batch <= 0 || (dims == 2 && w <= 0)) return 0;
+  const size_t S = size_t(batch) * size_t(n_or_h) * size_t(dims == 2 ? w : 1);
+  return (dims == 2 ? 4 : 3) * S * sizeof(float);
+}
+
+// 1-D: level j works on lines of len n >> (j-1); y0/y1 scratch 2*B*n, approx ping-pong 2 x B*n/2.
+extern "C" fhwt_status fhwt_direct_analyze_1d(const float* d, float* coeffs, int64_t n, int64_t batch, int levels,
+                                              void* workspace, fhwt_stream_t st) {
+  FHWT_TRY(check_1d(n, batch, levels));
+  FHWT_TRY(direct_common(d, coeffs, workspace, size_t(n) * batch * 4));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  float* y0 = static_cast<float*>(workspace);
+  float* y1 = y0 + batch * n;
+  float* pp[2] = {y1 + batch * n, y1 + batch * n + batch * (n / 2)};
+  const float* x = d;
+  int64_t xs = n;  // signal stride of the current input
+  for (int j = 1; j <= levels; ++j) {
+    const int64_t len = n >> (j - 1), half = len / 2;
+    float* a = j == levels ? coeffs : pp[j & 1];
+    const int64_t as = j == levels ? n : half;
+    FHWT_CUDA(direct_analysis_lines(x, lines(1, 0, batch, xs, len, 1), a, lines(1, 0, batch, as, half, 1),
+                                    coeffs + half, lines(1, 0, batch, n, half, 1), y0, y1, s),
+              "direct analysis 1-D");
+    x = a;
+    xs = as;
+  }
+  return FHWT_OK;
+}
+
+extern "C" fhwt_status fhwt_direct_synthesize_1d(const float* coeffs, float* dR, int64_t n, int64_t batch, int levels,
+                                                 void* workspace, fhwt_stream_t st) {
+  FHWT_TRY(check_1d(n, batch, levels));
+  FHWT_TRY(direct_common(coeffs, dR, workspace, size_t(n) * batch * 4));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  float* u0 = static_cast<float*>(workspace);
+  float* u1 = u0 + batch * n;
+  float* pp[2] = {u1 + batch * n, u1 + batch * n + batch * (n / 2)};
+  const float* a = coeffs;
+  int64_t as = n;
+  for (int j = levels; j >= 1; --j) {
+    const int64_t half = n >> j, len = 2 * half;
+    float* r = j == 1 ? dR : pp[j & 1];
+    const int64_t rs = j == 1 ? n : len;
+    FHWT_CUDA(direct_synthesis_lines(a, lines(1, 0, batch, as, half, 1), coeffs + half, lines(1, 0, batch, n, half, 1),
+                                     r, lines(1, 0, batch, rs, len, 1), u0, u1, s),
+              "direct synthesis 1-D");
+    a = r;
+    as = rs;
+  }
+  return FHWT_OK;
+}
+
+// 2-D, level j on the hc x wc LL region: rows (Fig. 2 along every row) -> L, H (compact
+// B x hc x wc/2); columns of L -> LL, LH and of H -> HL, HH.  Workspace: y0/y1 (2 S), L/H (S),
+// LL ping-pong (2 x S/4).
+extern "C" fhwt_status fhwt_direct_analyze_2d(const float* d, float* coeffs, int64_t h, int64_t w, int64_t batch,
+                                              int levels, void* workspace, fhwt_stream_t st) {
+  FHWT_TRY(check_2d(h, w, batch, levels));
+  FHWT_TRY(direct_common(d, coeffs, workspace, size_t(h) * w * batch * 4));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  const int64_t S = batch * h * w;
+  float* y0 = static_cast<float*>(workspace);
+  float* y1 = y0 + S;
+  float* Lb = y1 + S;
+  float* Hb = Lb + S / 2;
+  float* pp[2] = {Hb + S / 2, Hb + S / 2 + S / 4};
+  const float* x = d;
+  int64_t xb = h * w, xp = w;  // image stride, row pitch of the current LL input
+  for (int j = 1; j <= levels; ++j) {
+    const int64_t hc = h >> (j - 1), wc = w >> (j - 1), hh = hc / 2, wh = wc / 2;
+    // rows: batch x hc lines of wc -> L, H (batch x hc x wh, compact)
+    FHWT_CUDA(direct_analysis_lines(x, lines(batch, xb, hc, xp, wc, 1), Lb, lines(batch, hc * wh, hc, wh, wh, 1), Hb,
+                                    lines(batch, hc * wh, hc, wh, wh, 1), y0, y1, s),
+              "direct analysis 2-D rows");
+    // columns of L: wh lines of hc (stride wh) -> LL (to ping-pong or coeffs), LH (coeffs)
+    const bool last = j == levels;
+    float* ll = last ? coeffs : pp[j & 1];
+    const int64_t llb = last ? h * w : hh * wh, llp = last ? w : wh;
+    FHWT_CUDA(direct_analysis_lines(Lb, lines(batch, hc * wh, wh, 1, hc, wh), ll, lines(batch, llb, wh, 1, hh, llp),
+                                    coeffs + hh * w, lines(batch, h * w, wh, 1, hh, w), y0, y1, s),
+              "direct analysis 2-D columns (L)");
+    FHWT_CUDA(direct_analysis_lines(Hb, lines(batch, hc * wh, wh, 1, hc, wh), coeffs + wh,
+                                    lines(batch, h * w, wh, 1, hh, w), coeffs + hh * w + wh,
+                                    lines(batch, h * w, wh, 1, hh, w), y0, y1, s),
+              "direct analysis 2-D columns (H)");
+    x = ll;
+    xb = llb;
+    xp = llp;
+  }
+  return FHWT_OK;
+}
+
+extern "C" fhwt_status fhwt_direct_synthesize_2d(const float* coeffs, float* dR, int64_t h, int64_t w, int64_t batch,
+                                                 int levels, void* workspace, fhwt_stream_t st) {
+  FHWT_TRY(check_2d(h, w, batch, levels));
+  FHWT_TRY(direct_common(coeffs, dR, workspace, size_t(h) * w * batch * 4));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  const int64_t S = batch * h * w;
+  float* u0 = static_cast<float*>(workspace);
+  float* u1 = u0 + S;
+  float* Lb = u1 + S;
+  float* Hb = Lb + S / 2;
+  float* pp[2] = {Hb + S / 2, Hb + S / 2 + S / 4};
+  const float* ll = coeffs;
+  int64_t llb = h * w, llp = w;
+  for (int j = levels; j >= 1; --j) {
+    const int64_t hh = h >> j, wh = w >> j, hc = 2 * hh, wc = 2 * wh;
+    // columns: (LL, LH) -> L and (HL, HH) -> H, each batch x hc x wh compact
+    FHWT_CUDA(direct_synthesis_lines(ll, lines(batch, llb, wh, 1, hh, llp), coeffs + hh * w,
+                                     lines(batch, h * w, wh, 1, hh, w), Lb, lines(batch, hc * wh, wh, 1, hc, wh), u0,
+                                     u1, s),
+              "direct synthesis 2-D columns (L)");
+    FHWT_CUDA(direct_synthesis_lines(coeffs + wh, lines(batch, h * w, wh, 1, hh, w), coeffs + hh * w + wh,
+                                     lines(batch, h * w, wh, 1, hh, w), Hb, lines(batch, hc * wh, wh, 1, hc, wh), u0,
+                                     u1, s),
+              "direct synthesis 2-D columns (H)");
+    // rows: (L, H) -> LL_{j-1}
+    float* r = j == 1 ? dR : pp[j & 1];
+    const int64_t rb = j == 1 ? h * w : hc * wc, rp = j == 1 ? w : wc;
+    FHWT_CUDA(direct_synthesis_lines(Lb, lines(batch, hc * wh, hc, wh, wh, 1), Hb, lines(batch, hc * wh, hc, wh, wh, 1),
+                                     r, lines(batch, rb, hc, rp, wc, 1), u0, u1, s),
+              "direct synthesis 2-D rows");
+    ll = r;
+    llb = rb;
+    llp = rp;
+  }
+  return FHWT_OK;
+}
+
+// Static op counts.  Per 1-D level on N input samples (analysis) / N output samples (synthesis):
+//   direct analysis  4N mul + 2N add   (2 filters x N positions x (2 mul + 1 add))
+//   direct synthesis 4N mul + 3N add   (2 filters x N positions x (2 mul + 1 add) + N branch sums)
+//   fast             N mul + N add     (N/2 butterflies x (2 mul + 2 add))
+// 2-D separable level on hc x wc: hc lines of wc plus wc lines of hc (the L and H halves).
+// This library's 2-D kernels: per 2x2 block 4 mul + 8 add (exact x1/2 folding), both directions.
+extern "C" fhwt_status fhwt_op_counts(int dims, int64_t n_or_h, int64_t w, int64_t batch, int levels, int structure,
+                                      int synthesis, uint64_t* mul, uint64_t* add) {
+  if (!mul || !add || structure < 0 || structure > 2 || (dims != 1 && dims != 2))
+    return fail(FHWT_ERR_INVALID_ARG, "bad op-count query");
+  if (dims == 1)
+    FHWT_TRY(check_1d(n_or_h, batch, levels));
+  else
+    FHWT_TRY(check_2d(n_or_h, w, batch, levels));
+  auto per = [&](uint64_t N, uint64_t* m, uint64_t* a) {
+    if (structure == 0) {
+      *m = 4 * N;
+      *a = (synthesis ? 3 : 2) * N;
+    } else {
+      *m = N;
+      *a = N;
+    }
+  };
+  uint64_t M = 0, A = 0;
+  for (int j = 1; j <= levels; ++j) {
+    if (dims == 1) {
+      uint64_t m, a;
+      per(uint64_t(n_or_h >> (j - 1)), &m, &a);
+      M += m;
+      A += a;
+    } else {
+      const uint64_t hc = uint64_t(n_or_h >> (j - 1)), wc = uint64_t(w >> (j - 1));
+      if (structure == 2) {
+        M += hc * wc;       // (hc/2)(wc/2) blocks x 4 mul
+        A += 2 * hc * wc;   // x 8 add
+      } else {
+        uint64_t m1, a1, m2, a2;
+        per(wc, &m1, &a1);
+        per(hc, &m2, &a2);
+        M += hc * m1 + wc * m2;
+        A += hc * a1 + wc * a2;
+      }
+    }
+  }
+  *mul = M * uint64_t(batch);
+  *add = A * uint64_t(batch);
+  return FHWT_OK;
+}

@@ -105,6 +105,16 @@ cudaError_t launch_syn1d_l1_scalar(const float* c, float* d, int64_t n, int64_t 
 cudaError_t launch_pack_ll(const float* c, float* ll, int64_t h, int64_t w, int64_t batch, int levels,
                            cudaStream_t s);
 
+// Direct-form baseline (direct.cu, §8(f) f3): `batch` groups of `count` lines of `len` samples,
+// sample n of line s of group b at base[b * bstride + s * sstride + n * nstride].
+struct Lines_t {
+  int64_t batch, bstride, count, sstride, len, nstride;
+};
+cudaError_t direct_analysis_lines(const float* x, Lines_t lx, float* a, Lines_t la, float* d, Lines_t ld, float* y0,
+                                  float* y1, cudaStream_t s);
+cudaError_t direct_synthesis_lines(const float* a, Lines_t la, const float* d, Lines_t ld, float* r, Lines_t lr,
+                                   float* u0, float* u1, cudaStream_t s);
+
 void count_launch();
 
 // ------------------------------------------------------------------ device helpers

@@ -116,3 +116,33 @@ def test_null_and_cpu_pointer_rejection():
     assert L.fhwt_plan_destroy(None) == 0
     assert L.fhwt_status_string(8) == b"FHWT_ERR_MISALIGNED"
     assert ctypes.sizeof(fhwt.FilterBank) >= 8 * 8 + 4
+
+
+@pytest.mark.parametrize("shape,levels", [((8,), 1), ((64,), 3), ((1024,), 10), ((16, 16), 1), ((32, 64), 3),
+                                          ((64, 64), 5)])
+def test_op_counts_match_the_oracles_instrumented_count(shape, levels):
+    """The C-ABI op-count formulas equal the operations the fp64 oracle actually performs (its
+    OpCounter counts every sample multiply/add of the direct and fast structures)."""
+    import numpy as np
+
+    import oracle as o
+    x = np.ones(shape)
+    for structure, mode in (("direct", "direct"), ("fast", "fast")):
+        ops = o.OpCounter()
+        if len(shape) == 1:
+            c = o.decompose_1d(x, levels, mode, ops)
+        else:
+            c = o.analyze_2d(x, levels, mode, ops)
+        assert fhwt.op_counts(shape, levels, structure) == (ops.mul, ops.add), (structure, "analysis")
+        ops = o.OpCounter()
+        if len(shape) == 1:
+            o.reconstruct_1d(c, levels, mode, ops)
+        else:
+            o.synthesize_2d(c, levels, mode, ops)
+        assert fhwt.op_counts(shape, levels, structure, synthesis=True) == (ops.mul, ops.add), (structure, "synthesis")
+    dm, da = fhwt.op_counts(shape, levels, "direct")
+    fm, fa = fhwt.op_counts(shape, levels, "fast")
+    assert 4 * fm == dm and 3 * (fm + fa) == dm + da      # PAPER.md:124 "less than quarter"; 1/3 total
+    km, ka = fhwt.op_counts(shape, levels, "kernel")
+    assert km <= fm and km + ka <= fm + fa
+    assert fhwt.op_counts(shape, levels, "fast", batch=7) == (7 * fm, 7 * fa)

@@ -197,3 +197,41 @@ def test_host_roundtrip_api():
     ry = fhwt.roundtrip_1d_host(y, 12, coeffs_out=cy, chunk=3)
     assert_close(cy.double().numpy(), o.decompose_1d(y.numpy(), 12), y.numpy(), 1)
     assert_close(ry.double().numpy(), y.numpy(), y.numpy(), 1)
+
+
+# ------------------------------------------------------------------ §8(f) f3: direct-form baseline
+@pytest.mark.parametrize("n,batch,levels", [(1024, 3, 10), (12, 2, 2), (4096, 2, 7), (6, 2, 1)])
+def test_direct_form_1d(n, batch, levels):
+    x = datagen.uniform((batch, n), seed=n + 17 * levels)
+    c = fhwt.direct_analyze_1d(dev(x), levels)
+    assert_close(host(c), o.decompose_1d(x, levels, "direct"), x, 1, what="direct 1-D analysis")
+    c32 = o.decompose_1d(x, levels).astype(np.float32)
+    r = fhwt.direct_synthesize_1d(dev(c32), levels)
+    assert_close(host(r), o.reconstruct_1d(c32, levels, "direct"), x, 1, what="direct 1-D synthesis")
+    assert_close(host(fhwt.direct_synthesize_1d(c, levels)), x, x, 1, what="direct 1-D round trip")
+
+
+@pytest.mark.parametrize("h,w,batch,levels", [(64, 64, 2, 6), (96, 320, 1, 5), (8, 8, 3, 3), (6, 10, 1, 1)])
+def test_direct_form_2d(h, w, batch, levels):
+    x = datagen.uniform((batch, h, w), seed=h + w + levels)
+    c = fhwt.direct_analyze_2d(dev(x), levels)
+    assert_close(host(c), o.analyze_2d(x, levels, "direct"), x, 2, what="direct 2-D analysis")
+    c32 = o.analyze_2d(x, levels).astype(np.float32)
+    r = fhwt.direct_synthesize_2d(dev(c32), levels)
+    assert_close(host(r), o.synthesize_2d(c32, levels, "direct"), x, 2, what="direct 2-D synthesis")
+    assert_close(host(fhwt.direct_synthesize_2d(c, levels)), x, x, 2, what="direct 2-D round trip")
+
+
+# ------------------------------------------------------------------ §8(f) f4: dB report (Fig. 11)
+def test_error_db_approximation_bands():
+    """approximation data within -90 dB of the original Haar.  Per band, peak-normalised
+    (SPEC.md:305-313); fp32 kernels vs the fp64 direct oracle.  Detail bands are reported by
+    tools/error_db_report.py (the paper's -160 dB is below fp32 resolution)."""
+    x = datagen.c2_batch(0, 8)
+    c = host(fhwt.analyze_1d(dev(x), 10))
+    ref = o.decompose_1d(x, 10)
+    assert o.pointwise_error_db(c[:, :64], ref[:, :64]).max() <= -90.0
+    y = datagen.c4_batch(0, 2)
+    c2 = host(fhwt.analyze_2d(dev(y), 5))
+    ref2 = o.analyze_2d(y, 5)
+    assert o.pointwise_error_db(c2[:, :64, :64], ref2[:, :64, :64]).max() <= -90.0
