@@ -353,6 +353,45 @@ def measure_direct(name, cfg, d_host, steps=5):
             "mul_ratio_fast_over_direct": ops["fast"]["analysis_mul"] / ops["direct"]["analysis_mul"]}
 
 
+def measure_lowpass(steps=10):
+    """§8(f) f1: LL-only lowpass of the c4 images in their native uint8 form (Fig. 12):
+    reads 1 B/pixel, writes LL_5 only.  Algorithmic bytes per launch = S (uint8 in) + 4 S / 4^5."""
+    import torch
+
+    import datagen
+    import oracle
+    import paper_1002_2184_b200 as fhwt
+    cfg = WORKLOADS["c4"]
+    host = torch.empty((cfg["batch"], cfg["h"], cfg["w"]), dtype=torch.uint8).pin_memory()
+    datagen.generate("c4u8", count=cfg["batch"], out=host.numpy())
+    d = host.cuda()
+    L = cfg["levels"]
+    out = torch.empty((cfg["batch"], cfg["h"] >> L, cfg["w"] >> L), device="cuda")
+    for _ in range(3):
+        fhwt.lowpass_2d_u8(d, L, out=out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fhwt.lowpass_2d_u8(d, L, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    S = d.numel()
+    alg = S + 4 * S / 4 ** L
+    peak, src = measured_peak()
+    ref = oracle.analyze_2d(host[7].numpy().astype(np.float64), L)[: cfg["h"] >> L, : cfg["w"] >> L]
+    err = float(np.abs(out[7].double().cpu().numpy() - ref).max())
+    del d
+    torch.cuda.empty_cache()
+    return {"workload": "c4 images as uint8 (256 x 2048^2), LL_5 only", "ms": ms,
+            "gbs": alg / (ms * 1e-3) / 1e9, "gpix_per_s": S / (ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg / (ms * 1e-3) / 1e9 / peak, "peak_source": src,
+                         "algorithmic_bytes_per_launch": alg},
+            "parity": {"unit": "image 7", "max_abs_err_vs_oracle": err}}
+
+
 def measure_e2e(cfg, host, steps):
     """Same metric through the public host-buffer API: every step copies the pinned input H2D,
     runs DWT+IDWT and copies coefficients and d_R back D2H (fhwt_roundtrip_*_host)."""
@@ -486,6 +525,9 @@ def main():
         pg = dist.group.WORLD
     cfg = WORKLOADS[args.workload]
     res, (plan, host) = measure(args.workload, cfg, args, ws, rank, local, pg)
+    lowpass = None
+    if not args.no_breakdown and rank == 0:
+        lowpass = measure_lowpass()
     direct = None
     if not args.no_direct and rank == 0:
         direct = measure_direct(args.workload, cfg, host)
@@ -537,6 +579,7 @@ def main():
             "parity": res["parity"],
             "workloads": breakdown,
             "direct_form": direct,
+            "lowpass_u8": lowpass,
         }
         print(json.dumps(out), flush=True)
     if ws > 1:

@@ -109,6 +109,11 @@ def c4_image(i: int, size: int = 2048, seed: int = SEEDS["c4"]) -> np.ndarray:
     return u8.astype(np.float32) / np.float32(255.0)
 
 
+def c4_image_u8(i: int, size: int = 2048, seed: int = SEEDS["c4"]) -> np.ndarray:
+    """The 8-bit image behind c4_image(i) (for the uint8 lowpass path, §8(f) f1)."""
+    return image_u8(size, size, np.random.default_rng([seed, i]))
+
+
 def c4_batch(first: int, count: int, size: int = 2048, seed: int = SEEDS["c4"]) -> np.ndarray:
     return np.stack([c4_image(first + i, size, seed) for i in range(count)])
 
@@ -146,6 +151,9 @@ def _fill_worker(args):
         elif kind == "c4":
             for i in range(lo, hi):
                 arr[i] = c4_image(kw["first"] + i, size=shape[-1])
+        elif kind == "c4u8":
+            for i in range(lo, hi):
+                arr[i] = c4_image_u8(kw["first"] + i, size=shape[-1])
         elif kind == "c5":
             br = kw["band_rows"]
             arr[lo * br:hi * br] = c5_rows(kw["r0"] + lo * br, kw["r0"] + hi * br, size=kw["size"], band_rows=br)
@@ -164,12 +172,13 @@ def generate(kind: str, *, first: int = 0, count: int | None = None, size: int |
     import os
     from concurrent.futures import ProcessPoolExecutor
     from multiprocessing import shared_memory
-    cfg = CONFIGS[kind]
+    cfg = CONFIGS["c4" if kind == "c4u8" else kind]
+    dtype = np.uint8 if kind == "c4u8" else np.float32
     if kind == "c2":
         n = size or cfg["n"]
         count = cfg["batch"] if count is None else count
         shape, units, kw = (count, n), count, {"first": first}
-    elif kind == "c4":
+    elif kind in ("c4", "c4u8"):
         s = size or cfg["h"]
         count = cfg["batch"] if count is None else count
         shape, units, kw = (count, s, s), count, {"first": first}
@@ -181,11 +190,11 @@ def generate(kind: str, *, first: int = 0, count: int | None = None, size: int |
     else:
         raise ValueError(kind)
     workers = workers or min(32, len(os.sched_getaffinity(0)))
-    nbytes = int(np.prod(shape)) * 4
+    nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
     shm = shared_memory.SharedMemory(create=True, size=max(nbytes, 1))
     try:
         step = max(1, -(-units // (workers * 4)))
-        tasks = [(shm.name, shape, np.float32, kind, lo, min(units, lo + step), kw) for lo in range(0, units, step)]
+        tasks = [(shm.name, shape, dtype, kind, lo, min(units, lo + step), kw) for lo in range(0, units, step)]
         if workers <= 1 or len(tasks) <= 1:
             for t in tasks:
                 _fill_worker(t)
@@ -194,9 +203,9 @@ def generate(kind: str, *, first: int = 0, count: int | None = None, size: int |
             # forkserver: the caller may already hold CUDA / threads, where fork() is unsafe
             with ProcessPoolExecutor(workers, mp_context=mp.get_context("forkserver")) as ex:
                 list(ex.map(_fill_worker, tasks))
-        src = np.ndarray(shape, dtype=np.float32, buffer=shm.buf)
+        src = np.ndarray(shape, dtype=dtype, buffer=shm.buf)
         if out is None:
-            out = np.empty(shape, dtype=np.float32)
+            out = np.empty(shape, dtype=dtype)
         np.copyto(out.reshape(shape), src)
         del src
     finally:

@@ -144,6 +144,18 @@ fhwt_status fhwt_roundtrip_2d_host(const float *h_d, float *h_coeffs, float *h_d
 fhwt_status fhwt_roundtrip_1d_host(const float *h_d, float *h_coeffs, float *h_dR, int64_t n, int64_t batch,
                                    int levels, int64_t chunk);
 
+/* ------------------------------------------------------------------ LL-only lowpass path (§8(f) f1)
+ * The paper's image output (Fig. 12: "Lowpass output ... by applying ... Fast Haar
+ * wavelet"): only the LL branch of the separable Fast Haar analysis, LL_j = ½((a+b)+(c+d)) per 2x2
+ * block of LL_{j-1}, from 8-bit images.  d: [batch][h][w] uint8 (device, aligned to
+ * 2^min(levels,4) bytes); ll: [batch][h/2^levels][w/2^levels] fp32 (device) = the LL_levels band of
+ * fhwt_analyze_2d on the same image converted to fp32 (exact: integer sums below 2^53).
+ * workspace: fhwt_lowpass_workspace_bytes bytes (0 for levels <= 4), or NULL (stream-ordered
+ * allocation on s).  Errors as fhwt_plan_2d, plus MISALIGNED, INVALID_ARG, CUDA. */
+size_t fhwt_lowpass_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels);
+fhwt_status fhwt_lowpass_2d_u8(const uint8_t *d, float *ll, int64_t h, int64_t w, int64_t batch, int levels,
+                               void *workspace, fhwt_stream_t s);
+
 /* ------------------------------------------------------------------ direct-form baseline (§8(f) f3)
  * The paper's ORIGINAL structure, for comparison with the Fast structure on the same hardware:
  * analysis = full-rate filtering with b0/b1 then decimation keeping n = 2k+1 (Fig. 2, Eqs. (1)-(4),

@@ -934,3 +934,30 @@ extern "C" fhwt_status fhwt_op_counts(int dims, int64_t n_or_h, int64_t w, int64
   *add = A * uint64_t(batch);
   return FHWT_OK;
 }
+
+// ---------------------------------------------------------------------- LL-only lowpass (f1)
+extern "C" size_t fhwt_lowpass_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels) {
+  if (check_2d(h, w, batch, levels) != FHWT_OK) return 0;
+  return lowpass_workspace_bytes(h, w, batch, levels);
+}
+
+extern "C" fhwt_status fhwt_lowpass_2d_u8(const uint8_t* d, float* ll, int64_t h, int64_t w, int64_t batch,
+                                          int levels, void* workspace, fhwt_stream_t st) {
+  FHWT_TRY(check_2d(h, w, batch, levels));
+  if (!d || !ll) return fail(FHWT_ERR_INVALID_ARG, "null buffer pointer");
+  const int M = levels < 4 ? levels : 4;
+  if ((reinterpret_cast<uintptr_t>(d) & ((uintptr_t(1) << M) - 1)) || (reinterpret_cast<uintptr_t>(ll) & 3))
+    return fail(FHWT_ERR_MISALIGNED, "uint8 input must be %d-byte aligned (one vector row load per block)", 1 << M);
+  const char* a = reinterpret_cast<const char*>(d);
+  const char* b = reinterpret_cast<const char*>(ll);
+  const size_t in_bytes = size_t(batch) * h * w, out_bytes = size_t(batch) * (h >> levels) * (w >> levels) * 4;
+  if (a < b + out_bytes && b < a + in_bytes) return fail(FHWT_ERR_INVALID_ARG, "input and output buffers overlap");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  const size_t wsb = lowpass_workspace_bytes(h, w, batch, levels);
+  void* ws = workspace;
+  if (wsb && !ws) FHWT_CUDA(cudaMallocAsync(&ws, wsb, s), "lowpass workspace");
+  cudaError_t e = launch_lowpass_u8(d, ll, h, w, batch, levels, ws, s);
+  if (wsb && !workspace) cudaFreeAsync(ws, s);
+  if (e != cudaSuccess) return cuda_fail(e, "lowpass launch");
+  return FHWT_OK;
+}

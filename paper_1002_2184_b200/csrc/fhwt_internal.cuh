@@ -115,6 +115,11 @@ cudaError_t direct_analysis_lines(const float* x, Lines_t lx, float* a, Lines_t 
 cudaError_t direct_synthesis_lines(const float* a, Lines_t la, const float* d, Lines_t ld, float* r, Lines_t lr,
                                    float* u0, float* u1, cudaStream_t s);
 
+// LL-only uint8 lowpass path (lowpass.cu, §8(f) f1)
+size_t lowpass_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels);
+cudaError_t launch_lowpass_u8(const uint8_t* d, float* ll, int64_t h, int64_t w, int64_t batch, int levels, void* ws,
+                              cudaStream_t s);
+
 void count_launch();
 
 // ------------------------------------------------------------------ device helpers

@@ -235,3 +235,41 @@ def test_error_db_approximation_bands():
     c2 = host(fhwt.analyze_2d(dev(y), 5))
     ref2 = o.analyze_2d(y, 5)
     assert o.pointwise_error_db(c2[:, :64, :64], ref2[:, :64, :64]).max() <= -90.0
+
+
+# ------------------------------------------------------------------ §8(f) f1: LL-only uint8 lowpass
+@pytest.mark.parametrize("h,w,batch,levels", [(512, 512, 1, 1), (512, 512, 1, 2), (512, 512, 1, 3), (8, 8, 3, 3),
+                                              (64, 96, 2, 5), (512, 512, 2, 9), (32, 64, 1, 4), (2, 2, 1, 1)])
+def test_lowpass_u8_exact(h, w, batch, levels):
+    """Fig. 12's lowpass output from 8-bit images: exact (IEEE ==) against the exact
+    integer closed form, and identical to the LL band of the full fused analysis."""
+    rng = np.random.default_rng(h * w + levels)
+    u8 = rng.integers(0, 256, (batch, h, w), dtype=np.uint8)
+    ll = fhwt.lowpass_2d_u8(torch.from_numpy(u8).cuda(), levels)
+    hl, wl = h >> levels, w >> levels
+    exact = closed_form_2d(u8.astype(np.int64), levels, exact_int=True)[:, :hl, :wl]
+    got = host(ll)
+    assert np.array_equal(got, exact), f"{np.count_nonzero(got != exact)} LL values differ"
+    full = host(fhwt.analyze_2d(dev(u8.astype(np.float32)), levels))[:, :hl, :wl]
+    assert np.array_equal(got, full)
+
+
+def test_lowpass_u8_c3_and_c4_images():
+    x = datagen.image_u8(512, 512, np.random.default_rng(datagen.SEEDS["c3"]))       # the c3 image, uint8
+    for L in (1, 3):
+        got = host(fhwt.lowpass_2d_u8(torch.from_numpy(x).cuda(), L))
+        assert np.array_equal(got, closed_form_2d(x.astype(np.int64), L, exact_int=True)[:512 >> L, :512 >> L])
+    y = np.stack([datagen.c4_image_u8(i) for i in range(2)])
+    got = host(fhwt.lowpass_2d_u8(torch.from_numpy(y).cuda(), 5))
+    ref = o.analyze_2d(y.astype(np.float64), 5)[:, :64, :64]
+    assert np.abs(got - ref).max() <= 1e-9 * 255 * 32
+
+
+def test_lowpass_u8_errors():
+    buf = torch.zeros(1 + 64 * 64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(fhwt.Misaligned):
+        fhwt.lowpass_2d_u8(buf[1:].view(64, 64), 4)
+    with pytest.raises(fhwt.InsufficientLength):
+        fhwt.lowpass_2d_u8(torch.zeros(24, 24, dtype=torch.uint8, device="cuda"), 4)
+    with pytest.raises(fhwt.InvalidArgument):
+        fhwt.lowpass_2d_u8(torch.zeros(16, 16, device="cuda"), 2)
