@@ -189,6 +189,25 @@ fhwt_status check_2d(int64_t h, int64_t w, int64_t batch, int levels) {
   return FHWT_OK;
 }
 
+// Stream-ordered workspace allocations (one-shot calls) come from the device's default memory pool;
+// raising its release threshold keeps freed blocks cached instead of returning them to the driver
+// at every synchronisation (which made each call pay a fresh allocation).
+fhwt_status ws_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static std::once_flag flags[64];
+  int dev = 0;
+  FHWT_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev >= 0 && dev < 64)
+    std::call_once(flags[dev], [dev] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    });
+  FHWT_CUDA(cudaMallocAsync(p, bytes, s), "workspace cudaMallocAsync");
+  return FHWT_OK;
+}
+
 fhwt_status check_ptrs(const void* in, const void* out, size_t bytes) {
   if (!in || !out) return fail(FHWT_ERR_INVALID_ARG, "null buffer pointer");
   const char* a = static_cast<const char*>(in);
@@ -496,7 +515,7 @@ fhwt_status run(fhwt_plan p, const float* in, float* out, void* workspace, fhwt_
   bool owned = false;
   if (p->ws_bytes && !ws) {
     void* t = nullptr;
-    FHWT_CUDA(cudaMallocAsync(&t, p->ws_bytes, s), "workspace cudaMallocAsync");
+    FHWT_TRY(ws_alloc(&t, p->ws_bytes, s));
     ws = static_cast<char*>(t);
     owned = true;
   }
@@ -681,8 +700,7 @@ fhwt_status roundtrip_host(fhwt_plan_s* full, const float* h_d, float* h_c, floa
   fhwt_status rs = FHWT_OK;
   for (int i = 0; i < 2 && rs == FHWT_OK; ++i) {
     void* t = nullptr;
-    cudaError_t e = cudaMallocAsync(&t, 3 * align_up(cbytes, 256) + wsb, st[i]);
-    if (e != cudaSuccess) rs = cuda_fail(e, "staging cudaMallocAsync");
+    rs = ws_alloc(&t, 3 * align_up(cbytes, 256) + wsb, st[i]);
     buf[i] = static_cast<char*>(t);
   }
   for (int64_t u0 = 0, it = 0; u0 < B && rs == FHWT_OK; u0 += chunk, ++it) {
@@ -955,7 +973,7 @@ extern "C" fhwt_status fhwt_lowpass_2d_u8(const uint8_t* d, float* ll, int64_t h
   cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
   const size_t wsb = lowpass_workspace_bytes(h, w, batch, levels);
   void* ws = workspace;
-  if (wsb && !ws) FHWT_CUDA(cudaMallocAsync(&ws, wsb, s), "lowpass workspace");
+  if (wsb && !ws) FHWT_TRY(ws_alloc(&ws, wsb, s));
   cudaError_t e = launch_lowpass_u8(d, ll, h, w, batch, levels, ws, s);
   if (wsb && !workspace) cudaFreeAsync(ws, s);
   if (e != cudaSuccess) return cuda_fail(e, "lowpass launch");

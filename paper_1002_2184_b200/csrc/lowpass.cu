@@ -35,9 +35,20 @@ struct RowVec<1> {
 };
 
 template <int M>
-__device__ __forceinline__ void unpack_row(const uint8_t* p, float (&v)[1 << M]) {
+__device__ __forceinline__ typename RowVec<M>::T load_row(const uint8_t* p) {
   using T = typename RowVec<M>::T;
-  const T t = __ldg(reinterpret_cast<const T*>(p));
+  if constexpr (M == 4) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+  } else {
+    return __ldg(reinterpret_cast<const T*>(p));
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void unpack(const typename RowVec<M>::T& t, float (&v)[1 << M]) {
   const uint8_t* b = reinterpret_cast<const uint8_t*>(&t);
 #pragma unroll
   for (int i = 0; i < (1 << M); ++i) v[i] = float(b[i]);
@@ -55,13 +66,16 @@ __global__ void __launch_bounds__(256) lowpass_stage_a(const uint8_t* __restrict
     const int64_t b = i / (bh * bw), rem = i - b * bh * bw;
     const int64_t r = rem / bw, c = rem - r * bw;
     const uint8_t* src = d + (b * h + r * N) * w + c * N;
-    // level 1 on row pairs as they arrive
+    // all 2^M row loads first (2^M x 2^M bytes in flight per thread), then the levels
+    typename RowVec<M>::T raw[N];
+#pragma unroll
+    for (int y = 0; y < N; ++y) raw[y] = load_row<M>(src + int64_t(y) * w);
     float l1[N / 2][N / 2];
 #pragma unroll
     for (int y = 0; y < N; y += 2) {
       float r0[N], r1[N];
-      unpack_row<M>(src + int64_t(y) * w, r0);
-      unpack_row<M>(src + int64_t(y + 1) * w, r1);
+      unpack<M>(raw[y], r0);
+      unpack<M>(raw[y + 1], r1);
 #pragma unroll
       for (int x = 0; x < N; x += 2) l1[y / 2][x / 2] = ((r0[x] + r0[x + 1]) + (r1[x] + r1[x + 1])) * 0.5f;
     }
@@ -98,6 +112,102 @@ __global__ void __launch_bounds__(256) lowpass_stage_a(const uint8_t* __restrict
   }
 }
 
+// Wide variant (w % 16 == 0): one thread per 2^M rows x 16 columns — every row is one 16-B load,
+// all issued before the arithmetic — producing 16 >> M consecutive LL_M values.
+// The butterfly chain LL_j = ½((a+b)+(c+d)) is carried as the exact integer sums S_j = 2^j LL_j
+// (S_j = sum of the four S_{j-1}), two 16-bit lanes per register for level 1 (SWAR: no per-byte
+// int->float conversion, which is a quarter-rate pipe and bounded this kernel at ~4 TB/s), and the
+// exact power-of-two scale 2^-M is applied once.  For uint8 input this is bit-identical to the
+// floating-point butterflies (all values are exact dyadic rationals), which the tests assert.
+__device__ __forceinline__ uint32_t pair_sums(uint32_t w) {  // bytes b0..b3 -> lanes [b0+b1, b2+b3]
+  return (w & 0x00FF00FFu) + ((w >> 8) & 0x00FF00FFu);
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) lowpass_stage_a_wide(const uint8_t* __restrict__ d, float* __restrict__ out32,
+                                                            uint32_t* __restrict__ out_s4, int64_t h, int64_t w,
+                                                            int64_t batch) {
+  constexpr int R = 1 << M, NO = 16 >> M;
+  const int64_t bh = h >> M, bw = w >> 4;   // row blocks, 16-column groups
+  const int64_t total = batch * bh * bw;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / (bh * bw), rem = i - b * bh * bw;
+    const int64_t r = rem / bw, g = rem - r * bw;
+    const uint8_t* src = d + (b * h + r * R) * w + g * 16;
+    uint4 raw[R];
+#pragma unroll
+    for (int y = 0; y < R; ++y) raw[y] = load_row<4>(src + int64_t(y) * w);
+    // level 1: S1 = a + b + c + d per 2x2 block, lanes [S1(2k), S1(2k+1)] of word k (<= 1020)
+    uint32_t s1[R / 2][4];
+#pragma unroll
+    for (int y = 0; y < R / 2; ++y) {
+      const uint32_t t[4] = {raw[2 * y].x, raw[2 * y].y, raw[2 * y].z, raw[2 * y].w};
+      const uint32_t u[4] = {raw[2 * y + 1].x, raw[2 * y + 1].y, raw[2 * y + 1].z, raw[2 * y + 1].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s1[y][k] = pair_sums(t[k]) + pair_sums(u[k]);
+    }
+    const int64_t o = (b * bh + r) * (w >> M) + g * NO;
+    if constexpr (M == 1) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[2 * k] = float(s1[0][k] & 0xFFFFu) * 0.5f;
+        v[2 * k + 1] = float(s1[0][k] >> 16) * 0.5f;
+      }
+      stg_stream4(out32 + o, make_float4(v[0], v[1], v[2], v[3]));      // o is a multiple of 8
+      stg_stream4(out32 + o + 4, make_float4(v[4], v[5], v[6], v[7]));
+    } else {
+      // level 2: S2 = sum of a 2x2 block of S1 (lanes of one word, two row pairs)
+      uint32_t s2[R / 4][4];
+#pragma unroll
+      for (int y = 0; y < R / 4; ++y)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          s2[y][k] = ((s1[2 * y][k] & 0xFFFFu) + (s1[2 * y][k] >> 16)) +
+                     ((s1[2 * y + 1][k] & 0xFFFFu) + (s1[2 * y + 1][k] >> 16));
+      if constexpr (M == 2) {
+        stg_stream4(out32 + o, make_float4(float(s2[0][0]) * 0.25f, float(s2[0][1]) * 0.25f, float(s2[0][2]) * 0.25f,
+                                           float(s2[0][3]) * 0.25f));
+      } else {
+        uint32_t s3[R / 8][2];
+#pragma unroll
+        for (int y = 0; y < R / 8; ++y)
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            s3[y][k] = (s2[2 * y][2 * k] + s2[2 * y][2 * k + 1]) + (s2[2 * y + 1][2 * k] + s2[2 * y + 1][2 * k + 1]);
+        if constexpr (M == 3) {
+          out32[o] = float(s3[0][0]) * 0.125f;
+          out32[o + 1] = float(s3[0][1]) * 0.125f;
+        } else {  // level 4 (fp64 per DESIGN.md §5; exact either way)
+          const uint32_t s4 = (s3[0][0] + s3[0][1]) + (s3[1][0] + s3[1][1]);
+          if (out_s4)
+            out_s4[o] = s4;   // exact hand-off to the remaining levels
+          else
+            out32[o] = float(double(s4) * 0.0625);
+        }
+      }
+    }
+  }
+}
+
+// Levels 5..L in one launch, from the exact S4 = 16 LL_4 sums of the wide stage A: one thread per
+// LL_L value sums its 2^(L-4) x 2^(L-4) block of S4 (S_L = sum of the four S_{L-1}, recursively:
+// integer addition is exact, so the association order does not matter) and scales by 2^-L in fp64.
+__global__ void lowpass_stage_b_s4(const uint32_t* __restrict__ s4, int64_t rows4, int64_t cols4, int64_t batch,
+                                   int k, int levels, float* __restrict__ out) {
+  const int64_t n = int64_t(1) << k, orow = rows4 >> k, ocol = cols4 >> k, total = batch * orow * ocol;
+  const double scale = 1.0 / double(int64_t(1) << levels);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / (orow * ocol), rem = i - b * orow * ocol;
+    const int64_t r = rem / ocol, c = rem - r * ocol;
+    const uint32_t* p = s4 + (b * rows4 + r * n) * cols4 + c * n;
+    uint64_t acc = 0;
+    for (int64_t y = 0; y < n; ++y)
+      for (int64_t x = 0; x < n; ++x) acc += p[y * cols4 + x];
+    out[i] = float(double(acc) * scale);
+  }
+}
+
 // One further level on the fp64 chain: LL_{j} (rows x cols per image) -> LL_{j+1}.
 __global__ void lowpass_stage_b(const double* __restrict__ in, int64_t rows, int64_t cols, int64_t batch,
                                 double* __restrict__ out64, float* __restrict__ out32) {
@@ -114,18 +224,20 @@ __global__ void lowpass_stage_b(const double* __restrict__ in, int64_t rows, int
   }
 }
 
-int grid_lp(int64_t total) {
+int grid_lp(int64_t total) {   // grid-stride kernels: at most ~64 waves of resident CTAs
   int64_t g = (total + 255) / 256;
   if (g > 148 * 64) g = 148 * 64;
   return int(g < 1 ? 1 : g);
 }
+
+int grid_exact(int64_t total) { return int((total + 255) / 256); }
 
 }  // namespace
 
 size_t lowpass_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels) {
   if (levels <= 4) return 0;
   const int64_t n4 = batch * (h >> 4) * (w >> 4);
-  return size_t(n4 + n4 / 4 + 16) * sizeof(double);   // LL_4 chain + one ping-pong partner
+  return size_t(n4 + n4 / 4 + 16) * sizeof(double);   // LL_4 chain + one ping-pong partner (or the S4 sums)
 }
 
 cudaError_t launch_lowpass_u8(const uint8_t* d, float* ll, int64_t h, int64_t w, int64_t batch, int levels, void* ws,
@@ -135,11 +247,30 @@ cudaError_t launch_lowpass_u8(const uint8_t* d, float* ll, int64_t h, int64_t w,
   double* chain = levels > 4 ? static_cast<double*>(ws) : nullptr;
   float* out_a = levels > 4 ? nullptr : ll;
   count_launch();
-  switch (M) {
-    case 1: lowpass_stage_a<1><<<grid_lp(n_a), 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
-    case 2: lowpass_stage_a<2><<<grid_lp(n_a), 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
-    case 3: lowpass_stage_a<3><<<grid_lp(n_a), 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
-    default: lowpass_stage_a<4><<<grid_lp(n_a), 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
+  const int64_t n_wide = batch * (h >> M) * (w >> 4);
+  if (w % 16 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0 && (reinterpret_cast<uintptr_t>(ll) & 15) == 0 &&
+      n_wide < (int64_t(1) << 31) - 256) {
+    const int g = grid_exact(n_wide);
+    uint32_t* s4 = levels > 4 ? static_cast<uint32_t*>(ws) : nullptr;
+    switch (M) {
+      case 1: lowpass_stage_a_wide<1><<<g, 256, 0, s>>>(d, out_a, s4, h, w, batch); break;
+      case 2: lowpass_stage_a_wide<2><<<g, 256, 0, s>>>(d, out_a, s4, h, w, batch); break;
+      case 3: lowpass_stage_a_wide<3><<<g, 256, 0, s>>>(d, out_a, s4, h, w, batch); break;
+      default: lowpass_stage_a_wide<4><<<g, 256, 0, s>>>(d, out_a, s4, h, w, batch); break;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || levels <= 4) return e;
+    const int64_t nL = batch * (h >> levels) * (w >> levels);
+    count_launch();
+    lowpass_stage_b_s4<<<grid_lp(nL), 256, 0, s>>>(s4, h >> 4, w >> 4, batch, levels - 4, levels, ll);
+    return cudaGetLastError();
+  } else {
+    switch (M) {
+      case 1: lowpass_stage_a<1><<<grid_lp(n_a), 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
+      case 2: lowpass_stage_a<2><<<grid_lp(n_a), 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
+      case 3: lowpass_stage_a<3><<<grid_lp(n_a), 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
+      default: lowpass_stage_a<4><<<grid_lp(n_a), 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
+    }
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || levels <= 4) return e;
