@@ -1,0 +1,66 @@
+"""Randomised GPU parity sweep: seeded random (shape, levels, batch) draws across the 1-D and 2-D
+paths (fast tiles, generic tiles, ragged tiles, scalar single-level, multi-pass), each checked
+against the fp64 oracle at the north_star tolerance, round trip included."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle as o
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1002_2184_b200 as fhwt  # noqa: E402
+
+TOL = 1e-5
+
+
+def _draw_2d(rng):
+    L = int(rng.integers(1, 9))
+    h = (1 << L) * int(rng.integers(1, max(2, 512 >> L) + 1))
+    w = (1 << L) * int(rng.integers(1, max(2, 1024 >> L) + 1))
+    if h * w > 1 << 19:
+        h = 1 << L
+    return h, w, int(rng.integers(1, 4)), L
+
+
+def _draw_1d(rng):
+    J = int(rng.integers(1, 15))
+    n = (1 << J) * int(rng.integers(1, max(2, (1 << 15) >> J) + 1))
+    return n, int(rng.integers(1, 5)), J
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_2d(seed):
+    rng = np.random.default_rng(1000 + seed)
+    h, w, b, L = _draw_2d(rng)
+    x = datagen.uniform((b, h, w), seed=seed, lo=-2.0, hi=3.0)
+    xd = torch.from_numpy(x).cuda()
+    c = fhwt.analyze_2d(xd, L)
+    r = fhwt.synthesize_2d(c, L)
+    torch.cuda.synchronize()
+    scale = np.abs(x).max(axis=(1, 2), keepdims=True)
+    ref = o.analyze_2d(x, L)
+    assert (np.abs(c.double().cpu().numpy() - ref) / scale).max() <= TOL, (h, w, b, L)
+    assert (np.abs(r.double().cpu().numpy() - x) / scale).max() <= TOL, (h, w, b, L)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_1d(seed):
+    rng = np.random.default_rng(2000 + seed)
+    n, b, J = _draw_1d(rng)
+    x = datagen.uniform((b, n), seed=seed, lo=-3.0, hi=1.0)
+    xd = torch.from_numpy(x).cuda()
+    c = fhwt.analyze_1d(xd, J)
+    r = fhwt.synthesize_1d(c, J)
+    torch.cuda.synchronize()
+    scale = np.abs(x).max(axis=1, keepdims=True)
+    ref = o.decompose_1d(x, J)
+    # deep 1-D levels: coefficients reach 2^(J/2) max|d|; fp32 output rounding alone is
+    # 2^(J/2 - 24) max|d|, so the bar is the north_star's 1e-5 or that floor
+    tol = max(TOL, 4 * 2.0 ** (J / 2 - 24))
+    assert (np.abs(c.double().cpu().numpy() - ref) / scale).max() <= tol, (n, b, J)
+    assert (np.abs(r.double().cpu().numpy() - x) / scale).max() <= TOL, (n, b, J)
