@@ -33,7 +33,7 @@ def main():
         return s.elapsed_time(e) / reps
 
 
-    for ldg, tc, st in itertools.product((0, 2), (256,), (2, 3)):
+    for ldg, tc, st in [(0, 256, 2), (2, 256, 2), (0, 512, 2), (0, 512, 3), (2, 512, 2), (2, 512, 3)]:
         os.environ.update(FHWT_SYN_MODE=str(ldg), FHWT_SYN_TC=str(tc), FHWT_SYN_STAGES=str(st))
         try:
             t = timeit(lambda: plan.synthesize(c, out=r))
