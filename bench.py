@@ -353,6 +353,64 @@ def measure_direct(name, cfg, d_host, steps=5):
             "mul_ratio_fast_over_direct": ops["fast"]["analysis_mul"] / ops["direct"]["analysis_mul"]}
 
 
+def measure_latency(iters=200):
+    """c1 (1 x 1024, J=1) and c3 (512^2, L=3) are latency-bound: microseconds per
+    DWT+IDWT, eager launches vs one CUDA graph replay of the two launches; parity of the output."""
+    import torch
+
+    import datagen
+    import oracle
+    import paper_1002_2184_b200 as fhwt
+    out = {}
+    cases = {"c1": (datagen.c1_signal()[None], fhwt.Plan1d(1024, 1, 1), 1),
+             "c3": (datagen.c3_image()[None], fhwt.Plan2d(512, 512, 1, 3), 3)}
+    for name, (x_np, plan, L) in cases.items():
+        x = torch.from_numpy(x_np).cuda()
+        c = torch.empty_like(x)
+        r = torch.empty_like(x)
+
+        def step():
+            plan.analyze(x, out=c)
+            plan.synthesize(c, out=r)
+
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        eager = e0.elapsed_time(e1) / iters * 1e3
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step()
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(g):
+            step()
+        for _ in range(20):
+            g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        graph = e0.elapsed_time(e1) / iters * 1e3
+        if x_np.ndim == 2:
+            ref = oracle.decompose_1d(x_np, L)
+        else:
+            ref = oracle.analyze_2d(x_np, L)
+        err = float(np.abs(c.double().cpu().numpy() - ref).max() / np.abs(x_np).max())
+        rt = float((r - x).abs().max() / x.abs().max())
+        out[name] = {"eager_us_per_dwt_idwt": eager, "graph_us_per_dwt_idwt": graph, "samples": x.numel(),
+                     "max_err_rel": err, "roundtrip_err_rel": rt}
+    return out
+
+
 def measure_lowpass(steps=10):
     """§8(f) f1: LL-only lowpass of the c4 images in their native uint8 form (Fig. 12):
     reads 1 B/pixel, writes LL_5 only.  Algorithmic bytes per launch = S (uint8 in) + 4 S / 4^5."""
@@ -539,9 +597,10 @@ def main():
         pg = dist.group.WORLD
     cfg = WORKLOADS[args.workload]
     res, (plan, host) = measure(args.workload, cfg, args, ws, rank, local, pg)
-    lowpass = None
+    lowpass = latency = None
     if not args.no_breakdown and rank == 0:
         lowpass = measure_lowpass()
+        latency = measure_latency()
     direct = None
     if not args.no_direct and rank == 0:
         direct = measure_direct(args.workload, cfg, host)
@@ -594,6 +653,7 @@ def main():
             "workloads": breakdown,
             "direct_form": direct,
             "lowpass_u8": lowpass,
+            "latency": latency,
         }
         print(json.dumps(out), flush=True)
     if ws > 1:

@@ -214,8 +214,12 @@ def _shape_2d(x):
 
 
 def _guard_device(x):
+    import contextlib
+
     import torch
     _dev_f32(x, "input")          # validate (CUDA, float32, contiguous) before touching the device
+    if x.device.index == torch.cuda.current_device():
+        return contextlib.nullcontext()
     return torch.cuda.device(x.device)
 
 

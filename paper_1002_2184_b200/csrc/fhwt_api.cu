@@ -386,10 +386,10 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     bool fast = p.TR == 32 && (p.TC == 256 || p.TC == 128) && p.Win % p.TC == 0 && p.out_pitch % 4 == 0 &&
                 (W >> (ps.g0 + 1)) % 2 == 0;
     for (int j = 1; j <= ps.Lp; ++j) fast = fast && p.hoff[j] == 0 && bw[j] == (p.TC >> j);
-    // load path of the fast variant: 0 TMA boxes, 1 LDG level-1 bands, 2 cp.async (LDGSTS) for all
-    // boxes.  Measured on B200 (tools/sweep_syn.py): 2 = 6.10 TB/s, 0 = 5.86, 1 = 5.19.
-    const int mode = fast ? env_int("FHWT_SYN_MODE", 2) : 0;
-    p.l1_ldg = mode == 1;
+    // load path of the fast variant: 0 TMA boxes, 2 cp.async (LDGSTS) for all boxes.  Measured on
+    // B200 (tools/sweep_syn.py): cp.async 6.10 TB/s, TMA boxes 5.86 (register LDG of level 1: 5.19).
+    const int mode = fast ? (env_int("FHWT_SYN_MODE", 2) == 0 ? 0 : 2) : 0;
+    p.l1_ldg = 0;
     // stage layout: LL box, then per level j three boxes (128-B aligned: TMA destinations need it;
     // with cp.async a 16-B packing would admit a 3rd CTA/SM, which measured slower: 5.54 vs 6.10 TB/s)
     const size_t balign = 128;

@@ -363,21 +363,6 @@ __device__ __forceinline__ void syn_tile(const Syn2dParams& p, unsigned char* st
 }
 
 // Fast tile: 32 x TCF full tiles, hoff = 0, LP known at compile time (box pitch = TCF >> j).
-// Coarse levels J..2 from the TMA stage; leaves LL_1 in P[1].
-template <int J, int TCF>
-__device__ __forceinline__ void syn_fast_coarse(const Syn2dParams& p, unsigned char* stage, unsigned char* smem,
-                                                const float* ll, int64_t b, int64_t row0, int64_t col0) {
-  static_assert(J >= 2, "level 1 runs from registers");
-  constexpr int R = 32 >> J, C = TCF >> J;
-  const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]);
-  const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]);
-  const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]);
-  float* dst = reinterpret_cast<float*>(smem + p.p_off[(J - 1) & 1]);
-  syn_level<2, R, C, true>(p, ll, C, hl, lh, hh, C, R, C, true, b, row0, col0, dst);
-  __syncthreads();
-  if constexpr (J > 2) syn_fast_coarse<J - 1, TCF>(p, stage, smem, dst, b, row0, col0);
-}
-
 // All levels J..1 from the TMA stage (level 1 writes the output tile).
 template <int J, int TCF>
 __device__ __forceinline__ void syn_fast_step(const Syn2dParams& p, unsigned char* stage, unsigned char* smem,
@@ -437,31 +422,6 @@ __device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned
   cp_async_commit();
 }
 
-// Level-1 band values of one tile, held in registers (fast synthesis): unit k of this thread is
-// row r = u / UPR, cols 2c, 2c+1 with u = tid + 256 k (same mapping as syn_level<2>).
-template <int TCF>
-struct L1Bands {
-  static constexpr int C1 = TCF / 2, UPR = C1 / 2, N = 16 * UPR / kThreads2d;
-  float2 hl[N], lh[N], hh[N];
-  __device__ __forceinline__ void load(const Syn2dParams& p, int64_t t) {
-    const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
-    const int64_t b = rt / p.tiles_r;
-    const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = ct * p.TC;
-    const int g = p.g0 + 1;
-    const int64_t hgW = (p.H >> g) * p.W, wg = p.W >> g;
-    const float* base = p.coeffs + (b * p.H + (row0 >> 1)) * p.W + (col0 >> 1);
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      const int u = int(threadIdx.x) + k * kThreads2d;
-      const int r = u / UPR, c = (u % UPR) * 2;
-      const float* q = base + int64_t(r) * p.W + c;
-      hl[k] = ldg_stream2(q + wg);
-      lh[k] = ldg_stream2(q + hgW);
-      hh[k] = ldg_stream2(q + hgW + wg);
-    }
-  }
-};
-
 // Issues the TMA loads of tile t into one stage (LL box + 3 band boxes per level; level 1 is
 // skipped when it is read by LDG).  Called by all of warp 0; lane 0 issues.
 __device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* base,
@@ -506,7 +466,8 @@ __device__ __forceinline__ void cp_async_wait_rt(int n) {  // runtime-N wrapper 
   }
 }
 
-// MODE 0: all boxes by TMA; 1: level-1 bands by register LDG; 2: everything by cp.async (LDGSTS)
+// MODE 0: all boxes by TMA; 2: everything by cp.async (LDGSTS).  (A register-LDG level-1 variant
+// measured 5.19 TB/s vs 6.10 for cp.async and was removed; tools/sweep_syn.py history in profiles/.)
 template <int LPFAST, int TCF, int MODE>
 __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const __grid_constant__ Syn2dParams p,
                                                            const __grid_constant__ TmaMaps2d maps) {
@@ -522,7 +483,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const 
   __syncthreads();
   uint64_t pol = 0;
   auto issue = [&](int64_t t, int s) { syn_issue_tile(p, maps, smem + s * p.stage_bytes, &bars[s], t, pol); };
-  constexpr bool L1LDG = MODE == 1, CPASYNC = MODE == 2 && LPFAST > 0;
+  constexpr bool CPASYNC = MODE == 2 && LPFAST > 0;
   if constexpr (CPASYNC) {
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
@@ -538,9 +499,6 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const 
       if (t < p.ntiles) issue(t, s);
     }
   }
-  [[maybe_unused]] L1Bands<(LPFAST > 0 ? TCF : 256)> l1;
-  if constexpr (LPFAST > 0 && L1LDG)
-    if (blockIdx.x < p.ntiles) l1.load(p, blockIdx.x);
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
     const int s = it % p.stages;
@@ -554,42 +512,9 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const 
     const int64_t b = rt / p.tiles_r;
     const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
     unsigned char* stage = smem + s * p.stage_bytes;
-    if constexpr (LPFAST > 0 && !L1LDG) {
+    if constexpr (LPFAST > 0) {
       syn_fast_step<LPFAST, TCF>(p, stage, smem, reinterpret_cast<const float*>(stage + p.box_off[0][0]), b, row0,
                                  ct * p.TC);
-    } else if constexpr (LPFAST > 0) {
-      const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]);
-      if constexpr (LPFAST >= 2) {
-        syn_fast_coarse<LPFAST, TCF>(p, stage, smem, ll, b, row0, ct * p.TC);
-        ll = reinterpret_cast<const float*>(smem + p.p_off[1]);
-      }
-      // level 1: LL_1 from smem, bands from registers; the next tile's bands are requested as soon
-      // as these registers are consumed, so their HBM latency overlaps the next tile's coarse levels.
-      using B1 = L1Bands<TCF>;
-      float4 top[B1::N], bot[B1::N];
-#pragma unroll
-      for (int k = 0; k < B1::N; ++k) {
-        const int u = tid + k * kThreads2d;
-        const int r = u / B1::UPR, c = (u % B1::UPR) * 2;
-        const float2 vll = *reinterpret_cast<const float2*>(ll + r * B1::C1 + c);
-        const float s0 = vll.x + l1.lh[k].x, t0 = l1.hl[k].x + l1.hh[k].x;
-        const float u0 = vll.x - l1.lh[k].x, w0 = l1.hl[k].x - l1.hh[k].x;
-        const float s1 = vll.y + l1.lh[k].y, t1 = l1.hl[k].y + l1.hh[k].y;
-        const float u1 = vll.y - l1.lh[k].y, w1 = l1.hl[k].y - l1.hh[k].y;
-        top[k] = make_float4((s0 + t0) * 0.5f, (s0 - t0) * 0.5f, (s1 + t1) * 0.5f, (s1 - t1) * 0.5f);
-        bot[k] = make_float4((u0 + w0) * 0.5f, (u0 - w0) * 0.5f, (u1 + w1) * 0.5f, (u1 - w1) * 0.5f);
-      }
-      const int64_t next = tile + gridDim.x;
-      if (next < p.ntiles) l1.load(p, next);
-      float* obase = p.out + (b * p.Hin + row0) * p.out_pitch + ct * p.TC;
-#pragma unroll
-      for (int k = 0; k < B1::N; ++k) {
-        const int u = tid + k * kThreads2d;
-        const int r = u / B1::UPR, c = (u % B1::UPR) * 2;
-        float* o = obase + int64_t(2 * r) * p.out_pitch + 2 * c;
-        stg_stream4(o, top[k]);
-        stg_stream4(o + p.out_pitch, bot[k]);
-      }
     } else {
       syn_tile(p, stage, smem, b, row0, ct * p.TC);
     }
@@ -704,16 +629,13 @@ static const void* ana2d_fn(bool in_f64, int fast_lp) {
   return ((fast_lp >> 4) & 0xfff) == 128 ? ana2d_fast_fn<128>(fast_lp & 15) : ana2d_fast_fn<256>(fast_lp & 15);
 }
 
-// synthesis fast_lp additionally carries the load mode (0 TMA, 1 LDG level 1, 2 cp.async) in bits 16+
+// synthesis fast_lp additionally carries the load mode (0 TMA, 2 cp.async) in bits 16+
 static const void* syn2d_fn(int fast_lp) {
   if (fast_lp == 0) return (const void*)syn2d_kernel<0, 0, 0>;
   const int mode = (fast_lp >> 16) & 3;
   const int tc = (fast_lp >> 4) & 0xfff;
-  if (tc == 128)
-    return mode == 2 ? syn2d_fast_fn<128, 2>(fast_lp & 15)
-         : mode == 1 ? syn2d_fast_fn<128, 1>(fast_lp & 15) : syn2d_fast_fn<128, 0>(fast_lp & 15);
-  return mode == 2 ? syn2d_fast_fn<256, 2>(fast_lp & 15)
-       : mode == 1 ? syn2d_fast_fn<256, 1>(fast_lp & 15) : syn2d_fast_fn<256, 0>(fast_lp & 15);
+  if (tc == 128) return mode == 2 ? syn2d_fast_fn<128, 2>(fast_lp & 15) : syn2d_fast_fn<128, 0>(fast_lp & 15);
+  return mode == 2 ? syn2d_fast_fn<256, 2>(fast_lp & 15) : syn2d_fast_fn<256, 0>(fast_lp & 15);
 }
 
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm) {
