@@ -158,6 +158,7 @@ def measure(name, cfg, args, ws, rank, local, pg):
     import torch.distributed as dist
 
     import paper_1002_2184_b200 as fhwt
+    from paper_1002_2184_b200 import dist as fdist
     dev = torch.device("cuda", local)
     t0 = time.time()
     host, units = make_inputs(name, cfg, ws, rank)
@@ -187,7 +188,7 @@ def measure(name, cfg, args, ws, rank, local, pg):
         if cfg["shard"] == "rowband":
             fhwt.pack_ll_2d(coeffs, L, out=ll_local)      # K6 pack (same kernel family, counted)
             if gather:   # the only exchange (NCCL over NVLink): coarsest LL of every band
-                dist.all_gather_into_tensor(ll_all, ll_local, group=pg)
+                fdist.gather_coarse_ll(ll_local, group=pg, out=ll_all)
         if evs:
             evs[2].record(stream)
         plan.synthesize(coeffs, out=rec, workspace=wsb)
@@ -221,11 +222,10 @@ def measure(name, cfg, args, ws, rank, local, pg):
     ana = [e[0].elapsed_time(e[1]) for e in evs]
     mid = [e[1].elapsed_time(e[2]) for e in evs]
     syn = [e[2].elapsed_time(e[3]) for e in evs]
-    t = torch.tensor([total_ms, statistics.mean(ana), statistics.mean(syn), statistics.mean(mid)],
-                     dtype=torch.float64, device=dev)
+    vals = [total_ms, statistics.mean(ana), statistics.mean(syn), statistics.mean(mid)]
     if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=pg)
-    total_ms, ana_ms, syn_ms, mid_ms = (float(x) for x in t.tolist())
+        vals = fdist.max_over_ranks(vals, device=dev, group=pg)
+    total_ms, ana_ms, syn_ms, mid_ms = vals
     samples_rank = d.numel()
     samples_all = samples_rank * ws
     ms_step = total_ms / K
@@ -578,6 +578,8 @@ def main():
     ap.add_argument("--no-breakdown", action="store_true", help="skip the c2/c5 secondary measurements")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-direct", action="store_true", help="skip the direct-form (Fig. 2/5) baseline")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only for plumbing checks (FHWT_BENCH_ONE_DEVICE=1 on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
@@ -590,10 +592,15 @@ def main():
     import torch
     import torch.distributed as dist
     ws, rank, local = dist_env()
+    if os.environ.get("FHWT_BENCH_ONE_DEVICE"):   # plumbing check only: all ranks share cuda:0 (gloo)
+        local = 0
     torch.cuda.set_device(local)
     pg = None
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
         pg = dist.group.WORLD
     cfg = WORKLOADS[args.workload]
     res, (plan, host) = measure(args.workload, cfg, args, ws, rank, local, pg)
@@ -609,9 +616,8 @@ def main():
     if not args.no_e2e:
         e2e = measure_e2e(cfg, host, args.e2e_steps)
         if ws > 1:
-            t = torch.tensor([e2e["ms_per_step"]], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e["ms_per_step"] = float(t.item())
+            from paper_1002_2184_b200 import dist as fdist
+            e2e["ms_per_step"] = fdist.max_over_ranks(e2e["ms_per_step"], device=torch.device("cuda", local))
             e2e["value"] = 16.0 * host.numel() * ws / (e2e["ms_per_step"] * 1e-3) / 1e9
     del host
     breakdown = {}

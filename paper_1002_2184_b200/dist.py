@@ -41,23 +41,31 @@ def band_rows(r0: int, r1: int, level: int) -> tuple[int, int]:
     return r0 >> level, r1 >> level
 
 
-def gather_coarse_ll(ll_local: torch.Tensor, group=None) -> torch.Tensor:
+def gather_coarse_ll(ll_local: torch.Tensor, group=None, out: torch.Tensor | None = None) -> torch.Tensor:
     """All-gather the packed coarsest LL of every rank's row band, concatenated along rows
-    (rank order = row order).  NCCL: all_gather_into_tensor; other backends: all_gather."""
+    (rank order = row order).  NCCL: all_gather_into_tensor on the device (NVLink); other backends
+    (gloo, CPU tests): all_gather through host memory."""
     world = dist.get_world_size(group)
-    out = torch.empty((world * ll_local.shape[0],) + tuple(ll_local.shape[1:]), dtype=ll_local.dtype,
-                      device=ll_local.device)
+    shape = (world * ll_local.shape[0],) + tuple(ll_local.shape[1:])
+    if out is None:
+        out = torch.empty(shape, dtype=ll_local.dtype, device=ll_local.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, ll_local.contiguous(), group=group)
-    else:
-        parts = list(out.chunk(world, dim=0))
-        dist.all_gather(parts, ll_local.contiguous(), group=group)
-        out = torch.cat(parts, dim=0)
+        return out
+    src = ll_local.detach().to("cpu").contiguous()
+    parts = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(parts, src, group=group)
+    out.copy_(torch.cat(parts, dim=0))
     return out
 
 
-def max_over_ranks(value: float, device=None, group=None) -> float:
-    """Device-timed quantities are reported as the max over ranks."""
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+def max_over_ranks(values, device=None, group=None):
+    """Device-timed quantities are reported as the max over ranks (a float or a list of floats)."""
+    scalar = not isinstance(values, (list, tuple))
+    vals = [float(values)] if scalar else [float(v) for v in values]
+    if dist.get_backend(group) != "nccl":
+        device = "cpu"
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-    return float(t.item())
+    res = [float(v) for v in t.tolist()]
+    return res[0] if scalar else res

@@ -273,3 +273,39 @@ def test_lowpass_u8_errors():
         fhwt.lowpass_2d_u8(torch.zeros(24, 24, dtype=torch.uint8, device="cuda"), 4)
     with pytest.raises(fhwt.InvalidArgument):
         fhwt.lowpass_2d_u8(torch.zeros(16, 16, device="cuda"), 2)
+
+
+# ------------------------------------------------------------------ degenerate cases
+@pytest.mark.parametrize("shape,levels", [((3, 2048), 11), ((2, 256, 512), 8), ((4, 64, 64), 6)])
+def test_constant_input_gives_exactly_zero_details(shape, levels):
+    """SPEC.md:130 (constant => detail exactly 0) and the 2-D analogue; the LL/approximation is
+    c * 2^(L) (2-D) or c * 2^(J/2) (1-D) within rounding."""
+    x = np.full(shape, 0.7, dtype=np.float32)
+    if len(shape) == 2:
+        c = host(fhwt.analyze_1d(dev(x), levels))
+        n = shape[-1]
+        assert np.all(c[:, n >> levels:] == 0.0)
+        np.testing.assert_allclose(c[:, :n >> levels], 0.7 * 2 ** (levels / 2), rtol=1e-6)
+    else:
+        c = host(fhwt.analyze_2d(dev(x), levels))
+        h, w = shape[-2:]
+        ll = c[:, :h >> levels, :w >> levels].copy()
+        c[:, :h >> levels, :w >> levels] = 0.0
+        assert np.all(c == 0.0)
+        np.testing.assert_allclose(ll, 0.7 * 2 ** levels, rtol=1e-6)
+
+
+def test_non_finite_input_stays_inside_its_block():
+    """R1: 2^L-aligned blocks are independent, so a NaN contaminates only the coefficients of its
+    own block at every level (no halo, no spread)."""
+    L = 5
+    x = datagen.uniform((1, 128, 256), seed=42)
+    x[0, 70, 100] = np.nan
+    c = host(fhwt.analyze_2d(dev(x), L))[0]
+    bad = np.isnan(c)
+    expect = np.zeros_like(bad)
+    for j in range(1, L + 1):
+        hj, wj, r, q = 128 >> j, 256 >> j, 70 >> j, 100 >> j
+        expect[r, wj + q] = expect[hj + r, q] = expect[hj + r, wj + q] = True
+    expect[70 >> L, 100 >> L] = True
+    assert np.array_equal(bad, expect)
