@@ -200,6 +200,8 @@ def measure(name, cfg, args, ws, rank, local, pg):
     torch.cuda.synchronize(dev)
     # sampled parity of this run's own output against the fp64 oracle (one unit; not timed)
     parity = sampled_parity(name, cfg, host, coeffs, rec, rank, ws) if rank == 0 else None
+    if gather and rank == 0:
+        parity["gathered_ll"] = check_gathered_ll(cfg, ll_all, ws)
 
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
@@ -448,6 +450,26 @@ def measure_lowpass(steps=10):
                          "frac": alg / (ms * 1e-3) / 1e9 / peak, "peak_source": src,
                          "algorithmic_bytes_per_launch": alg},
             "parity": {"unit": "image 7", "max_abs_err_vs_oracle": err}}
+
+
+def check_gathered_ll(cfg, ll_all, ws):
+    """The all-gathered coarsest LL (row bands of every rank) against the oracle: one LL_L value in
+    the first and last LL row of each rank's band, from the regenerated 2^L x 2^L input block."""
+    import datagen
+    import oracle
+    L, size = cfg["levels"], cfg["h"]
+    b = 1 << L
+    rows_per_rank = (size >> L) // ws
+    errs = []
+    for r in range(ws):
+        for lr in (r * rows_per_rank, (r + 1) * rows_per_rank - 1):
+            lc = (7 * lr + 3) % (size >> L)
+            x = datagen.c5_rows((lr * b) // 256 * 256, (lr * b) // 256 * 256 + max(b, 256), size=size)
+            off = lr * b - (lr * b) // 256 * 256
+            blk = x[off:off + b, lc * b:(lc + 1) * b]
+            ref = oracle.analyze_2d(blk, L)[0, 0]
+            errs.append(abs(float(ll_all[lr, lc]) - ref))
+    return {"entries": len(errs), "max_abs_err": max(errs), "ranks": ws}
 
 
 def measure_e2e(cfg, host, steps):
