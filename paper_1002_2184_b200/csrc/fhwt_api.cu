@@ -127,14 +127,14 @@ int env_int(const char* name, int dflt) {
   return (v && *v) ? std::atoi(v) : dflt;
 }
 
-// occupancy cache: (kind, smem) -> blocks per SM.  kind = 0/1 ana2d f32/f64 generic,
-// 2 syn2d generic, 1e6 + fast_lp ana2d fast, 2e6 + fast_lp syn2d fast.
-fhwt_status occupancy(int kind, size_t smem, int* bps) {
+// occupancy cache: (family, fast, smem) -> blocks per SM.  family 0 = ana2d fp32, 1 = ana2d fp64,
+// 2 = syn2d; fast = the variant code (0 = generic kernel).
+fhwt_status occupancy(int family, int fast, size_t smem, int* bps) {
   static std::mutex mu;
   static std::vector<std::pair<std::pair<int64_t, size_t>, int>> cache;
   int dev = 0;
   FHWT_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
-  const int64_t key = int64_t(kind) * 64 + dev;
+  const int64_t key = ((int64_t(family) << 40) | (int64_t(fast) << 8)) + dev;
   {
     std::lock_guard<std::mutex> lk(mu);
     for (auto& e : cache)
@@ -143,10 +143,7 @@ fhwt_status occupancy(int kind, size_t smem, int* bps) {
         return FHWT_OK;
       }
   }
-  cudaError_t e = kind == 2         ? syn2d_occupancy(0, smem, bps)
-                  : kind >= 2000000 ? syn2d_occupancy(kind - 2000000, smem, bps)
-                  : kind >= 1000000 ? ana2d_occupancy(false, kind - 1000000, smem, bps)
-                                    : ana2d_occupancy(kind == 1, 0, smem, bps);
+  cudaError_t e = family == 2 ? syn2d_occupancy(fast, smem, bps) : ana2d_occupancy(family == 1, fast, smem, bps);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
   if (*bps < 1) return fail(FHWT_ERR_CUDA, "kernel does not fit on an SM with %zu B shared memory", smem);
   std::lock_guard<std::mutex> lk(mu);
@@ -285,6 +282,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     p.g0 = ps.g0;
     p.TR = choose_tr(p.Hin, ps.Lp);
     p.TC = int(std::min<int64_t>(in64 ? 128 : env_int("FHWT_ANA_TC", 256), p.Win));
+    if (!in64 && p.TC == 256 && p.Win % 256 && p.Win % 128 == 0) p.TC = 128;   // full tiles -> fast path
     p.tiles_r = p.Hin / p.TR;
     p.tiles_c = (p.Win + p.TC - 1) / p.TC;
     p.ntiles = B * p.tiles_r * p.tiles_c;
@@ -316,10 +314,11 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     p.bar_off = uint32_t(off);
     const size_t smem = off + 8 * size_t(p.stages);
     // compile-time 32 x 256 variant: first pass, full tiles (then every band offset is 8-B aligned)
-    const bool fast_ok = !in64 && ps.g0 == 0 && p.TR == 32 && (p.TC == 256 || p.TC == 128) && p.Win % p.TC == 0;
-    const int fast = fast_ok ? (p.TC << 4) | ps.Lp : 0;
+    const bool fast_ok = !in64 && ps.g0 == 0 && (p.TR == 32 || p.TR == 16 || p.TR == 8) &&
+                         (p.TC == 256 || p.TC == 128) && p.Win % p.TC == 0;
+    const int fast = fast_ok ? (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
-    FHWT_TRY(occupancy(fast ? 1000000 + fast : (in64 ? 1 : 0), smem, &bps));
+    FHWT_TRY(occupancy(in64 ? 1 : 0, fast, smem, &bps));
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
     FHWT_CUDA(launch_ana2d(p, map, in64, fast, int(grid), smem, s), "ana2d launch");
   }
@@ -349,6 +348,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     p.g0 = ps.g0;
     p.TR = choose_tr(p.Hin, ps.Lp);
     p.TC = int(std::min<int64_t>(env_int("FHWT_SYN_TC", 256), p.Win));
+    if (p.TC == 256 && p.Win % 256 && p.Win % 128 == 0) p.TC = 128;   // full tiles -> fast path
     p.tiles_r = p.Hin / p.TR;
     p.tiles_c = (p.Win + p.TC - 1) / p.TC;
     p.ntiles = B * p.tiles_r * p.tiles_c;
@@ -383,7 +383,8 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
                          p.row_boxes[ps.Lp] ? 1 : p.TR >> ps.Lp));
     }
     // Fast variant: 32 x TC full aligned tiles.
-    bool fast = p.TR == 32 && (p.TC == 256 || p.TC == 128) && p.Win % p.TC == 0 && p.out_pitch % 4 == 0 &&
+    bool fast = (p.TR == 32 || p.TR == 16 || p.TR == 8) && (p.TC == 256 || p.TC == 128) && p.Win % p.TC == 0 &&
+                p.out_pitch % 4 == 0 &&
                 (W >> (ps.g0 + 1)) % 2 == 0;
     for (int j = 1; j <= ps.Lp; ++j) fast = fast && p.hoff[j] == 0 && bw[j] == (p.TC >> j);
     // load path of the fast variant: 0 TMA boxes, 2 cp.async (LDGSTS) for all boxes.  Measured on
@@ -423,9 +424,9 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     off = align_up(off + pb[1], 128);
     p.bar_off = uint32_t(off);
     const size_t smem = off + 8 * size_t(p.stages);
-    const int fast_lp = fast ? (mode << 16) | (p.TC << 4) | ps.Lp : 0;
+    const int fast_lp = fast ? (mode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
-    FHWT_TRY(occupancy(fast ? 2000000 + fast_lp : 2, smem, &bps));
+    FHWT_TRY(occupancy(2, fast_lp, smem, &bps));
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
     FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
   }

@@ -212,12 +212,12 @@ struct Refill {
   }
 };
 
-// Fast tile: first pass (g0 = 0, fp32 input), 32 x TCF full tiles, LP levels known at compile
+// Fast tile: first pass (g0 = 0, fp32 input), TRF x TCF full tiles, LP levels known at compile
 // time, so every index is a shift/constant and levels g >= 4 are fp64 by construction.
-template <int J, int LP, int TCF>
+template <int J, int LP, int TRF, int TCF>
 __device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* src, unsigned char* smem, int64_t b,
                                               int64_t row0, int64_t col0, const Refill& refill) {
-  constexpr int R = 32 >> (J - 1), C = TCF >> (J - 1);
+  constexpr int R = TRF >> (J - 1), C = TCF >> (J - 1);
   constexpr bool src64 = J - 1 >= kFirstF64Level;
   constexpr bool cmp64 = J >= kFirstF64Level;
   using TS = typename std::conditional<src64, double, float>::type;
@@ -227,11 +227,11 @@ __device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* 
   if constexpr (J < LP) {
     __syncthreads();
     if constexpr (J == 1) refill();   // level 1 was the last reader of the TMA stage
-    ana_fast_step<J + 1, LP, TCF>(p, smem + p.p_off[J & 1], smem, b, row0, col0, refill);
+    ana_fast_step<J + 1, LP, TRF, TCF>(p, smem + p.p_off[J & 1], smem, b, row0, col0, refill);
   }
 }
 
-template <typename TIn, int LPFAST, int TCF>
+template <typename TIn, int LPFAST, int TRF, int TCF>
 __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_ANA) ana2d_kernel(const __grid_constant__ Ana2dParams p,
                                                            const __grid_constant__ CUtensorMap in_map) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_ANA) ana2d_kernel(const 
     const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
                         tile_bytes, row_bytes, pol};
     if constexpr (LPFAST > 0) {
-      ana_fast_step<1, LPFAST, TCF>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC, refill);
+      ana_fast_step<1, LPFAST, TRF, TCF>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC, refill);
       __syncthreads();  // LL buffers free again
       if constexpr (LPFAST == 1) refill();
     } else {
@@ -362,12 +362,12 @@ __device__ __forceinline__ void syn_tile(const Syn2dParams& p, unsigned char* st
   }
 }
 
-// Fast tile: 32 x TCF full tiles, hoff = 0, LP known at compile time (box pitch = TCF >> j).
+// Fast tile: TRF x TCF full tiles, hoff = 0, LP known at compile time (box pitch = TCF >> j).
 // All levels J..1 from the TMA stage (level 1 writes the output tile).
-template <int J, int TCF>
+template <int J, int TRF, int TCF>
 __device__ __forceinline__ void syn_fast_step(const Syn2dParams& p, unsigned char* stage, unsigned char* smem,
                                               const float* ll, int64_t b, int64_t row0, int64_t col0) {
-  constexpr int R = 32 >> J, C = TCF >> J;
+  constexpr int R = TRF >> J, C = TCF >> J;
   const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]);
   const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]);
   const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]);
@@ -375,14 +375,14 @@ __device__ __forceinline__ void syn_fast_step(const Syn2dParams& p, unsigned cha
   syn_level<2, R, C, true>(p, ll, C, hl, lh, hh, C, R, C, J > 1, b, row0, col0, dst);
   if constexpr (J > 1) {
     __syncthreads();
-    syn_fast_step<J - 1, TCF>(p, stage, smem, dst, b, row0, col0);
+    syn_fast_step<J - 1, TRF, TCF>(p, stage, smem, dst, b, row0, col0);
   }
 }
 
 // cp.async variant: every thread copies 16-B chunks of tile t (all boxes of all levels, same smem
 // layout as the TMA boxes) and commits one group.  Chunk q = tid + 256 i enumerates, level by
 // level, the rows of HL, LH, HH (and the LL block of level LP).
-template <int LP, int TCF>
+template <int LP, int TRF, int TCF>
 __device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned char* base, int64_t t) {
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
@@ -390,7 +390,7 @@ __device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned
   int q0 = 0;
 #pragma unroll
   for (int j = 1; j <= LP; ++j) {
-    const int rows = 32 >> j, cpr = (TCF >> j) / 4, nb = rows * cpr;   // chunks per band block
+    const int rows = TRF >> j, cpr = (TCF >> j) / 4, nb = rows * cpr;   // chunks per band block
     const int g = p.g0 + j;
     const int64_t hg = p.H >> g, wg = p.W >> g;
     const float* gb = p.coeffs + (b * p.H + (row0 >> j)) * p.W + (col0 >> j);
@@ -404,7 +404,7 @@ __device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned
     q0 += 3 * nb;
   }
   {
-    const int rows = 32 >> LP, cpr = (TCF >> LP) / 4;
+    const int rows = TRF >> LP, cpr = (TCF >> LP) / 4;
     const float* lsrc;
     int64_t lpitch;
     if (p.ll_from_ws) {
@@ -468,7 +468,7 @@ __device__ __forceinline__ void cp_async_wait_rt(int n) {  // runtime-N wrapper 
 
 // MODE 0: all boxes by TMA; 2: everything by cp.async (LDGSTS).  (A register-LDG level-1 variant
 // measured 5.19 TB/s vs 6.10 for cp.async and was removed; tools/sweep_syn.py history in profiles/.)
-template <int LPFAST, int TCF, int MODE>
+template <int LPFAST, int TRF, int TCF, int MODE>
 __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const __grid_constant__ Syn2dParams p,
                                                            const __grid_constant__ TmaMaps2d maps) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const 
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
       if (t < p.ntiles)
-        syn_cp_async_tile<LPFAST, TCF>(p, smem + s * p.stage_bytes, t);
+        syn_cp_async_tile<LPFAST, TRF, TCF>(p, smem + s * p.stage_bytes, t);
       else
         cp_async_commit();
     }
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const 
     const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
     unsigned char* stage = smem + s * p.stage_bytes;
     if constexpr (LPFAST > 0) {
-      syn_fast_step<LPFAST, TCF>(p, stage, smem, reinterpret_cast<const float*>(stage + p.box_off[0][0]), b, row0,
+      syn_fast_step<LPFAST, TRF, TCF>(p, stage, smem, reinterpret_cast<const float*>(stage + p.box_off[0][0]), b, row0,
                                  ct * p.TC);
     } else {
       syn_tile(p, stage, smem, b, row0, ct * p.TC);
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const 
     const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
     if constexpr (CPASYNC) {
       if (nt < p.ntiles)
-        syn_cp_async_tile<LPFAST, TCF>(p, smem + s * p.stage_bytes, nt);
+        syn_cp_async_tile<LPFAST, TRF, TCF>(p, smem + s * p.stage_bytes, nt);
       else
         cp_async_commit();
     } else if (tid < 32) {
@@ -600,42 +600,70 @@ static cudaError_t raise_smem_cap(const void* fn) {
   return e;
 }
 
-template <int TCF>
+// Fast variants: tile rows TRF in {8, 16, 32}, tile cols TCF in {128, 256}, levels LP <= log2(TRF).
+template <int TRF, int TCF>
 static const void* ana2d_fast_fn(int lp) {
   switch (lp) {
-    case 1: return (const void*)ana2d_kernel<float, 1, TCF>;
-    case 2: return (const void*)ana2d_kernel<float, 2, TCF>;
-    case 3: return (const void*)ana2d_kernel<float, 3, TCF>;
-    case 4: return (const void*)ana2d_kernel<float, 4, TCF>;
-    default: return (const void*)ana2d_kernel<float, 5, TCF>;
+    case 1: return (const void*)ana2d_kernel<float, 1, TRF, TCF>;
+    case 2: return (const void*)ana2d_kernel<float, 2, TRF, TCF>;
+    case 3: return (const void*)ana2d_kernel<float, 3, TRF, TCF>;
+    case 4:
+      if constexpr (TRF >= 16) return (const void*)ana2d_kernel<float, 4, TRF, TCF>;
+      return nullptr;
+    case 5:
+      if constexpr (TRF >= 32) return (const void*)ana2d_kernel<float, 5, TRF, TCF>;
+      return nullptr;
+    default: return nullptr;
   }
 }
 
-template <int TCF, int MODE>
+template <int TRF, int TCF, int MODE>
 static const void* syn2d_fast_fn(int lp) {
   switch (lp) {
-    case 1: return (const void*)syn2d_kernel<1, TCF, MODE>;
-    case 2: return (const void*)syn2d_kernel<2, TCF, MODE>;
-    case 3: return (const void*)syn2d_kernel<3, TCF, MODE>;
-    case 4: return (const void*)syn2d_kernel<4, TCF, MODE>;
-    default: return (const void*)syn2d_kernel<5, TCF, MODE>;
+    case 1: return (const void*)syn2d_kernel<1, TRF, TCF, MODE>;
+    case 2: return (const void*)syn2d_kernel<2, TRF, TCF, MODE>;
+    case 3: return (const void*)syn2d_kernel<3, TRF, TCF, MODE>;
+    case 4:
+      if constexpr (TRF >= 16) return (const void*)syn2d_kernel<4, TRF, TCF, MODE>;
+      return nullptr;
+    case 5:
+      if constexpr (TRF >= 32) return (const void*)syn2d_kernel<5, TRF, TCF, MODE>;
+      return nullptr;
+    default: return nullptr;
   }
 }
 
-// fast_lp: 0 = generic kernel; otherwise (tile cols << 4) | LP, tile cols 256 or 128
-static const void* ana2d_fn(bool in_f64, int fast_lp) {
-  if (in_f64) return (const void*)ana2d_kernel<double, 0, 0>;
-  if (fast_lp == 0) return (const void*)ana2d_kernel<float, 0, 0>;
-  return ((fast_lp >> 4) & 0xfff) == 128 ? ana2d_fast_fn<128>(fast_lp & 15) : ana2d_fast_fn<256>(fast_lp & 15);
+template <template <int, int> class F>
+static const void* by_geometry(int tr, int tc, int lp) {
+  if (tr == 32) return tc == 128 ? F<32, 128>::get(lp) : F<32, 256>::get(lp);
+  if (tr == 16) return tc == 128 ? F<16, 128>::get(lp) : F<16, 256>::get(lp);
+  return tc == 128 ? F<8, 128>::get(lp) : F<8, 256>::get(lp);
+}
+template <int TRF, int TCF>
+struct AnaF {
+  static const void* get(int lp) { return ana2d_fast_fn<TRF, TCF>(lp); }
+};
+template <int TRF, int TCF>
+struct SynF0 {
+  static const void* get(int lp) { return syn2d_fast_fn<TRF, TCF, 0>(lp); }
+};
+template <int TRF, int TCF>
+struct SynF2 {
+  static const void* get(int lp) { return syn2d_fast_fn<TRF, TCF, 2>(lp); }
+};
+
+// fast: 0 = generic kernel; else (mode << 24) | (tile rows << 16) | (tile cols << 4) | LP
+static const void* ana2d_fn(bool in_f64, int fast) {
+  if (in_f64) return (const void*)ana2d_kernel<double, 0, 0, 0>;
+  if (fast == 0) return (const void*)ana2d_kernel<float, 0, 0, 0>;
+  return by_geometry<AnaF>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15);
 }
 
-// synthesis fast_lp additionally carries the load mode (0 TMA, 2 cp.async) in bits 16+
-static const void* syn2d_fn(int fast_lp) {
-  if (fast_lp == 0) return (const void*)syn2d_kernel<0, 0, 0>;
-  const int mode = (fast_lp >> 16) & 3;
-  const int tc = (fast_lp >> 4) & 0xfff;
-  if (tc == 128) return mode == 2 ? syn2d_fast_fn<128, 2>(fast_lp & 15) : syn2d_fast_fn<128, 0>(fast_lp & 15);
-  return mode == 2 ? syn2d_fast_fn<256, 2>(fast_lp & 15) : syn2d_fast_fn<256, 0>(fast_lp & 15);
+static const void* syn2d_fn(int fast) {
+  if (fast == 0) return (const void*)syn2d_kernel<0, 0, 0, 0>;
+  const int mode = (fast >> 24) & 0xff;
+  return mode == 2 ? by_geometry<SynF2>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15)
+                   : by_geometry<SynF0>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15);
 }
 
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm) {
