@@ -180,9 +180,9 @@ fhwt_status check_2d(int64_t h, int64_t w, int64_t batch, int levels) {
   if (h % 2 || w % 2) return fail(FHWT_ERR_ODD_LENGTH, "odd dimension %lldx%lld", (long long)h, (long long)w);
   if (h % (int64_t(1) << levels) || w % (int64_t(1) << levels))
     return fail(FHWT_ERR_INSUFFICIENT_LENGTH, "%lldx%lld not divisible by 2^%d", (long long)h, (long long)w, levels);
-  if (batch * h >= (int64_t(1) << 31) || w >= (int64_t(1) << 31))
-    return fail(FHWT_ERR_INVALID_ARG, "batch*h=%lld or w=%lld exceeds the 2^31 TMA coordinate range",
-                (long long)(batch * h), (long long)w);
+  if (h >= (int64_t(1) << 30) || w >= (int64_t(1) << 30))   // TMA coordinates are int32 (batches are split)
+    return fail(FHWT_ERR_INVALID_ARG, "h=%lld or w=%lld exceeds the 2^30 TMA coordinate range", (long long)h,
+                (long long)w);
   return FHWT_OK;
 }
 
@@ -521,9 +521,24 @@ fhwt_status run(fhwt_plan p, const float* in, float* out, void* workspace, fhwt_
     owned = true;
   }
   fhwt_status st_ = FHWT_OK;
-  if (p->kind == 2)
-    st_ = analysis ? run_ana2d(p, in, out, ws, s) : run_syn2d(p, in, out, ws, s);
-  else
+  if (p->kind == 2) {
+    // TMA row coordinates are int32 over the [batch * h] row view: larger batches run as
+    // consecutive sub-batches (workspace needs scale with the batch, so the plan's buffer fits).
+    const int64_t max_rows = env_int("FHWT_TEST_MAX_TMA_ROWS", 0) > 0 ? env_int("FHWT_TEST_MAX_TMA_ROWS", 0)
+                                                                       : (int64_t(1) << 31) - 1;   // test hook
+    const int64_t max_b = std::max<int64_t>(1, max_rows / p->h);
+    if (p->batch <= max_b) {
+      st_ = analysis ? run_ana2d(p, in, out, ws, s) : run_syn2d(p, in, out, ws, s);
+    } else {
+      for (int64_t b0 = 0; b0 < p->batch && st_ == FHWT_OK; b0 += max_b) {
+        fhwt_plan_s sub = *p;
+        sub.batch = std::min(max_b, p->batch - b0);
+        plan_layout(&sub);
+        const int64_t off = b0 * p->h * p->w;
+        st_ = analysis ? run_ana2d(&sub, in + off, out + off, ws, s) : run_syn2d(&sub, in + off, out + off, ws, s);
+      }
+    }
+  } else
     st_ = analysis ? run_ana1d(p, in, out, ws, s) : run_syn1d(p, in, out, ws, s);
   if (owned) {
     cudaError_t e = cudaFreeAsync(ws, s);

@@ -41,6 +41,22 @@ def band_rows(r0: int, r1: int, level: int) -> tuple[int, int]:
     return r0 >> level, r1 >> level
 
 
+def segment_1d(n: int, world: int, rank: int, levels: int) -> tuple[int, int]:
+    """One very long 1-D signal split into `world` contiguous segments of 2^levels-aligned length
+    (§8(f) f2): samples [s0, s1) owned by `rank`.  Segments transform independently (reading R1)."""
+    return row_band(n, world, rank, levels)
+
+
+def segment_bands_1d(s0: int, s1: int, n: int, levels: int) -> dict:
+    """Where a segment's local Mallat output [a_J | d_J | ... | d_1] (length s1 - s0) lands in the
+    global Mallat layout of the n-sample signal: {band: (local_start, global_start, length)}."""
+    seg = s1 - s0
+    out = {"a": (0, s0 >> levels, seg >> levels)}
+    for j in range(1, levels + 1):
+        out[f"d{j}"] = (seg >> j, (n >> j) + (s0 >> j), seg >> j)
+    return out
+
+
 def gather_coarse_ll(ll_local: torch.Tensor, group=None, out: torch.Tensor | None = None) -> torch.Tensor:
     """All-gather the packed coarsest LL of every rank's row band, concatenated along rows
     (rank order = row order).  NCCL: all_gather_into_tensor on the device (NVLink); other backends

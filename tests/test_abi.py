@@ -65,7 +65,7 @@ def test_plan_1d_validation(args, exc):
     ((8, 5, 1, 1), fhwt.OddLength),
     ((8, 8, 1, 0), fhwt.InvalidLevels),
     ((8, 12, 1, 3), fhwt.InsufficientLength),
-    ((1 << 20, 8, 4096, 1), fhwt.InvalidArgument),   # beyond the 2^31 TMA row-coordinate range
+    ((1 << 30, 8, 1, 1), fhwt.InvalidArgument),      # beyond the TMA coordinate range
 ])
 def test_plan_2d_validation(args, exc):
     with pytest.raises(exc):
@@ -146,3 +146,9 @@ def test_op_counts_match_the_oracles_instrumented_count(shape, levels):
     km, ka = fhwt.op_counts(shape, levels, "kernel")
     assert km <= fm and km + ka <= fm + fa
     assert fhwt.op_counts(shape, levels, "fast", batch=7) == (7 * fm, 7 * fa)
+
+
+def test_huge_batches_are_accepted():
+    """batch * h beyond the int32 TMA row range is split into sub-batches, not rejected."""
+    p = fhwt.Plan2d(1 << 20, 8, 4096, 1)
+    assert p.batch == 4096

@@ -66,6 +66,17 @@ def _c5_like_rank(rank):
     return {"r0": r0, "r1": r1, "coeffs": coeffs, "ll_all": gathered.numpy(), "tmax": t}
 
 
+N1, J1 = 8192, 7
+
+
+def _segment_rank(rank):
+    s0, s1 = fdist.segment_1d(N1, WORLD, rank, J1)
+    x = datagen.c2_signal(0, n=N1)[s0:s1]
+    c = o.decompose_1d(x, J1)
+    a = torch.from_numpy(np.ascontiguousarray(c[:(s1 - s0) >> J1]))
+    return {"s0": s0, "s1": s1, "coeffs": c, "a_all": fdist.gather_coarse_ll(a[None]).numpy()}
+
+
 def _weak_rank(rank):
     first, count = fdist.unit_shard(3, rank)
     x = datagen.c4_batch(first, count, size=64)
@@ -105,6 +116,20 @@ def test_weak_scaling_unit_shards():
     for r in range(WORLD):
         f, c = res[r]["first"], res[r]["count"]
         np.testing.assert_allclose(res[r]["coeffs"], ref[f:f + c], atol=1e-12)
+
+
+@pytest.mark.timeout(300)
+def test_long_signal_segments():
+    """§8(f) f2: one long signal split into 2^J-aligned segments; every band of every segment lands
+    at its global Mallat offset, and the gathered coarse approximation is the global a_J."""
+    res = _run("_segment_rank")
+    ref = o.decompose_1d(datagen.c2_signal(0, n=N1), J1)
+    for r in range(WORLD):
+        d = res[r]
+        assert isinstance(d, dict), d
+        for band, (lo, go, ln) in fdist.segment_bands_1d(d["s0"], d["s1"], N1, J1).items():
+            np.testing.assert_allclose(d["coeffs"][lo:lo + ln], ref[go:go + ln], atol=1e-12, err_msg=band)
+        np.testing.assert_allclose(d["a_all"].reshape(-1), ref[:N1 >> J1], atol=1e-12)
 
 
 def test_row_band_validation():

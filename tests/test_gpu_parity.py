@@ -309,3 +309,57 @@ def test_non_finite_input_stays_inside_its_block():
         expect[r, wj + q] = expect[hj + r, q] = expect[hj + r, wj + q] = True
     expect[70 >> L, 100 >> L] = True
     assert np.array_equal(bad, expect)
+
+
+def test_sub_batching_beyond_the_tma_row_range(monkeypatch):
+    """batch * h beyond the int32 TMA row range runs as sub-batches; forced here with the library's
+    test hook (max rows = 3 images of 256 rows) and compared with the unsplit result."""
+    x = dev(datagen.uniform((7, 256, 512), seed=77))
+    c_ref = fhwt.analyze_2d(x, 8)
+    r_ref = fhwt.synthesize_2d(c_ref, 8)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("FHWT_TEST_MAX_TMA_ROWS", str(3 * 256))
+    c = fhwt.analyze_2d(x, 8)
+    r = fhwt.synthesize_2d(c, 8)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c_ref) and torch.equal(r, r_ref)
+
+
+# ------------------------------------------------------------------ pin C8: sharding is bitwise exact
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_row_band_shards_bitwise_equal_full_image(world):
+    """each rank's band output equals the single-GPU output's corresponding rows
+    bitwise, and the bands' coarsest LL concatenate to the full LL (what the all-gather delivers).
+    Ranks are run one after another on one GPU (no kernel waits on another)."""
+    from paper_1002_2184_b200 import dist as fdist
+    H, W, L = 2048, 1024, 8
+    x = dev(datagen.c5_rows(0, H, size=2048)[:, :W])
+    full = fhwt.analyze_2d(x, L)
+    lls = []
+    for r in range(world):
+        r0, r1 = fdist.row_band(H, world, r, L)
+        band = fhwt.analyze_2d(x[r0:r1].contiguous(), L)
+        bh = r1 - r0
+        for j in range(1, L + 1):
+            g0, g1 = fdist.band_rows(r0, r1, j)
+            hj, wj, bj = H >> j, W >> j, bh >> j
+            assert torch.equal(band[:bj, wj:2 * wj], full[g0:g1, wj:2 * wj])
+            assert torch.equal(band[bj:2 * bj, :wj], full[hj + g0:hj + g1, :wj])
+            assert torch.equal(band[bj:2 * bj, wj:2 * wj], full[hj + g0:hj + g1, wj:2 * wj])
+        lls.append(fhwt.pack_ll_2d(band, L))
+    assert torch.equal(torch.cat(lls, 0), full[:H >> L, :W >> L])
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_long_signal_segments_bitwise_equal(world):
+    """§8(f) f2: a long signal split into 2^J-aligned segments (segment starts are not multiples
+    of the kernel's 1024-sample chunk) gives bitwise the same coefficients as the whole signal."""
+    from paper_1002_2184_b200 import dist as fdist
+    N, J = 3 * 4096 * world, 9
+    x = dev(datagen.c2_signal(5, n=N)[None])
+    full = fhwt.analyze_1d(x, J)[0]
+    for r in range(world):
+        s0, s1 = fdist.segment_1d(N, world, r, J)
+        seg = fhwt.analyze_1d(x[:, s0:s1].contiguous(), J)[0]
+        for band, (lo, go, ln) in fdist.segment_bands_1d(s0, s1, N, J).items():
+            assert torch.equal(seg[lo:lo + ln], full[go:go + ln]), (r, band)
