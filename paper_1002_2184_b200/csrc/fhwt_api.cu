@@ -319,6 +319,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     const int fast = fast_ok ? (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
     FHWT_TRY(occupancy(in64 ? 1 : 0, fast, smem, &bps));
+    if (const int cap = env_int("FHWT_CTAS_PER_SM", 0)) bps = std::min(bps, cap);   // sweep knob
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
     FHWT_CUDA(launch_ana2d(p, map, in64, fast, int(grid), smem, s), "ana2d launch");
   }
@@ -427,6 +428,9 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     const int fast_lp = fast ? (mode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
     FHWT_TRY(occupancy(2, fast_lp, smem, &bps));
+    // At most 2 resident CTAs/SM: the lighter LP < 5 variants fit 3-4, which measured 2.5-6.5 %
+    // slower (tools/sweep_ctas.py, profiles/r01_sweep_ctas.jsonl); LP = 5 is indifferent.
+    bps = std::min(bps, env_int("FHWT_CTAS_PER_SM", 2));
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
     FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
   }

@@ -30,7 +30,7 @@ def timeit(fn, reps=10):
 
 t = timeit(lambda: c.copy_(x))
 print(json.dumps({"op": "torch copy_ 4 GiB fp32", "gbs": 8 * S / t / 1e6}), flush=True)
-for st in ("2", "3"):
+for st in ("2",):
     os.environ["FHWT_ANA_STAGES"] = os.environ["FHWT_SYN_STAGES"] = st
     for L in (1, 2, 3, 4, 5):
         p = fhwt.Plan2d(2048, 2048, 256, L)
