@@ -295,6 +295,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     // them per tile from one thread.  B200 (tools/membench.py, tools/sweep_2d.py): 32 one-row
     // 1-KB boxes stream at 6.9 TB/s where one 32-row box stops at 6.1 TB/s; smaller row boxes
     // are request-bound and slower than multi-row boxes.
+    p.l2hint = env_int("FHWT_ANA_L2HINT", 1);
     p.row_boxes = size_t(p.TC) * (in64 ? 8 : 4) >= 1024 && (size_t(p.TC) * (in64 ? 8 : 4)) % 128 == 0;
     FHWT_TRY(encode_2d(&map, in, in64, p.Win, B * p.Hin, in_pitch, p.TC, p.row_boxes ? 1 : p.TR));
     // shared memory layout: stages | P[0] | P[1] | barriers
@@ -306,17 +307,26 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
       const size_t sz = (in64 || ps.g0 + j >= kFirstF64Level) ? 8 : 4;
       pb[j & 1] = std::max(pb[j & 1], size_t(p.TR >> j) * size_t(p.TC >> j) * sz);
     }
-    size_t off = size_t(p.stages) * p.stage_bytes;
-    p.p_off[0] = uint32_t(off);
-    off = align_up(off + pb[0], 128);
-    p.p_off[1] = uint32_t(off);
-    off = align_up(off + pb[1], 128);
-    p.bar_off = uint32_t(off);
-    const size_t smem = off + 8 * size_t(p.stages);
     // compile-time 32 x 256 variant: first pass, full tiles (then every band offset is 8-B aligned)
     const bool fast_ok = !in64 && ps.g0 == 0 && (p.TR == 32 || p.TR == 16 || p.TR == 8) &&
                          (p.TC == 256 || p.TC == 128) && p.Win % p.TC == 0;
-    const int fast = fast_ok ? (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
+    // warp-decoupled variant (haar2d.cu ana2d_warp_kernel): 32 x 256 full tiles, one-row boxes
+    // FHWT_ANA_WARP: 0 = CTA-synchronous kernel, 1 = 32-column warp blocks, 2 = 64-column warp blocks
+    const int wmode = env_int("FHWT_ANA_WARP", 0);
+    const bool warp_ok = fast_ok && p.TR == 32 && p.TC == 256 && p.row_boxes && wmode != 0;
+    size_t off = size_t(p.stages) * p.stage_bytes;
+    p.p_off[0] = uint32_t(off);
+    if (warp_ok) {
+      off = align_up(off + size_t(wmode == 2 ? 4 : 8) * kWarpScratchBytes, 128);   // see AnaScratch
+      p.p_off[1] = p.p_off[0];
+    } else {
+      off = align_up(off + pb[0], 128);
+      p.p_off[1] = uint32_t(off);
+      off = align_up(off + pb[1], 128);
+    }
+    p.bar_off = uint32_t(off);
+    const size_t smem = off + 12 * size_t(p.stages);   // mbarriers + stage-release counters
+    const int fast = fast_ok ? ((warp_ok ? (wmode == 2 ? 4 : 1) : 0) << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
     FHWT_TRY(occupancy(in64 ? 1 : 0, fast, smem, &bps));
     if (const int cap = env_int("FHWT_CTAS_PER_SM", 0)) bps = std::min(bps, cap);   // sweep knob
@@ -390,7 +400,9 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     for (int j = 1; j <= ps.Lp; ++j) fast = fast && p.hoff[j] == 0 && bw[j] == (p.TC >> j);
     // load path of the fast variant: 0 TMA boxes, 2 cp.async (LDGSTS) for all boxes.  Measured on
     // B200 (tools/sweep_syn.py): cp.async 6.10 TB/s, TMA boxes 5.86 (register LDG of level 1: 5.19).
-    const int mode = fast ? (env_int("FHWT_SYN_MODE", 2) == 0 ? 0 : 2) : 0;
+    int mode = fast ? env_int("FHWT_SYN_MODE", 3) : 0;
+    if (mode != 0 && mode != 3) mode = 2;
+    if (mode == 3 && !(p.TR == 32 && p.TC == 256)) mode = 2;   // warp-decoupled variant: 32 x 256 tiles only
     p.l1_ldg = 0;
     // stage layout: LL box, then per level j three boxes (128-B aligned: TMA destinations need it;
     // with cp.async a 16-B packing would admit a 3rd CTA/SM, which measured slower: 5.54 vs 6.10 TB/s)
@@ -420,11 +432,16 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     }
     off = size_t(p.stages) * p.stage_bytes;
     p.p_off[0] = uint32_t(off);
-    off = align_up(off + pb[0], 128);
-    p.p_off[1] = uint32_t(off);
-    off = align_up(off + pb[1], 128);
+    if (mode == 3) {
+      off = align_up(off + size_t(kThreads2d / 32) * kSynScratchBytes, 128);
+      p.p_off[1] = p.p_off[0];
+    } else {
+      off = align_up(off + pb[0], 128);
+      p.p_off[1] = uint32_t(off);
+      off = align_up(off + pb[1], 128);
+    }
     p.bar_off = uint32_t(off);
-    const size_t smem = off + 8 * size_t(p.stages);
+    const size_t smem = off + 12 * size_t(p.stages);   // mbarriers + stage-release counters
     const int fast_lp = fast ? (mode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
     FHWT_TRY(occupancy(2, fast_lp, smem, &bps));

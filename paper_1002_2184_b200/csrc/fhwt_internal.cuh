@@ -19,6 +19,11 @@ constexpr int kChunk1d = 1024;
 constexpr int kThreads2d = 256;
 constexpr int kThreads1d = 256;
 
+// Warp-decoupled 2-D variants (haar2d.cu): 32 x 256 tiles, warp w owns the 32 x 32 block at
+// columns [32w, 32w + 32); per-warp LL scratch (LL1 16x16 f32, LL2 8x8 f32, LL3 4x4 f32, LL4 2x2 f64).
+constexpr int kWarpScratchBytes = 2560;   // analysis (AnaScratch<64>)
+constexpr int kSynScratchBytes = 1408;    // synthesis (WarpScratch)
+
 // First global level computed in fp64 (levels 1..3 fp32).  DESIGN.md "Precision".
 constexpr int kFirstF64Level = 4;
 
@@ -37,6 +42,7 @@ struct Ana2dParams {
   int stages;
   uint32_t stage_bytes, p_off[2], bar_off;
   int final_pass;
+  int l2hint;            // 1: TMA loads carry an L2 evict_first policy (sweep knob FHWT_ANA_L2HINT)
   int row_boxes;         // 1: the map's box is one row and TR boxes are issued per tile (rows of
                          // 128-B multiples; TMA smem destinations must be 128-B aligned); 0: one TR-row box
 };
@@ -164,6 +170,15 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_nohint(void* smem_dst, const CUtensorMap* map, int c0, int c1,
+                                                   uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
 

@@ -190,9 +190,14 @@ __device__ __forceinline__ void ana_issue_tile(const Ana2dParams& p, const CUten
   if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
   __syncwarp();
   if (p.row_boxes) {
-    if (lane == 0)
-      for (int r = 0; r < p.TR; ++r)
-        tma_load_2d(dst + r * row_bytes, map, int(ct * p.TC), int(rt * p.TR + r), bar, pol);
+    if (lane == 0) {
+      if (p.l2hint)
+        for (int r = 0; r < p.TR; ++r)
+          tma_load_2d(dst + r * row_bytes, map, int(ct * p.TC), int(rt * p.TR + r), bar, pol);
+      else
+        for (int r = 0; r < p.TR; ++r)
+          tma_load_2d_nohint(dst + r * row_bytes, map, int(ct * p.TC), int(rt * p.TR + r), bar);
+    }
   } else if (lane == 0) {
     tma_load_2d(dst, map, int(ct * p.TC), int(rt * p.TR), bar, pol);
   }
@@ -272,6 +277,196 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_ANA) ana2d_kernel(const 
       __syncthreads();  // stage s and the LL buffers are free again
       refill();
     }
+  }
+}
+
+// ------------------------------------------------------ warp-decoupled analysis (32 x 256 tiles)
+// Haar's 2-tap support (reading R1) makes every 32 x 32 input block independent for all 5 levels,
+// so warp w of the CTA takes columns [32w, 32w + 32) of each TMA-staged 32 x 256 tile and runs
+// levels 1..LP on its block with only __syncwarp between levels (LL in per-warp scratch).  No
+// CTA-wide barrier remains: the stage is released by the last warp to finish level 1 (a shared
+// counter), which also issues the refill, so one warp's coarse levels overlap the other warps'
+// level 1 instead of idling the CTA at a barrier.
+struct WarpScratch {
+  float ll1[16 * 16];
+  float ll2[8 * 8];
+  float ll3[4 * 4];
+  double ll4[2 * 2];
+};
+static_assert(sizeof(WarpScratch) <= kSynScratchBytes, "host smem layout");
+
+struct TileXY {
+  int64_t b, row0, col0;
+};
+// tile -> (image, first row, first column); 32-bit division when the tile count allows it
+__device__ __forceinline__ TileXY tile_xy(int64_t tile, int64_t tiles_c, int64_t tiles_r, int TR, int TC) {
+  TileXY t;
+  if (tiles_c * tiles_r < (int64_t(1) << 31) && tile < (int64_t(1) << 31)) {
+    const uint32_t rt = uint32_t(tile) / uint32_t(tiles_c), ct = uint32_t(tile) - rt * uint32_t(tiles_c);
+    const uint32_t b = rt / uint32_t(tiles_r);
+    t.b = b;
+    t.row0 = int64_t(rt - b * uint32_t(tiles_r)) * TR;
+    t.col0 = int64_t(ct) * TC;
+  } else {
+    const int64_t rt = tile / tiles_c, ct = tile - rt * tiles_c;
+    t.b = rt / tiles_r;
+    t.row0 = (rt - t.b * tiles_r) * TR;
+    t.col0 = ct * TC;
+  }
+  return t;
+}
+
+// Per-warp LL scratch of the analysis variant with BW-column warp blocks (BW = 32 or 64):
+// LL1 16 x BW/2 f32 | LL2 8 x BW/4 f32 | LL3 4 x BW/8 f32 | LL4 2 x BW/16 f64.
+// LL1/LL3 share one buffer and LL2/LL4 the other (a level reads LL_{j-1} and writes LL_j).
+template <int BW>
+struct AnaScratch {
+  static constexpr int off(int j) {   // byte offset of LL_j
+    return (j & 1) ? 0 : 16 * (BW / 2) * 4;
+  }
+  static constexpr int bytes = 16 * (BW / 2) * 4 + 8 * (BW / 4) * 4;
+};
+static_assert(AnaScratch<64>::bytes <= kWarpScratchBytes && AnaScratch<32>::bytes <= kWarpScratchBytes, "host layout");
+
+template <typename T, int N>
+__device__ __forceinline__ void load_row8(const T* src, T (&v)[N]) {
+  if constexpr (sizeof(T) == 4 && N == 8) {
+    const float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+    load_row<T, N, true>(src, v);
+  }
+}
+
+// One level J of a warp's block: (32 >> (J-1)) x (BW >> (J-1)) source -> half that per band.
+template <int J, int LP, int BW>
+__device__ __forceinline__ void warp_ana_level(const Ana2dParams& p, const void* srcv, unsigned char* sc, int64_t b,
+                                               int64_t row0, int64_t colw) {
+  constexpr int NR = 32 >> (J - 1), NC = BW >> (J - 1);
+  constexpr int SP = J == 1 ? 256 : NC;                      // J = 1 reads the TMA stage (pitch TC)
+  constexpr bool src64 = J - 1 >= kFirstF64Level;
+  constexpr bool cmp64 = J >= kFirstF64Level;
+  using TS = typename std::conditional<src64, double, float>::type;
+  using TC = typename std::conditional<cmp64, double, float>::type;
+  constexpr int OC = NC / 2, V = OC >= 2 ? 2 : 1, UPR = OC / V, NU = (NR / 2) * UPR;
+  const TS* src = static_cast<const TS*>(srcv);
+  const int lane = threadIdx.x & 31;
+  const int64_t W = p.W;
+  const int64_t brow = row0 >> J, bcol = colw >> J;
+  float* const base = p.out + (b * p.H + brow) * W + bcol;
+  const int64_t wg = W >> J, hgW = (p.H >> J) * W;
+  TC* lldst = nullptr;
+  if constexpr (J < LP) lldst = reinterpret_cast<TC*>(sc + AnaScratch<BW>::off(J));
+  const TC half = TC(0.5);
+#pragma unroll
+  for (int it = 0; it < (NU + 31) / 32; ++it) {
+    const int u = lane + 32 * it;
+    if (NU % 32 != 0 && u >= NU) break;
+    const int orow = u / UPR, oc = (u - orow * UPR) * V;
+    TS t0[2 * V], t1[2 * V];
+    load_row<TS, 2 * V, true>(src + (2 * orow) * SP + 2 * oc, t0);
+    load_row<TS, 2 * V, true>(src + (2 * orow + 1) * SP + 2 * oc, t1);
+    float hl[V], lh[V], hh[V];
+    TC ll[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const TC a = TC(t0[2 * v]), bb = TC(t0[2 * v + 1]), c = TC(t1[2 * v]), d = TC(t1[2 * v + 1]);
+      const TC s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+      ll[v] = (s1 + s2) * half;
+      lh[v] = float((s1 - s2) * half);
+      hl[v] = float((d1 + d2) * half);
+      hh[v] = float((d1 - d2) * half);
+    }
+    float* const pr = base + int64_t(orow) * W + oc;
+    store_row<V, true>(pr + wg, hl, V);
+    store_row<V, true>(pr + hgW, lh, V);
+    store_row<V, true>(pr + hgW + wg, hh, V);
+    if constexpr (J < LP) {
+      store_ll_smem<TC, V>(lldst + orow * OC + oc, ll);
+    } else {
+      if (p.final_pass) {
+        float llf[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) llf[v] = float(ll[v]);
+        store_row<V, true>(pr, llf, V);
+      } else {   // fp64 hand-off of LL_LP (pitch = padded Win >> LP, see fhwt_api.cu)
+        const int64_t wpitch = ((p.Win >> LP) + 3) & ~int64_t(3);
+        double* w = p.ws_out + (b * (p.Hin >> LP) + brow + orow) * wpitch + bcol + oc;
+#pragma unroll
+        for (int v = 0; v < V; ++v) w[v] = double(ll[v]);
+      }
+    }
+  }
+}
+
+template <int J, int LP, int BW>
+__device__ __forceinline__ void warp_ana_rest(const Ana2dParams& p, unsigned char* sc, int64_t b, int64_t row0,
+                                              int64_t colw) {
+  if constexpr (J <= LP) {
+    __syncwarp();
+    warp_ana_level<J, LP, BW>(p, sc + AnaScratch<BW>::off(J - 1), sc, b, row0, colw);
+    warp_ana_rest<J + 1, LP, BW>(p, sc, b, row0, colw);
+  }
+}
+
+// lane-0 version of ana_issue_tile (the releasing warp's lane 0 refills the stage)
+__device__ __forceinline__ void ana_issue_tile_lane(const Ana2dParams& p, const CUtensorMap* map, unsigned char* dst,
+                                                    uint64_t* bar, int64_t t, uint32_t bytes, uint32_t row_bytes,
+                                                    uint64_t pol) {
+  const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+  mbar_arrive_expect_tx(bar, bytes);
+  if (p.l2hint)
+    for (int r = 0; r < 32; ++r) tma_load_2d(dst + r * row_bytes, map, int(ct * 256), int(rt * 32 + r), bar, pol);
+  else
+    for (int r = 0; r < 32; ++r) tma_load_2d_nohint(dst + r * row_bytes, map, int(ct * 256), int(rt * 32 + r), bar);
+}
+
+// BW = columns per warp block (32: 8 warps per 32 x 256 tile; 64: 4 warps, level-1 band rows of
+// 128 B per warp and full 32-B sectors down to level 3).
+template <int LP, int BW>
+__global__ void __launch_bounds__(32 * (256 / BW), BW == 64 ? 4 : FHWT_MINB_ANA)
+    ana2d_warp_kernel(const __grid_constant__ Ana2dParams p, const __grid_constant__ CUtensorMap in_map) {
+  constexpr unsigned NW = 256 / BW;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  unsigned* cnt = reinterpret_cast<unsigned*>(smem + p.bar_off + 8 * p.stages);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned char* sc = smem + p.p_off[0] + warp * kWarpScratchBytes;
+  constexpr uint32_t row_bytes = 256 * 4, tile_bytes = 32 * row_bytes;
+  if (tid == 0) {
+    prefetch_tmap(&in_map);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&bars[s], 1);
+      cnt[s] = 0;
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  if (tid == 0)
+    for (int s = 0; s < p.stages; ++s) {
+      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
+      if (t < p.ntiles) ana_issue_tile_lane(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, tile_bytes, row_bytes, pol);
+    }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+    const int s = it % p.stages;
+    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256);
+    const int64_t colw = xy.col0 + BW * warp;
+    warp_ana_level<1, LP, BW>(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes) + BW * warp, sc, xy.b,
+                              xy.row0, colw);
+    __syncwarp();
+    if (lane == 0) {   // stage release: the last warp through level 1 refills it
+      __threadfence_block();
+      if ((atomicAdd(&cnt[s], 1u) % NW) == NW - 1) {
+        const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
+        if (nt < p.ntiles)
+          ana_issue_tile_lane(p, &in_map, smem + s * p.stage_bytes, &bars[s], nt, tile_bytes, row_bytes, pol);
+      }
+    }
+    warp_ana_rest<2, LP, BW>(p, sc, xy.b, xy.row0, colw);
+    __syncwarp();   // scratch is rewritten by the next tile
   }
 }
 
@@ -449,6 +644,138 @@ __device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMa
       tma_load_2d(base + p.box_off[j][0] + r * rb, &maps.level[j], hc, int(br + r), bar, pol);
       tma_load_2d(base + p.box_off[j][1] + r * rb, &maps.level[j], int(bc), int(br + hg + r), bar, pol);
       tma_load_2d(base + p.box_off[j][2] + r * rb, &maps.level[j], hc, int(br + hg + r), bar, pol);
+    }
+  }
+}
+
+// --------------------------------------------------- warp-decoupled synthesis (32 x 256 tiles)
+// Mirror of ana2d_warp_kernel: warp w rebuilds output columns [32w, 32w + 32) of a tile from the
+// level-j coefficient blocks at columns [(32w) >> j, (32w + 32) >> j) of the staged boxes.
+__device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* base,
+                                                    uint64_t* bar, int64_t t, uint64_t pol) {
+  const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+  const int64_t b = rt / p.tiles_r;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = ct * p.TC;
+  mbar_arrive_expect_tx(bar, p.tx_bytes);
+  const int L = p.Lp;
+  const int64_t llrow = p.ll_from_ws ? b * (p.Hin >> L) + (row0 >> L) : b * p.H + (row0 >> L);
+  const int llrows = p.row_boxes[L] ? (p.TR >> L) : 1;
+  for (int r = 0; r < llrows; ++r)
+    tma_load_2d(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int(col0 >> L), int(llrow + r), bar, pol);
+  for (int j = L; j >= 1; --j) {
+    const int g = p.g0 + j;
+    const int64_t hg = p.H >> g, wg = p.W >> g;
+    const int64_t br = b * p.H + (row0 >> j), bc = col0 >> j;
+    const int rb = p.box_pitch[j] * 4;
+    const int nrows = p.row_boxes[j] ? (p.TR >> j) : 1;
+    for (int r = 0; r < nrows; ++r) {
+      tma_load_2d(base + p.box_off[j][0] + r * rb, &maps.level[j], int(wg + bc), int(br + r), bar, pol);
+      tma_load_2d(base + p.box_off[j][1] + r * rb, &maps.level[j], int(bc), int(br + hg + r), bar, pol);
+      tma_load_2d(base + p.box_off[j][2] + r * rb, &maps.level[j], int(wg + bc), int(br + hg + r), bar, pol);
+    }
+  }
+}
+
+template <int J>
+__device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float* __restrict__ ll, int llp,
+                                               const unsigned char* stage, int warp, float* __restrict__ dst,
+                                               int64_t b, int64_t row0, int64_t colw) {
+  constexpr int R = 32 >> J, C = 32 >> J, BP = 256 >> J;
+  constexpr int V = C >= 2 ? 2 : 1, UPR = C / V, NU = R * UPR, OC = 2 * C;
+  const int co = (32 * warp) >> J;
+  const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]) + co;
+  const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]) + co;
+  const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]) + co;
+  const int lane = threadIdx.x & 31;
+  float* const obase = p.out + (b * p.Hin + row0) * p.out_pitch + colw;
+#pragma unroll
+  for (int it = 0; it < (NU + 31) / 32; ++it) {
+    const int u = lane + 32 * it;
+    if (NU % 32 != 0 && u >= NU) break;
+    const int r = u / UPR, c = (u - r * UPR) * V;
+    float vll[V], vhl[V], vlh[V], vhh[V];
+    load_row<float, V, true>(ll + r * llp + c, vll);
+    load_row<float, V, true>(hl + r * BP + c, vhl);
+    load_row<float, V, true>(lh + r * BP + c, vlh);
+    load_row<float, V, true>(hh + r * BP + c, vhh);
+    float top[2 * V], bot[2 * V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const float s = vll[v] + vlh[v], t = vhl[v] + vhh[v];
+      const float s2 = vll[v] - vlh[v], t2 = vhl[v] - vhh[v];
+      top[2 * v] = (s + t) * 0.5f;
+      top[2 * v + 1] = (s - t) * 0.5f;
+      bot[2 * v] = (s2 + t2) * 0.5f;
+      bot[2 * v + 1] = (s2 - t2) * 0.5f;
+    }
+    if constexpr (J > 1) {
+      float* d0 = dst + (2 * r) * OC + 2 * c;
+      if constexpr (V == 2) {
+        *reinterpret_cast<float4*>(d0) = make_float4(top[0], top[1], top[2], top[3]);
+        *reinterpret_cast<float4*>(d0 + OC) = make_float4(bot[0], bot[1], bot[2], bot[3]);
+      } else {
+        *reinterpret_cast<float2*>(d0) = make_float2(top[0], top[1]);
+        *reinterpret_cast<float2*>(d0 + OC) = make_float2(bot[0], bot[1]);
+      }
+    } else {
+      float* o = obase + int64_t(2 * r) * p.out_pitch + 2 * c;
+      store_out_row<V, true>(o, top, 2 * V);
+      store_out_row<V, true>(o + p.out_pitch, bot, 2 * V);
+    }
+  }
+}
+
+template <int J, int LP>
+__device__ __forceinline__ void warp_syn_steps(const Syn2dParams& p, const float* ll, int llp,
+                                               const unsigned char* stage, int warp, WarpScratch* sc, int64_t b,
+                                               int64_t row0, int64_t colw) {
+  float* dst = J == 5 ? reinterpret_cast<float*>(sc->ll4) : J == 4 ? sc->ll3 : J == 3 ? sc->ll2 : sc->ll1;
+  warp_syn_level<J>(p, ll, llp, stage, warp, dst, b, row0, colw);
+  if constexpr (J > 1) {
+    __syncwarp();
+    warp_syn_steps<J - 1, LP>(p, dst, 2 * (32 >> J), stage, warp, sc, b, row0, colw);
+  }
+}
+
+template <int LP>
+__global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(const __grid_constant__ Syn2dParams p,
+                                                                const __grid_constant__ TmaMaps2d maps) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  unsigned* cnt = reinterpret_cast<unsigned*>(smem + p.bar_off + 8 * p.stages);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  WarpScratch* sc = reinterpret_cast<WarpScratch*>(smem + p.p_off[0] + warp * kSynScratchBytes);
+  if (tid == 0) {
+    for (int j = 1; j <= LP; ++j) prefetch_tmap(&maps.level[j]);
+    prefetch_tmap(&maps.ll);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&bars[s], 1);
+      cnt[s] = 0;
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  if (tid == 0)
+    for (int s = 0; s < p.stages; ++s) {
+      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
+      if (t < p.ntiles) syn_issue_tile_lane(p, maps, smem + s * p.stage_bytes, &bars[s], t, pol);
+    }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+    const int s = it % p.stages;
+    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256);
+    const unsigned char* stage = smem + s * p.stage_bytes;
+    const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> LP);
+    warp_syn_steps<LP, LP>(p, ll, 256 >> LP, stage, warp, sc, xy.b, xy.row0, xy.col0 + 32 * warp);
+    __syncwarp();
+    if (lane == 0) {   // stage release: the 8th warp through level 1 refills it
+      __threadfence_block();
+      if ((atomicAdd(&cnt[s], 1u) & 7u) == 7u) {
+        const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
+        if (nt < p.ntiles) syn_issue_tile_lane(p, maps, smem + s * p.stage_bytes, &bars[s], nt, pol);
+      }
     }
   }
 }
@@ -653,24 +980,53 @@ struct SynF2 {
 };
 
 // fast: 0 = generic kernel; else (mode << 24) | (tile rows << 16) | (tile cols << 4) | LP
+template <template <int> class K>
+static const void* warp_fn(int lp) {
+  switch (lp) {
+    case 1: return K<1>::get();
+    case 2: return K<2>::get();
+    case 3: return K<3>::get();
+    case 4: return K<4>::get();
+    case 5: return K<5>::get();
+    default: return nullptr;
+  }
+}
+template <int LP>
+struct AnaW {
+  static const void* get() { return (const void*)ana2d_warp_kernel<LP, 32>; }
+};
+template <int LP>
+struct AnaW64 {
+  static const void* get() { return (const void*)ana2d_warp_kernel<LP, 64>; }
+};
+template <int LP>
+struct SynW {
+  static const void* get() { return (const void*)syn2d_warp_kernel<LP>; }
+};
+
 static const void* ana2d_fn(bool in_f64, int fast) {
   if (in_f64) return (const void*)ana2d_kernel<double, 0, 0, 0>;
   if (fast == 0) return (const void*)ana2d_kernel<float, 0, 0, 0>;
+  if (((fast >> 24) & 0xff) == 1) return warp_fn<AnaW>(fast & 15);
+  if (((fast >> 24) & 0xff) == 4) return warp_fn<AnaW64>(fast & 15);
   return by_geometry<AnaF>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15);
 }
 
 static const void* syn2d_fn(int fast) {
   if (fast == 0) return (const void*)syn2d_kernel<0, 0, 0, 0>;
   const int mode = (fast >> 24) & 0xff;
+  if (mode == 3) return warp_fn<SynW>(fast & 15);
   return mode == 2 ? by_geometry<SynF2>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15)
                    : by_geometry<SynF0>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15);
 }
+
+int ana2d_threads(int fast) { return ((fast >> 24) & 0xff) == 4 ? 128 : kThreads2d; }
 
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm) {
   const void* fn = ana2d_fn(in_f64, fast_lp);
   cudaError_t e = raise_smem_cap(fn);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kThreads2d, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, ana2d_threads(in_f64 ? 0 : fast_lp), smem);
 }
 
 cudaError_t syn2d_occupancy(int fast_lp, size_t smem, int* blocks_per_sm) {
@@ -684,7 +1040,8 @@ cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool i
                          size_t smem, cudaStream_t s) {
   count_launch();
   void* args[] = {const_cast<Ana2dParams*>(&p), const_cast<CUtensorMap*>(&in_map)};
-  return cudaLaunchKernel(ana2d_fn(in_f64, fast_lp), dim3(grid), dim3(kThreads2d), args, smem, s);
+  return cudaLaunchKernel(ana2d_fn(in_f64, fast_lp), dim3(grid), dim3(ana2d_threads(in_f64 ? 0 : fast_lp)), args,
+                          smem, s);
 }
 
 cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int fast_lp, int grid, size_t smem,

@@ -363,3 +363,26 @@ def test_long_signal_segments_bitwise_equal(world):
         seg = fhwt.analyze_1d(x[:, s0:s1].contiguous(), J)[0]
         for band, (lo, go, ln) in fdist.segment_bands_1d(s0, s1, N, J).items():
             assert torch.equal(seg[lo:lo + ln], full[go:go + ln]), (r, band)
+
+
+@pytest.mark.parametrize("knob,values", [("FHWT_ANA_WARP", ["0", "1", "2"]), ("FHWT_SYN_MODE", ["0", "2", "3"])])
+@pytest.mark.parametrize("levels", [1, 3, 5, 7])
+def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
+    """Every selectable 2-D kernel variant (CTA-synchronous, warp-decoupled 32/64-column blocks for
+    analysis; TMA boxes, cp.async, warp-decoupled for synthesis) performs the same arithmetic in the
+    same order, so outputs agree bitwise; the default is also checked against the oracle.  Shape:
+    3 images 128 x 512 (full 32 x 256 tiles, several per image, and the L > 5 second pass)."""
+    x = np.stack([datagen.c4_image(i, 512)[:128] for i in range(3)])
+    xd = dev(x)
+    outs = []
+    for v in values:
+        monkeypatch.setenv(knob, v)
+        c = fhwt.analyze_2d(xd, levels)
+        r = fhwt.synthesize_2d(c, levels)
+        torch.cuda.synchronize()
+        outs.append((c.clone(), r.clone()))
+    monkeypatch.delenv(knob)
+    for c, r in outs[1:]:
+        assert torch.equal(c, outs[0][0]) and torch.equal(r, outs[0][1])
+    assert_close(host(outs[0][0]), o.analyze_2d(x, levels), x, 2, what=f"variants L={levels}")
+    assert_close(host(outs[0][1]), x, x, 2, what=f"variants round trip L={levels}")

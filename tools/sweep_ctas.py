@@ -9,7 +9,7 @@ import torch  # noqa: E402
 import paper_1002_2184_b200 as fhwt  # noqa: E402
 
 
-def timeit(fn, reps=10):
+def timeit(fn, reps=int(os.environ.get("FHWT_TIMEIT_REPS", "10"))):
     for _ in range(3):
         fn()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
