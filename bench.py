@@ -178,6 +178,8 @@ def measure(name, cfg, args, ws, rank, local, pg):
         ll_local = torch.empty((ll_rows, ll_cols), dtype=torch.float32, device=dev)
         ll_all = torch.empty((ll_rows * ws, ll_cols), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(dev)     # c5: LL pack + all-gather, overlapped with the synthesis pass
+    ana_done = torch.cuda.Event()
 
     def step(evs=None):
         if evs:
@@ -186,12 +188,24 @@ def measure(name, cfg, args, ws, rank, local, pg):
         if evs:
             evs[1].record(stream)
         if cfg["shard"] == "rowband":
-            fhwt.pack_ll_2d(coeffs, L, out=ll_local)      # K6 pack (same kernel family, counted)
-            if gather:   # the only exchange (NCCL over NVLink): coarsest LL of every band
-                fdist.gather_coarse_ll(ll_local, group=pg, out=ll_all)
-        if evs:
+            # Synthesis needs only this band's own coefficients, so the pack (K6)
+            # and the one exchange (NCCL all-gather of the coarsest LL) run on a side stream.
+            ana_done.record(stream)
+            side.wait_event(ana_done)
+            with torch.cuda.stream(side):
+                if evs:
+                    evs[4].record(side)
+                fhwt.pack_ll_2d(coeffs, L, out=ll_local, stream=side)
+                if gather:
+                    fdist.gather_coarse_ll(ll_local, group=pg, out=ll_all)
+                if evs:
+                    evs[2].record(side)
+        elif evs:
+            evs[4].record(stream)
             evs[2].record(stream)
         plan.synthesize(coeffs, out=rec, workspace=wsb)
+        if cfg["shard"] == "rowband":
+            stream.wait_stream(side)      # the step ends when the gathered LL is in place too
         if evs:
             evs[3].record(stream)
 
@@ -204,7 +218,7 @@ def measure(name, cfg, args, ws, rank, local, pg):
         parity["gathered_ll"] = check_gathered_ll(ll_all, ll_local, rank, ws)
 
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
     if ws > 1:
         dist.barrier(group=pg)
     torch.cuda.synchronize(dev)
@@ -222,8 +236,8 @@ def measure(name, cfg, args, ws, rank, local, pg):
         dist.barrier(group=pg)
     total_ms = start.elapsed_time(end)
     ana = [e[0].elapsed_time(e[1]) for e in evs]
-    mid = [e[1].elapsed_time(e[2]) for e in evs]
-    syn = [e[2].elapsed_time(e[3]) for e in evs]
+    mid = [e[4].elapsed_time(e[2]) for e in evs]      # pack + gather on the side stream
+    syn = [e[1].elapsed_time(e[3]) for e in evs]      # synthesis (+ the gather's tail, if any)
     vals = [total_ms, statistics.mean(ana), statistics.mean(syn), statistics.mean(mid)]
     if ws > 1:
         vals = fdist.max_over_ranks(vals, device=dev, group=pg)

@@ -171,29 +171,44 @@ def haar_filter_bank() -> FilterBank:
 
 
 # ------------------------------------------------------------------ tensor marshalling
-def _stream(stream):
-    import torch
-    s = torch.cuda.current_stream() if stream is None else stream
-    return ctypes.c_void_p(s.cuda_stream)
+# Per-call host cost matters for the latency-bound configs (c1, c3): the helpers below use
+# torch's raw current-stream / current-device queries and plain attribute checks (a call costs
+# ~2 us of Python on top of the C ABI call).
+_torch = None
+
+
+def _t():
+    global _torch
+    if _torch is None:
+        import torch
+        _torch = torch
+    return _torch
+
+
+def _stream(stream, t=None):
+    torch = _t()
+    if stream is None:
+        dev = t.get_device() if t is not None else torch._C._cuda_getDevice()
+        return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(dev))
+    return ctypes.c_void_p(stream.cuda_stream)
 
 
 def _dev_f32(t, what):
-    import torch
+    torch = _t()
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{what} must be a torch.Tensor")
     if not t.is_cuda:
         raise InvalidArgument(f"{what} must be a CUDA tensor (this library has no CPU path)")
-    if t.dtype != torch.float32:
+    if t.dtype is not torch.float32:
         raise InvalidArgument(f"{what} must be float32, got {t.dtype}")
     if not t.is_contiguous():
         raise InvalidArgument(f"{what} must be contiguous")
-    return ctypes.c_void_p(t.data_ptr())
+    return t.data_ptr()
 
 
 def _out_like(x, out):
-    import torch
     if out is None:
-        return torch.empty_like(x)
+        return _t().empty_like(x)
     if out.shape != x.shape:
         raise ShapeMismatch(f"out has shape {tuple(out.shape)}, expected {tuple(x.shape)}")
     return out
@@ -213,14 +228,25 @@ def _shape_2d(x):
     return h, w, (x.numel() // (h * w) if h * w else 0)
 
 
-def _guard_device(x):
-    import contextlib
+class _NoGuard:
+    def __enter__(self):
+        return None
 
-    import torch
+    def __exit__(self, *exc):
+        return False
+
+
+_NO_GUARD = _NoGuard()
+
+
+def _guard_device(x):
+    """Context that makes x's device current for the call (a no-op when it already is)."""
+    torch = _t()
     _dev_f32(x, "input")          # validate (CUDA, float32, contiguous) before touching the device
-    if x.device.index == torch.cuda.current_device():
-        return contextlib.nullcontext()
-    return torch.cuda.device(x.device)
+    dv = x.get_device()
+    if dv == torch._C._cuda_getDevice():
+        return _NO_GUARD
+    return torch.cuda.device(dv)
 
 
 def analyze_1d(d, levels: int, out=None, stream=None):
@@ -228,7 +254,7 @@ def analyze_1d(d, levels: int, out=None, stream=None):
     n, batch = _shape_1d(d)
     out = _out_like(d, out)
     with _guard_device(d):
-        _check(lib().fhwt_analyze_1d(_dev_f32(d, "d"), _dev_f32(out, "coeffs"), n, batch, int(levels), _stream(stream)))
+        _check(lib().fhwt_analyze_1d(_dev_f32(d, "d"), _dev_f32(out, "coeffs"), n, batch, int(levels), _stream(stream, d)))
     return out
 
 
@@ -238,7 +264,7 @@ def synthesize_1d(coeffs, levels: int, out=None, stream=None):
     out = _out_like(coeffs, out)
     with _guard_device(coeffs):
         _check(lib().fhwt_synthesize_1d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"), n, batch, int(levels),
-                                        _stream(stream)))
+                                        _stream(stream, coeffs)))
     return out
 
 
@@ -248,7 +274,7 @@ def analyze_2d(d, levels: int, out=None, stream=None):
     out = _out_like(d, out)
     with _guard_device(d):
         _check(lib().fhwt_analyze_2d(_dev_f32(d, "d"), _dev_f32(out, "coeffs"), h, w, batch, int(levels),
-                                     _stream(stream)))
+                                     _stream(stream, d)))
     return out
 
 
@@ -258,7 +284,7 @@ def synthesize_2d(coeffs, levels: int, out=None, stream=None):
     out = _out_like(coeffs, out)
     with _guard_device(coeffs):
         _check(lib().fhwt_synthesize_2d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"), h, w, batch, int(levels),
-                                        _stream(stream)))
+                                        _stream(stream, coeffs)))
     return out
 
 
@@ -299,7 +325,7 @@ class _Plan:
         out = _out_like(d, out)
         with _guard_device(d):
             _check(lib().fhwt_plan_analyze(self._h, _dev_f32(d, "d"), _dev_f32(out, "coeffs"), self._ws(d, workspace),
-                                           _stream(stream)))
+                                           _stream(stream, d)))
         return out
 
     def synthesize(self, coeffs, out=None, workspace=None, stream=None):
@@ -307,7 +333,7 @@ class _Plan:
         out = _out_like(coeffs, out)
         with _guard_device(coeffs):
             _check(lib().fhwt_plan_synthesize(self._h, _dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"),
-                                              self._ws(coeffs, workspace), _stream(stream)))
+                                              self._ws(coeffs, workspace), _stream(stream, coeffs)))
         return out
 
 
@@ -348,7 +374,7 @@ def pack_ll_2d(coeffs, levels: int, out=None, stream=None):
         out = torch.empty(shape, dtype=coeffs.dtype, device=coeffs.device)
     with _guard_device(coeffs):
         _check(lib().fhwt_pack_ll_2d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "ll"), h, w, batch, int(levels),
-                                     _stream(stream)))
+                                     _stream(stream, coeffs)))
     return out
 
 
@@ -418,7 +444,7 @@ def direct_analyze_1d(d, levels: int, out=None, workspace=None, stream=None):
     out = _out_like(d, out)
     with _guard_device(d):
         _check(lib().fhwt_direct_analyze_1d(_dev_f32(d, "d"), _dev_f32(out, "coeffs"), n, batch, int(levels),
-                                            _direct_ws(d, 1, n, 0, batch, workspace), _stream(stream)))
+                                            _direct_ws(d, 1, n, 0, batch, workspace), _stream(stream, d)))
     return out
 
 
@@ -429,7 +455,7 @@ def direct_synthesize_1d(coeffs, levels: int, out=None, workspace=None, stream=N
     with _guard_device(coeffs):
         _check(lib().fhwt_direct_synthesize_1d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"), n, batch,
                                                int(levels), _direct_ws(coeffs, 1, n, 0, batch, workspace),
-                                               _stream(stream)))
+                                               _stream(stream, coeffs)))
     return out
 
 
@@ -438,7 +464,7 @@ def direct_analyze_2d(d, levels: int, out=None, workspace=None, stream=None):
     out = _out_like(d, out)
     with _guard_device(d):
         _check(lib().fhwt_direct_analyze_2d(_dev_f32(d, "d"), _dev_f32(out, "coeffs"), h, w, batch, int(levels),
-                                            _direct_ws(d, 2, h, w, batch, workspace), _stream(stream)))
+                                            _direct_ws(d, 2, h, w, batch, workspace), _stream(stream, d)))
     return out
 
 
@@ -448,7 +474,7 @@ def direct_synthesize_2d(coeffs, levels: int, out=None, workspace=None, stream=N
     with _guard_device(coeffs):
         _check(lib().fhwt_direct_synthesize_2d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"), h, w, batch,
                                                int(levels), _direct_ws(coeffs, 2, h, w, batch, workspace),
-                                               _stream(stream)))
+                                               _stream(stream, coeffs)))
     return out
 
 
@@ -476,5 +502,5 @@ def lowpass_2d_u8(d, levels: int, out=None, stream=None):
         out = torch.empty(shape, dtype=torch.float32, device=d.device)
     with torch.cuda.device(d.device):
         _check(lib().fhwt_lowpass_2d_u8(ctypes.c_void_p(d.data_ptr()), _dev_f32(out, "ll"), h, w, batch, int(levels),
-                                        None, _stream(stream)))
+                                        None, _stream(stream, d)))
     return out
