@@ -296,6 +296,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     // 1-KB boxes stream at 6.9 TB/s where one 32-row box stops at 6.1 TB/s; smaller row boxes
     // are request-bound and slower than multi-row boxes.
     p.l2hint = env_int("FHWT_ANA_L2HINT", 1);
+    p.fused = env_int("FHWT_ANA_FUSED", ps.Lp == 5 ? 1 : 0);   // measured: +3 % at LP = 5, slower at 3 and 4
     p.row_boxes = size_t(p.TC) * (in64 ? 8 : 4) >= 1024 && (size_t(p.TC) * (in64 ? 8 : 4)) % 128 == 0;
     FHWT_TRY(encode_2d(&map, in, in64, p.Win, B * p.Hin, in_pitch, p.TC, p.row_boxes ? 1 : p.TR));
     // shared memory layout: stages | P[0] | P[1] | barriers

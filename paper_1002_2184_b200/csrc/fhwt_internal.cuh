@@ -42,6 +42,7 @@ struct Ana2dParams {
   int stages;
   uint32_t stage_bytes, p_off[2], bar_off;
   int final_pass;
+  int fused;             // 32 x 256 fast tiles, LP >= 3: levels 2+3 and 4+5 fused (FHWT_ANA_FUSED, default 1)
   int l2hint;            // 1: TMA loads carry an L2 evict_first policy (sweep knob FHWT_ANA_L2HINT)
   int row_boxes;         // 1: the map's box is one row and TR boxes are issued per tile (rows of
                          // 128-B multiples; TMA smem destinations must be 128-B aligned); 0: one TR-row box

@@ -236,6 +236,122 @@ __device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* 
   }
 }
 
+// Two levels of one thread's 4 x 4 LL block (rows r0.., cols c0.. of the level-(J-1) band block):
+// level J gives 2 x 2 outputs per band, level J+1 one output per band and LL_{J+1}.  TA: level-J
+// arithmetic type, TB: level-(J+1) type (fp64 from kFirstF64Level).
+template <typename TA, typename TB, int J, int LP>
+__device__ __forceinline__ TB ana_pair(const Ana2dParams& p, const float (&x)[4][4], int64_t b, int64_t row0,
+                                       int64_t col0, int br, int bc) {
+  const int64_t W = p.W;
+  TA ll[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {   // level J: rows 2br + i, cols 2bc + {0, 1} of the level-J bands
+    float hl[2], lh[2], hh[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const TA a = TA(x[2 * i][2 * k]), bb = TA(x[2 * i][2 * k + 1]);
+      const TA c = TA(x[2 * i + 1][2 * k]), d = TA(x[2 * i + 1][2 * k + 1]);
+      const TA s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+      ll[i][k] = (s1 + s2) * TA(0.5);
+      lh[k] = float((s1 - s2) * TA(0.5));
+      hl[k] = float((d1 + d2) * TA(0.5));
+      hh[k] = float((d1 - d2) * TA(0.5));
+    }
+    float* pr = p.out + (b * p.H + (row0 >> J) + 2 * br + i) * W + (col0 >> J) + 2 * bc;
+    const int64_t wg = W >> J, hgW = (p.H >> J) * W;
+    stg_stream2(pr + wg, make_float2(hl[0], hl[1]));
+    stg_stream2(pr + hgW, make_float2(lh[0], lh[1]));
+    stg_stream2(pr + hgW + wg, make_float2(hh[0], hh[1]));
+  }
+  // level J + 1 on the 2 x 2 LL_J block (rounded to TA first, exactly as the level-by-level kernel)
+  const TB a = TB(ll[0][0]), bb = TB(ll[0][1]), c = TB(ll[1][0]), d = TB(ll[1][1]);
+  const TB s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+  constexpr int J1 = J + 1;
+  float* pr = p.out + (b * p.H + (row0 >> J1) + br) * W + (col0 >> J1) + bc;
+  const int64_t wg = W >> J1, hgW = (p.H >> J1) * W;
+  stg_stream1(pr + wg, float((d1 + d2) * TB(0.5)));
+  stg_stream1(pr + hgW, float((s1 - s2) * TB(0.5)));
+  stg_stream1(pr + hgW + wg, float((d1 - d2) * TB(0.5)));
+  const TB ll1 = (s1 + s2) * TB(0.5);
+  if constexpr (J1 == LP) {   // last level of the pass: LL to the coefficients or the fp64 hand-off
+    if (p.final_pass) {
+      stg_stream1(pr, float(ll1));
+    } else {
+      const int64_t wpitch = ((p.Win >> LP) + 3) & ~int64_t(3);
+      p.ws_out[(b * (p.Hin >> LP) + (row0 >> LP) + br) * wpitch + (col0 >> LP) + bc] = double(ll1);
+    }
+  }
+  return ll1;
+}
+
+// Fused fast path for 32 x 256 tiles, LP in 3..5: level 1 by all threads, levels 2+3 in one step
+// (128 threads, one 4 x 4 LL1 block each), levels 4+5 in one step (8 threads, one 4 x 4 LL3 block
+// each).  Two CTA barriers per tile instead of five, and the levels 4-5 threads overlap the next
+// tile's level 1 (LL1 and LL3 live in different buffers; the next tile's first barrier orders the
+// reuse).  Same arithmetic, same order, as ana_fast_step: outputs are bitwise identical.
+template <int LP>
+__device__ __forceinline__ void ana_fused_tile(const Ana2dParams& p, const float* stage, unsigned char* smem, int64_t b,
+                                               int64_t row0, int64_t col0, const Refill& refill) {
+  static_assert(LP >= 3 && LP <= 5, "fused path covers 3..5 levels");
+  float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]);   // 16 x 128
+  float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);   // 4 x 32
+  ana_level<float, float, 2, 32, 256, true>(p, stage, 32, 256, 1, b, row0, col0, ll1, false);
+  __syncthreads();
+  refill();
+  const int tid = threadIdx.x;
+  if (tid < 128) {   // levels 2 + 3: block (br, bc) of LL1, 4 x 32 blocks
+    const int br = tid >> 5, bc = tid & 31;
+    float x[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(ll1 + (4 * br + r) * 128 + 4 * bc);
+      x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+    }
+    const float l3 = ana_pair<float, float, 2, LP>(p, x, b, row0, col0, br, bc);
+    if constexpr (LP > 3) ll3[br * 32 + bc] = l3;
+  }
+  if constexpr (LP > 3) {
+    __syncthreads();
+    if (tid >= 224 && tid < 232) {   // levels 4 (+ 5): warp 7 lanes 0..7, block q of LL3 (4 x 32)
+      const int q = tid - 224;
+      float x[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float4 v = *reinterpret_cast<const float4*>(ll3 + r * 32 + 4 * q);
+        x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+      }
+      if constexpr (LP == 5) {
+        ana_pair<double, double, 4, 5>(p, x, b, row0, col0, 0, q);
+      } else {   // LP == 4: level 4 only, on the two 2 x 4 halves of the block
+        const int64_t W = p.W;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          float hl[2], lh[2], hh[2], llv[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const double a = x[2 * i][2 * k], bb = x[2 * i][2 * k + 1], c = x[2 * i + 1][2 * k], d = x[2 * i + 1][2 * k + 1];
+            const double s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+            llv[k] = float((s1 + s2) * 0.5);
+            lh[k] = float((s1 - s2) * 0.5);
+            hl[k] = float((d1 + d2) * 0.5);
+            hh[k] = float((d1 - d2) * 0.5);
+            if (!p.final_pass) {
+              const int64_t wpitch = ((p.Win >> 4) + 3) & ~int64_t(3);
+              p.ws_out[(b * (p.Hin >> 4) + (row0 >> 4) + i) * wpitch + (col0 >> 4) + 2 * q + k] = (s1 + s2) * 0.5;
+            }
+          }
+          float* pr = p.out + (b * p.H + (row0 >> 4) + i) * W + (col0 >> 4) + 2 * q;
+          const int64_t wg = W >> 4, hgW = (p.H >> 4) * W;
+          stg_stream2(pr + wg, make_float2(hl[0], hl[1]));
+          stg_stream2(pr + hgW, make_float2(lh[0], lh[1]));
+          stg_stream2(pr + hgW + wg, make_float2(hh[0], hh[1]));
+          if (p.final_pass) stg_stream2(pr, make_float2(llv[0], llv[1]));
+        }
+      }
+    }
+  }
+}
+
 template <typename TIn, int LPFAST, int TRF, int TCF>
 __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_ANA) ana2d_kernel(const __grid_constant__ Ana2dParams p,
                                                            const __grid_constant__ CUtensorMap in_map) {
@@ -268,7 +384,15 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_ANA) ana2d_kernel(const 
     const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
     const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
                         tile_bytes, row_bytes, pol};
-    if constexpr (LPFAST > 0) {
+    if constexpr (LPFAST >= 3 && TRF == 32 && TCF == 256) {
+      if (p.fused) {   // 2 barriers per tile (see ana_fused_tile)
+        ana_fused_tile<LPFAST>(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC,
+                               refill);
+      } else {
+        ana_fast_step<1, LPFAST, TRF, TCF>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC, refill);
+        __syncthreads();  // LL buffers free again
+      }
+    } else if constexpr (LPFAST > 0) {
       ana_fast_step<1, LPFAST, TRF, TCF>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC, refill);
       __syncthreads();  // LL buffers free again
       if constexpr (LPFAST == 1) refill();
