@@ -255,6 +255,16 @@ int choose_tr(int64_t rows, int Lp) {
   return std::max(tr, 1 << Lp);
 }
 
+// Small problems (fewer tiles than SMs, e.g. one 512 x 512 image): shorter and narrower tiles so
+// the work spreads over more SMs; each CTA's serial chain (load, levels, store) is what sets the
+// latency there.  Only between compile-time fast geometries (rows 8/16/32, columns 128/256).
+void shrink_for_small(int64_t batch, int64_t rows, int64_t cols, int Lp, int sms, int* TR, int* TC) {
+  if (env_int("FHWT_SMALL_TILES", 1) == 0) return;
+  auto tiles = [&] { return batch * (rows / *TR) * ((cols + *TC - 1) / *TC); };
+  while (tiles() < sms && *TR > std::max(8, 1 << Lp) && rows % (*TR / 2) == 0) *TR /= 2;
+  if (tiles() < sms && *TC == 256 && cols % 128 == 0) *TC = 128;
+}
+
 // ------------------------------------------------------------------ 2-D execution
 fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char* ws, cudaStream_t s) {
   const int64_t H = pl->h, W = pl->w, B = pl->batch;
@@ -283,6 +293,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     p.TR = choose_tr(p.Hin, ps.Lp);
     p.TC = int(std::min<int64_t>(in64 ? 128 : env_int("FHWT_ANA_TC", 256), p.Win));
     if (!in64 && p.TC == 256 && p.Win % 256 && p.Win % 128 == 0) p.TC = 128;   // full tiles -> fast path
+    if (!in64) shrink_for_small(B, p.Hin, p.Win, ps.Lp, di.sms, &p.TR, &p.TC);
     p.tiles_r = p.Hin / p.TR;
     p.tiles_c = (p.Win + p.TC - 1) / p.TC;
     p.ntiles = B * p.tiles_r * p.tiles_c;
@@ -361,6 +372,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     p.TR = choose_tr(p.Hin, ps.Lp);
     p.TC = int(std::min<int64_t>(env_int("FHWT_SYN_TC", 256), p.Win));
     if (p.TC == 256 && p.Win % 256 && p.Win % 128 == 0) p.TC = 128;   // full tiles -> fast path
+    if (ps.g0 == 0) shrink_for_small(B, p.Hin, p.Win, ps.Lp, di.sms, &p.TR, &p.TC);
     p.tiles_r = p.Hin / p.TR;
     p.tiles_c = (p.Win + p.TC - 1) / p.TC;
     p.ntiles = B * p.tiles_r * p.tiles_c;
