@@ -109,6 +109,12 @@ fhwt_status fhwt_plan_analyze(fhwt_plan p, const float *d, float *coeffs, void *
 fhwt_status fhwt_plan_synthesize(fhwt_plan p, const float *coeffs, float *d_R, void *workspace,
                                  fhwt_stream_t s);
 
+/* The same three plan calls under the names of SURVEY §8(b) (fhwt_workspace_bytes, fhwt_analyze,
+ * fhwt_synthesize): identical arguments, behaviour and errors. */
+size_t fhwt_workspace_bytes(fhwt_plan p);
+fhwt_status fhwt_analyze(fhwt_plan p, const float *d, float *coeffs, void *workspace, fhwt_stream_t s);
+fhwt_status fhwt_synthesize(fhwt_plan p, const float *coeffs, float *d_R, void *workspace, fhwt_stream_t s);
+
 /* ------------------------------------------------------------------ one-shot entry points
  * Equivalent to plan + call + destroy with the §II filter bank. */
 fhwt_status fhwt_analyze_1d(const float *d, float *coeffs, int64_t n, int64_t batch, int levels, fhwt_stream_t s);
@@ -132,6 +138,9 @@ int64_t fhwt_band_offset_2d(int64_t h, int64_t w, int level, int band, int64_t *
  * row-band sharded images. */
 fhwt_status fhwt_pack_ll_2d(const float *coeffs, float *ll_packed, int64_t h, int64_t w, int64_t batch,
                             int levels, fhwt_stream_t s);
+/* The same pack with (h, w, batch, levels) taken from a 2-D plan (SURVEY §8(b) form).
+ * Errors: INVALID_ARG (NULL plan, 1-D plan, NULL buffers). */
+fhwt_status fhwt_plan_pack_ll_2d(fhwt_plan p, const float *coeffs, float *ll_packed, fhwt_stream_t s);
 
 /* ------------------------------------------------------------------ host-buffer round trip
  * End-to-end DWT + IDWT on HOST buffers (pinned memory recommended): the batch is streamed in

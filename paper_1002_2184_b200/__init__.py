@@ -126,6 +126,10 @@ def lib():
         "fhwt_band_offset_1d": (i64, [i64, c_int, c_int, ctypes.POINTER(i64)]),
         "fhwt_band_offset_2d": (i64, [i64, i64, c_int, c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "fhwt_pack_ll_2d": (st, [vp, vp, i64, i64, i64, c_int, vp]),
+        "fhwt_plan_pack_ll_2d": (st, [vp, vp, vp, vp]),
+        "fhwt_workspace_bytes": (ctypes.c_size_t, [vp]),
+        "fhwt_analyze": (st, [vp, vp, vp, vp, vp]),
+        "fhwt_synthesize": (st, [vp, vp, vp, vp, vp]),
         "fhwt_roundtrip_2d_host": (st, [vp, vp, vp, i64, i64, i64, c_int, i64]),
         "fhwt_roundtrip_1d_host": (st, [vp, vp, vp, i64, i64, c_int, i64]),
         "fhwt_direct_workspace_bytes": (ctypes.c_size_t, [c_int, i64, i64, i64]),
@@ -363,6 +367,18 @@ class Plan2d(_Plan):
         self.h, self.w, self.batch, self.levels = int(h), int(w), int(batch), int(levels)
         self._tail = (self.h, self.w)
         self._numel = self.h * self.w * self.batch
+
+    def pack_ll(self, coeffs, out=None, stream=None):
+        """fhwt_plan_pack_ll_2d: the coarsest LL of every image, packed [batch][h >> L][w >> L]."""
+        self._check_shape(coeffs)
+        torch = _t()
+        L = self.levels
+        if out is None:
+            out = torch.empty((self.batch, self.h >> L, self.w >> L), dtype=torch.float32, device=coeffs.device)
+        with _guard_device(coeffs):
+            _check(lib().fhwt_plan_pack_ll_2d(self._h, _dev_f32(coeffs, "coeffs"), _dev_f32(out, "ll"),
+                                              _stream(stream, coeffs)))
+        return out
 
 
 def pack_ll_2d(coeffs, levels: int, out=None, stream=None):

@@ -666,6 +666,15 @@ fhwt_status fhwt_plan_synthesize(fhwt_plan p, const float* coeffs, float* dR, vo
   return run(p, coeffs, dR, workspace, s, false);
 }
 
+// SURVEY §8(b) names of the plan calls (same functions)
+size_t fhwt_workspace_bytes(fhwt_plan p) { return fhwt_plan_workspace_bytes(p); }
+fhwt_status fhwt_analyze(fhwt_plan p, const float* d, float* coeffs, void* workspace, fhwt_stream_t s) {
+  return run(p, d, coeffs, workspace, s, true);
+}
+fhwt_status fhwt_synthesize(fhwt_plan p, const float* coeffs, float* dR, void* workspace, fhwt_stream_t s) {
+  return run(p, coeffs, dR, workspace, s, false);
+}
+
 fhwt_status fhwt_analyze_1d(const float* d, float* coeffs, int64_t n, int64_t batch, int levels, fhwt_stream_t s) {
   fhwt_plan p;
   FHWT_TRY(fhwt_plan_1d(&p, n, batch, levels, nullptr));
@@ -723,6 +732,12 @@ fhwt_status fhwt_pack_ll_2d(const float* coeffs, float* ll_packed, int64_t h, in
   if (!coeffs || !ll_packed) return fail(FHWT_ERR_INVALID_ARG, "null buffer pointer");
   FHWT_CUDA(launch_pack_ll(coeffs, ll_packed, h, w, batch, levels, reinterpret_cast<cudaStream_t>(s)), "pack_ll launch");
   return FHWT_OK;
+}
+
+fhwt_status fhwt_plan_pack_ll_2d(fhwt_plan p, const float* coeffs, float* ll_packed, fhwt_stream_t s) {
+  if (!p) return fail(FHWT_ERR_INVALID_ARG, "null plan");
+  if (p->kind != 2) return fail(FHWT_ERR_INVALID_ARG, "fhwt_plan_pack_ll_2d needs a 2-D plan");
+  return fhwt_pack_ll_2d(coeffs, ll_packed, p->h, p->w, p->batch, p->levels, s);
 }
 
 }  // extern "C"

@@ -152,3 +152,13 @@ def test_huge_batches_are_accepted():
     """batch * h beyond the int32 TMA row range is split into sub-batches, not rejected."""
     p = fhwt.Plan2d(1 << 20, 8, 4096, 1)
     assert p.batch == 4096
+
+
+def test_plan_pack_ll_rejects_bad_plans():
+    L = fhwt.lib()
+    assert L.fhwt_plan_pack_ll_2d(None, None, None, None) == 1          # INVALID_ARG: NULL plan
+    p1 = fhwt.Plan1d(64, 2, 3)
+    assert L.fhwt_plan_pack_ll_2d(p1._h, None, None, None) == 1         # INVALID_ARG: 1-D plan
+    p2 = fhwt.Plan2d(64, 64, 1, 3)
+    assert L.fhwt_plan_pack_ll_2d(p2._h, None, None, None) == 1         # INVALID_ARG: NULL buffers
+    assert L.fhwt_workspace_bytes(p2._h) == L.fhwt_plan_workspace_bytes(p2._h) == 0

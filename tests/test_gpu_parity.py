@@ -184,6 +184,23 @@ def test_pack_ll_matches_band():
     c = fhwt.analyze_2d(x, 4)
     ll = fhwt.pack_ll_2d(c, 4)
     assert torch.equal(ll, c[:, :16, :8])
+    plan = fhwt.Plan2d(256, 128, 3, 4)
+    assert torch.equal(plan.pack_ll(c), ll)
+
+
+def test_survey_named_plan_calls_match():
+    """fhwt_analyze / fhwt_synthesize / fhwt_workspace_bytes (SURVEY §8(b) names) are the plan calls."""
+    import ctypes
+    L = fhwt.lib()
+    x = dev(datagen.uniform((2, 64, 2048), seed=8))
+    plan = fhwt.Plan2d(64, 2048, 2, 6)
+    assert L.fhwt_workspace_bytes(plan._h) == plan.workspace_bytes > 0
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device="cuda")
+    c, r = torch.empty_like(x), torch.empty_like(x)
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.fhwt_analyze(plan._h, x.data_ptr(), c.data_ptr(), ws.data_ptr(), ctypes.c_void_p(s)) == 0
+    assert L.fhwt_synthesize(plan._h, c.data_ptr(), r.data_ptr(), ws.data_ptr(), ctypes.c_void_p(s)) == 0
+    assert torch.equal(c, plan.analyze(x)) and torch.equal(r, plan.synthesize(c))
 
 
 def test_host_roundtrip_api():
