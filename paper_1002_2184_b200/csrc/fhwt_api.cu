@@ -343,7 +343,13 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     FHWT_TRY(occupancy(in64 ? 1 : 0, fast, smem, &bps));
     if (const int cap = env_int("FHWT_CTAS_PER_SM", 0)) bps = std::min(bps, cap);   // sweep knob
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
+    // 5 < L <= 8 on the 32-row fast path: the coarse levels run after a grid barrier in the same,
+    // cooperative, launch (haar2d.cu ana_coarse) instead of a second small-grid pass.
+    const bool coop = k == 0 && np == 2 && pl->passes[1].Lp <= 3 && ps.Lp == 5 && fast_ok && !warp_ok &&
+                      env_int("FHWT_COOP", 1) != 0;
+    p.tail = coop ? pl->passes[1].Lp : 0;
     FHWT_CUDA(launch_ana2d(p, map, in64, fast, int(grid), smem, s), "ana2d launch");
+    if (coop) break;
   }
   return FHWT_OK;
 }
@@ -359,7 +365,18 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
   DevInfo di;
   FHWT_TRY(device_info(&di));
   const size_t np = pl->passes.size();
+  // 5 < L <= 8 with 32 x 256 fine tiles: one cooperative launch of syn2d_warp_kernel<5> whose head
+  // phase rebuilds LL5 from the coarse levels (haar2d.cu syn_coarse) before a grid barrier.
+  bool coop = false;
+  if (np == 2 && pl->passes[1].Lp <= 3 && pl->passes[0].Lp == 5 && env_int("FHWT_COOP", 1) != 0 &&
+      env_int("FHWT_SYN_MODE", 3) == 3) {
+    int tr = choose_tr(H, 5), tc = int(std::min<int64_t>(env_int("FHWT_SYN_TC", 256), W));
+    if (tc == 256 && W % 256 && W % 128 == 0) tc = 128;
+    shrink_for_small(B, H, W, 5, di.sms, &tr, &tc);
+    coop = tr == 32 && tc == 256 && W % 256 == 0;
+  }
   for (size_t kk = np; kk-- > 0;) {
+    if (coop && kk == 1) continue;
     const Pass ps = pl->passes[kk];
     Syn2dParams p{};
     p.H = H;
@@ -462,6 +479,11 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     // slower (tools/sweep_ctas.py, profiles/r01_sweep_ctas.jsonl); LP = 5 is indifferent.
     bps = std::min(bps, env_int("FHWT_CTAS_PER_SM", 2));
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
+    if (coop) {
+      if (mode != 3) return fail(FHWT_ERR_CUDA, "internal: cooperative synthesis needs the warp-decoupled kernel");
+      p.head = pl->passes[1].Lp;
+      p.ll_ws_out = reinterpret_cast<float*>(ws + pl->ws_off[0]);
+    }
     FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
   }
   return FHWT_OK;

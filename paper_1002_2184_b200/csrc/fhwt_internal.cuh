@@ -43,6 +43,8 @@ struct Ana2dParams {
   uint32_t stage_bytes, p_off[2], bar_off;
   int final_pass;
   int fused;             // 32 x 256 fast tiles, LP >= 3: levels 2+3 and 4+5 fused (FHWT_ANA_FUSED, default 1)
+  int tail;              // > 0: after the tiles, a grid barrier and levels 6..5+tail of the fp64 LL5
+                         // hand-off in the same (cooperative) launch (ana_coarse); 0: none
   int l2hint;            // 1: TMA loads carry an L2 evict_first policy (sweep knob FHWT_ANA_L2HINT)
   int row_boxes;         // 1: the map's box is one row and TR boxes are issued per tile (rows of
                          // 128-B multiples; TMA smem destinations must be 128-B aligned); 0: one TR-row box
@@ -69,6 +71,9 @@ struct Syn2dParams {
   uint32_t p_off[2];
   uint32_t tx_bytes;       // bytes landed per stage
   int ll_from_ws;          // LL_{g0+Lp} comes from the workspace map (else from coeffs)
+  int head;                // > 0: levels 5+head..6 rebuilt into the fp32 LL5 workspace first, then a grid
+                           // barrier, then the tiles, in one cooperative launch (syn_coarse); 0: none
+  float* ll_ws_out;        // head > 0: the LL5 workspace the head phase writes (same buffer as ll_ws)
   int row_boxes[6];        // per pass-level j: one-row boxes (1) or one (TR >> j)-row box (0); see Ana2dParams
 };
 
@@ -97,7 +102,7 @@ struct Haar1dParams {
 // launchers (return cudaError_t of the launch)
 // fast_lp > 0 selects the compile-time full-tile variant: fast_lp = (tile cols << 4) | levels
 cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool in_f64, int fast_lp, int grid,
-                         size_t smem, cudaStream_t s);
+                         size_t smem, cudaStream_t s);   // cooperative launch when p.tail > 0
 cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int fast_lp, int grid, size_t smem,
                          cudaStream_t s);
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm);
@@ -139,6 +144,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 __device__ __forceinline__ void fence_proxy_async() {

@@ -161,7 +161,7 @@ def test_deterministic_and_launch_count():
     b = fhwt.analyze_2d(x, 7)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
-    assert fhwt.launch_count() - n0 == 4      # two passes per call
+    assert fhwt.launch_count() - n0 == 2      # one cooperative launch per call (levels 6-7 after a grid barrier)
 
 
 def test_misaligned_and_cpu_inputs_fail_loudly():
@@ -383,7 +383,8 @@ def test_long_signal_segments_bitwise_equal(world):
 
 
 @pytest.mark.parametrize("knob,values", [("FHWT_ANA_WARP", ["0", "1", "2"]), ("FHWT_ANA_FUSED", ["1", "0"]),
-                                         ("FHWT_SYN_MODE", ["0", "2", "3"])])
+                                         ("FHWT_SYN_MODE", ["0", "2", "3"]),
+                                         ("FHWT_COOP", ["1", "0"])])
 @pytest.mark.parametrize("levels", [1, 3, 5, 7])
 def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
     """Every selectable 2-D kernel variant (CTA-synchronous, warp-decoupled 32/64-column blocks for

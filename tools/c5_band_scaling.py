@@ -31,6 +31,9 @@ def main():
             fhwt.pack_ll_2d(c, L, out=ll)
             plan.synthesize(c, out=r, workspace=ws)
 
+        n0 = fhwt.launch_count()
+        step()
+        launches = fhwt.launch_count() - n0
         for _ in range(3):
             step()
         torch.cuda.synchronize()
@@ -46,7 +49,8 @@ def main():
         ok = bool(torch.equal(r, x)) or float((r - x).abs().max()) <= 1e-5 * float(x.abs().max())
         res.append({"P": P, "band_rows": h, "ms_per_rank_step": round(t, 4),
                     "gbs_per_rank": round(16 * x.numel() / t / 1e6), "projected_efficiency": round(t1 / (P * t), 4),
-                    "roundtrip_ok": ok, "launches_per_step": 5})
+                    "roundtrip_ok": ok, "launches_per_step": launches,
+                    "coop": os.environ.get("FHWT_COOP", "1")})
         print(json.dumps(res[-1]), flush=True)
 
 
