@@ -255,6 +255,16 @@ int choose_tr(int64_t rows, int Lp) {
   return std::max(tr, 1 << Lp);
 }
 
+// Ring depth by stage size (tools/generic_shapes.py sweeps): analysis keeps >= 64 KB of input
+// staged per CTA (2 .. 8 stages: 8 x 128 tiles 5.1 -> 6.1 TB/s at 8 stages); synthesis peaks near
+// 48 KB (2 .. 4 stages; 8 stages of 8 x 128 tiles fall to 3.8 TB/s from 4.9 at 4).
+int ring_stages(uint32_t stage_bytes) {
+  return int(std::min<uint32_t>(8, std::max<uint32_t>(2, (65536 + stage_bytes - 1) / stage_bytes)));
+}
+int syn_ring_stages(uint32_t stage_bytes) {
+  return int(std::min<uint32_t>(4, std::max<uint32_t>(2, (49152 + stage_bytes - 1) / stage_bytes)));
+}
+
 // Small problems (fewer tiles than SMs, e.g. one 512 x 512 image): shorter and narrower tiles so
 // the work spreads over more SMs; each CTA's serial chain (load, levels, store) is what sets the
 // latency there.  Only between compile-time fast geometries (rows 8/16/32, columns 128/256).
@@ -312,8 +322,11 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     FHWT_TRY(encode_2d(&map, in, in64, p.Win, B * p.Hin, in_pitch, p.TC, p.row_boxes ? 1 : p.TR));
     // shared memory layout: stages | P[0] | P[1] | barriers
     const size_t es = in64 ? 8 : 4;
-    p.stages = in64 ? 2 : env_int("FHWT_ANA_STAGES", 2);
     p.stage_bytes = uint32_t(align_up(size_t(p.TR) * p.TC * es, 1024));
+    // Ring depth: at least 64 KB of staged input per CTA (2 stages of 32 x 256 fp32 tiles; up to 8
+    // stages of smaller tiles, e.g. 8 x 128 for 1080-row frames, where 2 stages kept too few bytes
+    // in flight).
+    p.stages = in64 ? 2 : env_int("FHWT_ANA_STAGES", ring_stages(p.stage_bytes));
     size_t pb[2] = {0, 0};
     for (int j = 1; j < ps.Lp; ++j) {
       const size_t sz = (in64 || ps.g0 + j >= kFirstF64Level) ? 8 : 4;
@@ -454,7 +467,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     }
     p.tx_bytes = uint32_t(tx);
     p.stage_bytes = uint32_t(align_up(off, 1024));
-    p.stages = env_int("FHWT_SYN_STAGES", 2);   // 2 stages -> 3 CTAs/SM (measured best, tools/sweep_2d.py)
+    p.stages = env_int("FHWT_SYN_STAGES", syn_ring_stages(p.stage_bytes));   // 2 for 32 x 256 tiles
     size_t pb[2] = {0, 0};
     for (int j = 2; j <= ps.Lp; ++j) {
       const int jj = j - 1;
@@ -477,7 +490,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     FHWT_TRY(occupancy(2, fast_lp, smem, &bps));
     // At most 2 resident CTAs/SM: the lighter LP < 5 variants fit 3-4, which measured 2.5-6.5 %
     // slower (tools/sweep_ctas.py, profiles/r01_sweep_ctas.jsonl); LP = 5 is indifferent.
-    bps = std::min(bps, env_int("FHWT_CTAS_PER_SM", 2));
+    bps = std::min(bps, env_int("FHWT_CTAS_PER_SM", 2 * kThreads2d / syn2d_threads(fast_lp)));
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
     if (coop) {
       if (mode != 3) return fail(FHWT_ERR_CUDA, "internal: cooperative synthesis needs the warp-decoupled kernel");

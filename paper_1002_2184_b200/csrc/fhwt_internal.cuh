@@ -105,6 +105,7 @@ cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool i
                          size_t smem, cudaStream_t s);   // cooperative launch when p.tail > 0
 cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int fast_lp, int grid, size_t smem,
                          cudaStream_t s);
+int syn2d_threads(int fast_lp);   // CTA size of a synthesis variant (fast code as in launch_syn2d)
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm);
 cudaError_t syn2d_occupancy(int fast_lp, size_t smem, int* blocks_per_sm);
 cudaError_t launch_ana1d(const Haar1dParams& p, bool in_f64, cudaStream_t s);

@@ -31,6 +31,17 @@ namespace fhwt {
 
 namespace {
 
+// Threads per CTA of a compile-time fast variant: one 2 x 2V unit per thread on level 1 of the
+// smallest tiles (8 x 128: 64 threads), so small-tile shapes (e.g. 1080-row frames) run many
+// independent CTAs per SM instead of a few latency-bound 256-thread ones; 256 from 32 x 128 up.
+#ifndef FHWT_FAST_PX_PER_THREAD
+#define FHWT_FAST_PX_PER_THREAD 32   // measured: 16 x 256 tiles (2160-row frames) 4.8 -> 5.6 / 4.7 -> 6.0 TB/s
+#endif
+constexpr int fast_threads(int TRF, int TCF) {
+  return TRF * TCF / FHWT_FAST_PX_PER_THREAD < 64 ? 64
+         : (TRF * TCF / FHWT_FAST_PX_PER_THREAD > kThreads2d ? kThreads2d : TRF * TCF / FHWT_FAST_PX_PER_THREAD);
+}
+
 // Stores V consecutive floats at ptr[0..V) of which the first `nvalid` lie inside the band.
 // ALIGNED: the caller guarantees an 8-B aligned ptr and a full vector (fast tiles).
 template <int V, bool ALIGNED>
@@ -87,7 +98,7 @@ __device__ __forceinline__ void store_ll_smem(TC* dst, const TC (&ll)[V]) {
 // level g to HBM and LL_g to smem (lldst, pitch C/2) or, on the pass's last level, to HBM (coeffs
 // LL region or the fp64 workspace).
 // RC, CC: compile-time R, C (0 = runtime).  FAST: full, 8-B aligned tile (no masks, no checks).
-template <typename TS, typename TC, int V, int RC, int CC, bool FAST>
+template <typename TS, typename TC, int V, int RC, int CC, bool FAST, int NT = kThreads2d>
 __device__ __forceinline__ void ana_level(const Ana2dParams& p, const TS* __restrict__ src, int R_, int C_, int j,
                                           int64_t b, int64_t row0, int64_t col0, TC* __restrict__ lldst,
                                           bool last) {
@@ -103,11 +114,11 @@ __device__ __forceinline__ void ana_level(const Ana2dParams& p, const TS* __rest
   float* const base = p.out + (b * p.H + brow) * W + bcol;  // (orow, oc) = (0, 0) of LL_g in this tile
   const int64_t nvalid_row = FAST ? int64_t(OC) : (p.Win >> j) - bcol;
   const TC half = TC(0.5);
-  const int iters = (nunits + kThreads2d - 1) / kThreads2d;
+  const int iters = (nunits + NT - 1) / NT;
 #pragma unroll
   for (int it = 0; it < iters; ++it) {
-    const int u = int(threadIdx.x) + it * kThreads2d;
-    if ((nunits % kThreads2d) != 0 && u >= nunits) break;
+    const int u = int(threadIdx.x) + it * NT;
+    if ((nunits % NT) != 0 && u >= nunits) break;
     const int orow = u / upr;
     const int oc = (u - orow * upr) * V;
     TS t0[2 * V], t1[2 * V];
@@ -229,7 +240,7 @@ __device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* 
   constexpr bool cmp64 = J >= kFirstF64Level;
   using TS = typename std::conditional<src64, double, float>::type;
   using TC = typename std::conditional<cmp64, double, float>::type;
-  ana_level<TS, TC, 2, R, C, true>(p, static_cast<const TS*>(src), R, C, J, b, row0, col0,
+  ana_level<TS, TC, 2, R, C, true, fast_threads(TRF, TCF)>(p, static_cast<const TS*>(src), R, C, J, b, row0, col0,
                                    reinterpret_cast<TC*>(smem + p.p_off[J & 1]), J == LP);
   if constexpr (J < LP) {
     __syncthreads();
@@ -449,7 +460,9 @@ __device__ __forceinline__ void syn_coarse(const Syn2dParams& p) {
 }
 
 template <typename TIn, int LPFAST, int TRF, int TCF>
-__global__ void __launch_bounds__(kThreads2d, FHWT_MINB_ANA) ana2d_kernel(const __grid_constant__ Ana2dParams p,
+__global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads2d,
+                                  LPFAST > 0 ? FHWT_MINB_ANA * kThreads2d / fast_threads(TRF, TCF) : FHWT_MINB_ANA)
+    ana2d_kernel(const __grid_constant__ Ana2dParams p,
                                                            const __grid_constant__ CUtensorMap in_map) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
@@ -714,7 +727,7 @@ __device__ __forceinline__ void store_out_row(float* ptr, const float (&v)[2 * V
 
 // One synthesis level: coefficient block R x C (tile rows/cols at level j) -> LL_{j-1} (2R x 2C),
 // into smem (to_smem, pitch 2C) or, for pass-level 1, into HBM.
-template <int V, int RC, int CC, bool FAST>
+template <int V, int RC, int CC, bool FAST, int NT = kThreads2d>
 __device__ __forceinline__ void syn_level(const Syn2dParams& p, const float* __restrict__ ll, int llp,
                                           const float* __restrict__ hl, const float* __restrict__ lh,
                                           const float* __restrict__ hh, int bp, int R_, int C_, bool to_smem,
@@ -724,12 +737,12 @@ __device__ __forceinline__ void syn_level(const Syn2dParams& p, const float* __r
   const int upr = C / V;
   const int nunits = R * upr;
   const int OC = 2 * C;  // dst pitch when dst is smem
-  const int iters = (nunits + kThreads2d - 1) / kThreads2d;
+  const int iters = (nunits + NT - 1) / NT;
   float* const obase = p.out + (b * p.Hin + row0) * p.out_pitch + col0;
 #pragma unroll
   for (int it = 0; it < iters; ++it) {
-    const int u = int(threadIdx.x) + it * kThreads2d;
-    if ((nunits % kThreads2d) != 0 && u >= nunits) break;
+    const int u = int(threadIdx.x) + it * NT;
+    if ((nunits % NT) != 0 && u >= nunits) break;
     const int r = u / upr;
     const int c = (u - r * upr) * V;
     float vll[V], vhl[V], vlh[V], vhh[V];
@@ -795,7 +808,7 @@ __device__ __forceinline__ void syn_fast_step(const Syn2dParams& p, unsigned cha
   const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]);
   const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]);
   float* dst = reinterpret_cast<float*>(smem + p.p_off[(J - 1) & 1]);
-  syn_level<2, R, C, true>(p, ll, C, hl, lh, hh, C, R, C, J > 1, b, row0, col0, dst);
+  syn_level<2, R, C, true, fast_threads(TRF, TCF)>(p, ll, C, hl, lh, hh, C, R, C, J > 1, b, row0, col0, dst);
   if constexpr (J > 1) {
     __syncthreads();
     syn_fast_step<J - 1, TRF, TCF>(p, stage, smem, dst, b, row0, col0);
@@ -818,7 +831,7 @@ __device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned
     const int64_t hg = p.H >> g, wg = p.W >> g;
     const float* gb = p.coeffs + (b * p.H + (row0 >> j)) * p.W + (col0 >> j);
 #pragma unroll
-    for (int q = int(threadIdx.x); q < 3 * nb; q += kThreads2d) {
+    for (int q = int(threadIdx.x); q < 3 * nb; q += fast_threads(TRF, TCF)) {
       const int band = q / nb, rem = q - band * nb, r = rem / cpr, c = (rem - r * cpr) * 4;
       // band 0 = HL (right half), 1 = LH (bottom half), 2 = HH (both)
       const float* src = gb + (band >= 1 ? hg * p.W : 0) + (band != 1 ? wg : 0) + int64_t(r) * p.W + c;
@@ -837,7 +850,7 @@ __device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned
       lpitch = p.W;
       lsrc = p.coeffs + (b * p.H + (row0 >> LP)) * p.W + (col0 >> LP);
     }
-    for (int q = int(threadIdx.x); q < rows * cpr; q += kThreads2d) {
+    for (int q = int(threadIdx.x); q < rows * cpr; q += fast_threads(TRF, TCF)) {
       const int r = q / cpr, c = (q - r * cpr) * 4;
       cp_async16(base + p.box_off[0][0] + (r * (TCF >> LP) + c) * 4, lsrc + int64_t(r) * lpitch + c);
     }
@@ -1034,7 +1047,9 @@ __device__ __forceinline__ void cp_async_wait_rt(int n) {  // runtime-N wrapper 
 // MODE 0: all boxes by TMA; 2: everything by cp.async (LDGSTS).  (A register-LDG level-1 variant
 // measured 5.19 TB/s vs 6.10 for cp.async and was removed; tools/sweep_syn.py history in profiles/.)
 template <int LPFAST, int TRF, int TCF, int MODE>
-__global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const __grid_constant__ Syn2dParams p,
+__global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads2d,
+                                  LPFAST > 0 ? FHWT_MINB_SYN * kThreads2d / fast_threads(TRF, TCF) : FHWT_MINB_SYN)
+    syn2d_kernel(const __grid_constant__ Syn2dParams p,
                                                            const __grid_constant__ TmaMaps2d maps) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
@@ -1068,7 +1083,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_kernel(const 
   for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
     const int s = it % p.stages;
     if constexpr (CPASYNC) {
-      cp_async_wait_rt<3>(p.stages - 1);   // this thread's copies of the oldest stage have landed
+      cp_async_wait_rt<7>(p.stages - 1);   // this thread's copies of the oldest stage have landed
       __syncthreads();                     // ... and everyone else's
     } else {
       mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
@@ -1258,7 +1273,14 @@ static const void* syn2d_fn(int fast) {
                    : by_geometry<SynF0>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15);
 }
 
-int ana2d_threads(int fast) { return ((fast >> 24) & 0xff) == 4 ? 128 : kThreads2d; }
+int fast_threads_rt(int fast) {   // threads of a compile-time fast variant (code as in ana2d_fn)
+  return fast == 0 ? kThreads2d : fast_threads((fast >> 16) & 0xff, (fast >> 4) & 0xfff);
+}
+int ana2d_threads(int fast) {
+  const int mode = (fast >> 24) & 0xff;
+  return mode == 4 ? 128 : mode == 1 ? kThreads2d : fast_threads_rt(fast);
+}
+int syn2d_threads(int fast) { return ((fast >> 24) & 0xff) == 3 ? kThreads2d : fast_threads_rt(fast); }
 
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm) {
   const void* fn = ana2d_fn(in_f64, fast_lp);
@@ -1271,7 +1293,7 @@ cudaError_t syn2d_occupancy(int fast_lp, size_t smem, int* blocks_per_sm) {
   const void* fn = syn2d_fn(fast_lp);
   cudaError_t e = raise_smem_cap(fn);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kThreads2d, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, syn2d_threads(fast_lp), smem);
 }
 
 cudaError_t launch_ana2d(const Ana2dParams& p, const CUtensorMap& in_map, bool in_f64, int fast_lp, int grid,
@@ -1289,8 +1311,9 @@ cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int fast_l
                          cudaStream_t s) {
   count_launch();
   void* args[] = {const_cast<Syn2dParams*>(&p), const_cast<TmaMaps2d*>(&maps)};
-  if (p.head > 0) return cudaLaunchCooperativeKernel(syn2d_fn(fast_lp), dim3(grid), dim3(kThreads2d), args, smem, s);
-  return cudaLaunchKernel(syn2d_fn(fast_lp), dim3(grid), dim3(kThreads2d), args, smem, s);
+  const dim3 block(syn2d_threads(fast_lp));
+  if (p.head > 0) return cudaLaunchCooperativeKernel(syn2d_fn(fast_lp), dim3(grid), block, args, smem, s);
+  return cudaLaunchKernel(syn2d_fn(fast_lp), dim3(grid), block, args, smem, s);
 }
 
 cudaError_t launch_ana2d_l1_scalar(const float* d, float* c, int64_t h, int64_t w, int64_t batch, cudaStream_t s) {
