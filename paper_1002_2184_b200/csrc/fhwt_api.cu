@@ -255,6 +255,17 @@ int choose_tr(int64_t rows, int Lp) {
   return std::max(tr, 1 << Lp);
 }
 
+// Tile width of a first pass: 256 or 128 columns (full tiles when w % 128 == 0); narrower images
+// use w itself (generic kernels).
+int choose_tc(int64_t w, int pref) {
+  if (w < 128 || pref < 256) return int(std::min<int64_t>(pref, w));
+  if (w % 256 == 0) return 256;
+  if (w % 128 == 0) return 128;
+  // ragged: 256-column tiles unless they would pad a row by more than 20 % (e.g. 800 -> 1024);
+  // measured: 1600-wide rows 5.4 TB/s with 256-column tiles vs 4.6 with 128
+  return ((w + 255) / 256 * 256 - w) * 5 > w ? 128 : 256;
+}
+
 // Ring depth by stage size (tools/generic_shapes.py sweeps): analysis keeps >= 64 KB of input
 // staged per CTA (2 .. 8 stages: 8 x 128 tiles 5.1 -> 6.1 TB/s at 8 stages); synthesis peaks near
 // 48 KB (2 .. 4 stages; 8 stages of 8 x 128 tiles fall to 3.8 TB/s from 4.9 at 4).
@@ -301,8 +312,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     p.Lp = ps.Lp;
     p.g0 = ps.g0;
     p.TR = choose_tr(p.Hin, ps.Lp);
-    p.TC = int(std::min<int64_t>(in64 ? 128 : env_int("FHWT_ANA_TC", 256), p.Win));
-    if (!in64 && p.TC == 256 && p.Win % 256 && p.Win % 128 == 0) p.TC = 128;   // full tiles -> fast path
+    p.TC = in64 ? int(std::min<int64_t>(128, p.Win)) : choose_tc(p.Win, env_int("FHWT_ANA_TC", 256));
     if (!in64) shrink_for_small(B, p.Hin, p.Win, ps.Lp, di.sms, &p.TR, &p.TC);
     p.tiles_r = p.Hin / p.TR;
     p.tiles_c = (p.Win + p.TC - 1) / p.TC;
@@ -334,11 +344,14 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     }
     // compile-time 32 x 256 variant: first pass, full tiles (then every band offset is 8-B aligned)
     const bool fast_ok = !in64 && ps.g0 == 0 && (p.TR == 32 || p.TR == 16 || p.TR == 8) &&
-                         (p.TC == 256 || p.TC == 128) && p.Win % p.TC == 0;
+                         (p.TC == 256 || p.TC == 128) && (p.Win % p.TC == 0 || env_int("FHWT_ANA_RAGGED_FAST", 1) != 0);
+    // ragged widths: compile-time tile geometry with masked edge tiles (TMA zero-fills past the
+    // edge); band rows are 8-B aligned when every band offset W >> j (j <= Lp) is even
+    p.mask_mode = (W % (int64_t(2) << ps.Lp)) != 0 ? 2 : (p.Win % p.TC != 0 ? 1 : 0);
     // warp-decoupled variant (haar2d.cu ana2d_warp_kernel): 32 x 256 full tiles, one-row boxes
     // FHWT_ANA_WARP: 0 = CTA-synchronous kernel, 1 = 32-column warp blocks, 2 = 64-column warp blocks
     const int wmode = env_int("FHWT_ANA_WARP", 0);
-    const bool warp_ok = fast_ok && p.TR == 32 && p.TC == 256 && p.row_boxes && wmode != 0;
+    const bool warp_ok = fast_ok && p.mask_mode == 0 && p.TR == 32 && p.TC == 256 && p.row_boxes && wmode != 0;
     size_t off = size_t(p.stages) * p.stage_bytes;
     p.p_off[0] = uint32_t(off);
     if (warp_ok) {
@@ -400,8 +413,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     p.Lp = ps.Lp;
     p.g0 = ps.g0;
     p.TR = choose_tr(p.Hin, ps.Lp);
-    p.TC = int(std::min<int64_t>(env_int("FHWT_SYN_TC", 256), p.Win));
-    if (p.TC == 256 && p.Win % 256 && p.Win % 128 == 0) p.TC = 128;   // full tiles -> fast path
+    p.TC = choose_tc(p.Win, env_int("FHWT_SYN_TC", 256));
     if (ps.g0 == 0) shrink_for_small(B, p.Hin, p.Win, ps.Lp, di.sms, &p.TR, &p.TC);
     p.tiles_r = p.Hin / p.TR;
     p.tiles_c = (p.Win + p.TC - 1) / p.TC;
@@ -437,13 +449,16 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
                          p.row_boxes[ps.Lp] ? 1 : p.TR >> ps.Lp));
     }
     // Fast variant: 32 x TC full aligned tiles.
-    bool fast = (p.TR == 32 || p.TR == 16 || p.TR == 8) && (p.TC == 256 || p.TC == 128) && p.Win % p.TC == 0 &&
-                p.out_pitch % 4 == 0 &&
-                (W >> (ps.g0 + 1)) % 2 == 0;
-    for (int j = 1; j <= ps.Lp; ++j) fast = fast && p.hoff[j] == 0 && bw[j] == (p.TC >> j);
+    // compile-time tile geometry (fast variants); full = no ragged edge and every box 16-B aligned
+    const bool geom = (p.TR == 32 || p.TR == 16 || p.TR == 8) && (p.TC == 256 || p.TC == 128) &&
+                      p.out_pitch % 4 == 0;
+    bool full = geom && p.Win % p.TC == 0 && (W >> (ps.g0 + 1)) % 2 == 0;
+    for (int j = 1; j <= ps.Lp; ++j) full = full && p.hoff[j] == 0 && bw[j] == (p.TC >> j);
+    const bool fast = full || (geom && env_int("FHWT_SYN_RAGGED_FAST", 1) != 0);
+    p.mask_mode = full ? 0 : 1;   // ragged or shifted boxes: masked variant, TMA boxes (mode 0)
     // load path of the fast variant: 0 TMA boxes, 2 cp.async (LDGSTS) for all boxes.  Measured on
     // B200 (tools/sweep_syn.py): cp.async 6.10 TB/s, TMA boxes 5.86 (register LDG of level 1: 5.19).
-    int mode = fast ? env_int("FHWT_SYN_MODE", 3) : 0;
+    int mode = full ? env_int("FHWT_SYN_MODE", 3) : 0;
     if (mode != 0 && mode != 3) mode = 2;
     if (mode == 3 && !(p.TR == 32 && p.TC == 256)) mode = 2;   // warp-decoupled variant: 32 x 256 tiles only
     p.l1_ldg = 0;

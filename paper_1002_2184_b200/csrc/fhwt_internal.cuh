@@ -42,6 +42,8 @@ struct Ana2dParams {
   int stages;
   uint32_t stage_bytes, p_off[2], bar_off;
   int final_pass;
+  int mask_mode;         // fast variants: 0 all tiles full + 8-B aligned bands, 1 last column tile ragged,
+                         // 2 masked/checked stores everywhere (a band offset W >> j is odd)
   int fused;             // 32 x 256 fast tiles, LP >= 3: levels 2+3 and 4+5 fused (FHWT_ANA_FUSED, default 1)
   int tail;              // > 0: after the tiles, a grid barrier and levels 6..5+tail of the fp64 LL5
                          // hand-off in the same (cooperative) launch (ana_coarse); 0: none
@@ -71,6 +73,7 @@ struct Syn2dParams {
   uint32_t p_off[2];
   uint32_t tx_bytes;       // bytes landed per stage
   int ll_from_ws;          // LL_{g0+Lp} comes from the workspace map (else from coeffs)
+  int mask_mode;           // fast variants: 0 full tiles, hoff = 0; 1 ragged / shifted boxes (TMA mode only)
   int head;                // > 0: levels 5+head..6 rebuilt into the fp32 LL5 workspace first, then a grid
                            // barrier, then the tiles, in one cooperative launch (syn_coarse); 0: none
   float* ll_ws_out;        // head > 0: the LL5 workspace the head phase writes (same buffer as ll_ws)

@@ -232,7 +232,9 @@ struct Refill {
 
 // Fast tile: first pass (g0 = 0, fp32 input), TRF x TCF full tiles, LP levels known at compile
 // time, so every index is a shift/constant and levels g >= 4 are fp64 by construction.
-template <int J, int LP, int TRF, int TCF>
+// FULL: a full tile with 8-B aligned band rows (no masks); else stores are masked at the image's
+// right edge (TMA zero-fills the columns past it) and checked for alignment (odd band offsets).
+template <int J, int LP, int TRF, int TCF, bool FULL = true>
 __device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* src, unsigned char* smem, int64_t b,
                                               int64_t row0, int64_t col0, const Refill& refill) {
   constexpr int R = TRF >> (J - 1), C = TCF >> (J - 1);
@@ -240,12 +242,12 @@ __device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* 
   constexpr bool cmp64 = J >= kFirstF64Level;
   using TS = typename std::conditional<src64, double, float>::type;
   using TC = typename std::conditional<cmp64, double, float>::type;
-  ana_level<TS, TC, 2, R, C, true, fast_threads(TRF, TCF)>(p, static_cast<const TS*>(src), R, C, J, b, row0, col0,
+  ana_level<TS, TC, 2, R, C, FULL, fast_threads(TRF, TCF)>(p, static_cast<const TS*>(src), R, C, J, b, row0, col0,
                                    reinterpret_cast<TC*>(smem + p.p_off[J & 1]), J == LP);
   if constexpr (J < LP) {
     __syncthreads();
     if constexpr (J == 1) refill();   // level 1 was the last reader of the TMA stage
-    ana_fast_step<J + 1, LP, TRF, TCF>(p, smem + p.p_off[J & 1], smem, b, row0, col0, refill);
+    ana_fast_step<J + 1, LP, TRF, TCF, FULL>(p, smem + p.p_off[J & 1], smem, b, row0, col0, refill);
   }
 }
 
@@ -493,6 +495,16 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
     const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
     const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
                         tile_bytes, row_bytes, pol};
+    // mask_mode 0: every tile full and aligned; 1: the last column tile is ragged; 2: masked throughout
+    const bool full = p.mask_mode == 0 || (p.mask_mode == 1 && ct + 1 < p.tiles_c);
+    if constexpr (LPFAST > 0) {
+      if (!full) {
+        ana_fast_step<1, LPFAST, TRF, TCF, false>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC, refill);
+        __syncthreads();  // LL buffers free again
+        if constexpr (LPFAST == 1) refill();
+        continue;
+      }
+    }
     if constexpr (LPFAST >= 3 && TRF == 32 && TCF == 256) {
       if (p.fused) {   // 2 barriers per tile (see ana_fused_tile)
         ana_fused_tile<LPFAST>(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC,
@@ -800,18 +812,22 @@ __device__ __forceinline__ void syn_tile(const Syn2dParams& p, unsigned char* st
 
 // Fast tile: TRF x TCF full tiles, hoff = 0, LP known at compile time (box pitch = TCF >> j).
 // All levels J..1 from the TMA stage (level 1 writes the output tile).
-template <int J, int TRF, int TCF>
+// FULL: full tile, TMA boxes starting at their band block (hoff = 0), vector loads/stores unchecked.
+// !FULL (ragged width or (W >> g) % 4 != 0): same compile-time geometry, boxes shifted left by
+// hoff[J] (pitch box_pitch[J]), alignment-checked loads, stores masked at the image's right edge.
+template <int J, int TRF, int TCF, bool FULL = true>
 __device__ __forceinline__ void syn_fast_step(const Syn2dParams& p, unsigned char* stage, unsigned char* smem,
-                                              const float* ll, int64_t b, int64_t row0, int64_t col0) {
+                                              const float* ll, int llp, int64_t b, int64_t row0, int64_t col0) {
   constexpr int R = TRF >> J, C = TCF >> J;
-  const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]);
+  const int sh = FULL ? 0 : p.hoff[J], bp = FULL ? C : p.box_pitch[J];
+  const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]) + sh;
   const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]);
-  const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]);
+  const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]) + sh;
   float* dst = reinterpret_cast<float*>(smem + p.p_off[(J - 1) & 1]);
-  syn_level<2, R, C, true, fast_threads(TRF, TCF)>(p, ll, C, hl, lh, hh, C, R, C, J > 1, b, row0, col0, dst);
+  syn_level<2, R, C, FULL, fast_threads(TRF, TCF)>(p, ll, llp, hl, lh, hh, bp, R, C, J > 1, b, row0, col0, dst);
   if constexpr (J > 1) {
     __syncthreads();
-    syn_fast_step<J - 1, TRF, TCF>(p, stage, smem, dst, b, row0, col0);
+    syn_fast_step<J - 1, TRF, TCF, FULL>(p, stage, smem, dst, 2 * C, b, row0, col0);   // LL_{J-1} pitch 2C
   }
 }
 
@@ -1093,8 +1109,11 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
     const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
     unsigned char* stage = smem + s * p.stage_bytes;
     if constexpr (LPFAST > 0) {
-      syn_fast_step<LPFAST, TRF, TCF>(p, stage, smem, reinterpret_cast<const float*>(stage + p.box_off[0][0]), b, row0,
-                                 ct * p.TC);
+      const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]);
+      if (p.mask_mode == 0)
+        syn_fast_step<LPFAST, TRF, TCF>(p, stage, smem, ll, TCF >> LPFAST, b, row0, ct * p.TC);
+      else
+        syn_fast_step<LPFAST, TRF, TCF, false>(p, stage, smem, ll, p.box_pitch[LPFAST], b, row0, ct * p.TC);
     } else {
       syn_tile(p, stage, smem, b, row0, ct * p.TC);
     }
