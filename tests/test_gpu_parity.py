@@ -432,3 +432,23 @@ def test_cuda_graph_capture_of_cooperative_launches():
     torch.cuda.synchronize()
     assert torch.equal(c, ref_c) and torch.equal(r, ref_r)
     assert_close(host(r), host(x), host(x), 2, what="graph round trip")
+
+
+@pytest.mark.parametrize("b,h,w,levels", [(2, 600, 800, 3), (1, 1000, 1000, 3), (2, 1200, 1600, 4), (1, 72, 1000, 3),
+                                          (2, 96, 1160, 3), (3, 64, 200, 2), (1, 2160, 3840, 4), (1, 64, 1184, 5)])
+def test_ragged_widths_fast_geometry(monkeypatch, b, h, w, levels):
+    """Ragged widths on the compile-time-geometry kernels (masked edge tiles, TMA zero fill past the
+    edge, odd band offsets, synthesis boxes shifted by hoff): oracle parity, and bitwise equality
+    with the generic runtime-geometry kernels (same operations, same order)."""
+    x = datagen.uniform((b, h, w), seed=h + w, lo=-1.0, hi=2.0)
+    xd = dev(x)
+    c = fhwt.analyze_2d(xd, levels)
+    r = fhwt.synthesize_2d(c, levels)
+    assert_close(host(c), o.analyze_2d(x, levels), x, 2, what=f"ragged {h}x{w} L={levels}")
+    assert_close(host(r), x, x, 2, what="ragged round trip")
+    monkeypatch.setenv("FHWT_ANA_RAGGED_FAST", "0")
+    monkeypatch.setenv("FHWT_SYN_RAGGED_FAST", "0")
+    cg = fhwt.analyze_2d(xd, levels)
+    rg = fhwt.synthesize_2d(c, levels)
+    torch.cuda.synchronize()
+    assert torch.equal(c, cg) and torch.equal(r, rg)
