@@ -461,6 +461,63 @@ __device__ __forceinline__ void syn_coarse(const Syn2dParams& p) {
   }
 }
 
+// Level-pair fused path v2 for 32 x 256 tiles, LP = 5: levels 1+2 in registers (every thread, two
+// 4 x 4 input blocks), so LL1 never touches shared memory; one CTA barrier per tile (LL2 complete,
+// stage free); levels 3+4 and then 5 by one "tail" warp (warp 7 / 6 on alternate tiles, LL2 and
+// LL4 double-buffered) while the other warps start the next tile.  Same operations on the same
+// operands as the level-by-level kernel: bitwise identical output.
+__device__ __forceinline__ void ana_level5_pair(const Ana2dParams& p, const double* ll4, int64_t b, int64_t row0,
+                                                int64_t col0, int q) {
+  const double2 r0 = *reinterpret_cast<const double2*>(ll4 + 2 * q);
+  const double2 r1 = *reinterpret_cast<const double2*>(ll4 + 16 + 2 * q);
+  const double a = r0.x, bb = r0.y, c = r1.x, d = r1.y;
+  const double s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+  const int64_t W = p.W, wg = W >> 5, hgW = (p.H >> 5) * W;
+  float* pr = p.out + (b * p.H + (row0 >> 5)) * W + (col0 >> 5) + q;
+  stg_stream1(pr + wg, float((d1 + d2) * 0.5));
+  stg_stream1(pr + hgW, float((s1 - s2) * 0.5));
+  stg_stream1(pr + hgW + wg, float((d1 - d2) * 0.5));
+  const double ll = (s1 + s2) * 0.5;
+  if (p.final_pass) {
+    stg_stream1(pr, float(ll));
+  } else {
+    const int64_t wpitch = ((p.Win >> 5) + 3) & ~int64_t(3);
+    p.ws_out[(b * (p.Hin >> 5) + (row0 >> 5)) * wpitch + (col0 >> 5) + q] = ll;
+  }
+}
+
+__device__ __forceinline__ void ana_fused2_tile(const Ana2dParams& p, const float* stage, unsigned char* smem, int64_t b,
+                                                int64_t row0, int64_t col0, int it, const Refill& refill) {
+  float* ll2 = reinterpret_cast<float*>(smem + p.p_off[1]) + (it & 1) * 512;                  // 8 x 64
+  double* ll4 = reinterpret_cast<double*>(smem + p.p_off[1] + 4096) + (it & 1) * 32;          // 2 x 16
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {   // levels 1 + 2: 8 x 64 blocks of 4 x 4 input pixels
+    const int u = tid + 256 * k, rb = u >> 6, cb = u & 63;
+    float x[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(stage + (4 * rb + r) * 256 + 4 * cb);
+      x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+    }
+    ll2[rb * 64 + cb] = ana_pair<float, float, 1, 5>(p, x, b, row0, col0, rb, cb);
+  }
+  __syncthreads();   // LL2 complete; every warp is done with the stage
+  refill();
+  if ((tid >> 5) == 7 - (it & 1)) {   // tail warp: levels 3 + 4 (one 4 x 4 LL2 block per lane), then 5
+    const int lane = tid & 31, br = lane >> 4, bc = lane & 15;
+    float x[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(ll2 + (4 * br + r) * 64 + 4 * bc);
+      x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+    }
+    ll4[br * 16 + bc] = ana_pair<float, double, 3, 5>(p, x, b, row0, col0, br, bc);
+    __syncwarp();
+    if (lane < 8) ana_level5_pair(p, ll4, b, row0, col0, lane);
+  }
+}
+
 template <typename TIn, int LPFAST, int TRF, int TCF>
 __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads2d,
                                   LPFAST > 0 ? FHWT_MINB_ANA * kThreads2d / fast_threads(TRF, TCF) : FHWT_MINB_ANA)
@@ -502,6 +559,13 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
         ana_fast_step<1, LPFAST, TRF, TCF, false>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC, refill);
         __syncthreads();  // LL buffers free again
         if constexpr (LPFAST == 1) refill();
+        continue;
+      }
+    }
+    if constexpr (LPFAST == 5 && TRF == 32 && TCF == 256) {
+      if (p.fused == 2) {   // 1 barrier per tile (see ana_fused2_tile)
+        ana_fused2_tile(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC, it,
+                        refill);
         continue;
       }
     }
