@@ -235,6 +235,10 @@ def measure(name, cfg, args, ws, rank, local, pg):
     if ws > 1:
         dist.barrier(group=pg)
     total_ms = start.elapsed_time(end)
+    sustained = None
+    if getattr(args, "sustained", 0) > 0 and name == args.workload:
+        sustained = measure_sustained(step, stream, local, total_ms / K, args.sustained,
+                                      16.0 * d.numel() * ws)
     ana = [e[0].elapsed_time(e[1]) for e in evs]
     mid = [e[4].elapsed_time(e[2]) for e in evs]      # pack + gather on the side stream
     syn = [e[1].elapsed_time(e[3]) for e in evs]      # synthesis (+ the gather's tail, if any)
@@ -269,10 +273,75 @@ def measure(name, cfg, args, ws, rank, local, pg):
         "samples_per_rank": samples_rank,
         "units": units,
         "parity": parity,
+        "sustained": sustained,
     }
     del d, coeffs, rec, wsb
     torch.cuda.empty_cache()
     return res, (plan, host)
+
+
+# Analysis-kernel variants compared under sustained load (profiles/r01_power_cap.md):
+# the default CTA-synchronous fused kernel is fastest at full clock, the dedicated-tail-warp kernel
+# (FHWT_ANA_FUSED=3, 3 stages) once the board sits at its power cap.
+SUSTAINED_VARIANTS = {"default": {}, "ana_fused3_st3": {"FHWT_ANA_FUSED": "3", "FHWT_ANA_STAGES": "3"}}
+
+
+def measure_sustained(step, stream, local, ms_per_step, seconds, bytes_per_step):
+    """Back-to-back steps for `seconds` of warm load, then `seconds` timed (CUDA events), per
+    analysis variant, with NVML SM clock / board power / clock-event reasons sampled during the
+    timed part: the regime of a long streaming job, where the board power cap lowers SM clocks."""
+    import threading
+
+    import torch
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(local)
+    except Exception:  # noqa: BLE001
+        nv = h = None
+    n = max(10, int(seconds * 1e3 / max(ms_per_step, 1e-3)))
+    out = {}
+    saved = {k: os.environ.get(k) for v in SUSTAINED_VARIANTS.values() for k in v}
+    for name, env in SUSTAINED_VARIANTS.items():
+        for k in saved:
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        for _ in range(n):
+            step()
+        samples, stop = [], threading.Event()
+
+        def poll():
+            while not stop.is_set() and h is not None:
+                try:
+                    samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), nv.nvmlDeviceGetPowerUsage(h) / 1e3,
+                                    nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                except Exception:  # noqa: BLE001
+                    pass
+                time.sleep(0.02)
+
+        th = threading.Thread(target=poll, daemon=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        th.start()
+        e0.record(stream)
+        for _ in range(n):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        stop.set()
+        th.join()
+        ms = e0.elapsed_time(e1) / n
+        reasons = 0
+        for x in samples:
+            reasons |= x[2]
+        out[name] = {"env": env, "value": bytes_per_step / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+                     "steps": n, "sm_mhz_median": statistics.median(x[0] for x in samples) if samples else None,
+                     "power_w_median": statistics.median(x[1] for x in samples) if samples else None,
+                     "clock_event_reasons": hex(reasons), "sw_power_cap": bool(reasons & 0x4)}
+    for k, v in saved.items():
+        os.environ.pop(k, None)
+        if v is not None:
+            os.environ[k] = v
+    return out
 
 
 def sampled_parity(name, cfg, host, coeffs, rec, rank, ws):
@@ -578,6 +647,8 @@ def main():
                     help="gloo only for plumbing checks (FHWT_BENCH_ONE_DEVICE=1 on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--sustained", type=float, default=1.5,
+                    help="seconds of warm + timed back-to-back steps per analysis variant (0 = skip)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules; using 3")
@@ -647,6 +718,7 @@ def main():
             "gsamples_per_s": res["gsamples_per_s"],
             "kernels": {k: res[k] for k in ("analysis_ms", "synthesis_ms", "gather_ms", "analysis_gbs", "synthesis_gbs")},
             "roofline": res["roofline"],
+            "sustained": res["sustained"],
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": res["gpu_launches"],

@@ -364,7 +364,11 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     }
     p.bar_off = uint32_t(off);
     const size_t smem = off + 12 * size_t(p.stages);   // mbarriers + stage-release counters
-    const int fast = fast_ok ? ((warp_ok ? (wmode == 2 ? 4 : 1) : 0) << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
+    // FHWT_ANA_FUSED=3: the fused2 path with a dedicated 9th tail warp (ana2d_fused3_kernel)
+    const bool fused3 = fast_ok && !warp_ok && p.fused == 3 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 &&
+                        p.mask_mode == 0;
+    const int vmode = warp_ok ? (wmode == 2 ? 4 : 1) : fused3 ? 5 : 0;
+    const int fast = fast_ok ? (vmode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
     FHWT_TRY(occupancy(in64 ? 1 : 0, fast, smem, &bps));
     if (const int cap = env_int("FHWT_CTAS_PER_SM", 0)) bps = std::min(bps, cap);   // sweep knob

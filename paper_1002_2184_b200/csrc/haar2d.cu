@@ -486,6 +486,8 @@ __device__ __forceinline__ void ana_level5_pair(const Ana2dParams& p, const doub
   }
 }
 
+// DEDICATED: a 9th warp (threads 256..287) is the tail warp of every tile and skips levels 1 + 2.
+template <bool DEDICATED = false>
 __device__ __forceinline__ void ana_fused2_tile(const Ana2dParams& p, const float* stage, unsigned char* smem, int64_t b,
                                                 int64_t row0, int64_t col0, int it, const Refill& refill) {
   float* ll2 = reinterpret_cast<float*>(smem + p.p_off[1]) + (it & 1) * 512;                  // 8 x 64
@@ -493,6 +495,7 @@ __device__ __forceinline__ void ana_fused2_tile(const Ana2dParams& p, const floa
   const int tid = threadIdx.x;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {   // levels 1 + 2: 8 x 64 blocks of 4 x 4 input pixels
+    if (DEDICATED && tid >= 256) break;
     const int u = tid + 256 * k, rb = u >> 6, cb = u & 63;
     float x[4][4];
 #pragma unroll
@@ -504,7 +507,7 @@ __device__ __forceinline__ void ana_fused2_tile(const Ana2dParams& p, const floa
   }
   __syncthreads();   // LL2 complete; every warp is done with the stage
   refill();
-  if ((tid >> 5) == 7 - (it & 1)) {   // tail warp: levels 3 + 4 (one 4 x 4 LL2 block per lane), then 5
+  if ((tid >> 5) == (DEDICATED ? 8 : 7 - (it & 1))) {   // tail warp: levels 3 + 4 (one 4 x 4 LL2 block per lane), then 5
     const int lane = tid & 31, br = lane >> 4, bc = lane & 15;
     float x[4][4];
 #pragma unroll
@@ -515,6 +518,47 @@ __device__ __forceinline__ void ana_fused2_tile(const Ana2dParams& p, const floa
     ll4[br * 16 + bc] = ana_pair<float, double, 3, 5>(p, x, b, row0, col0, br, bc);
     __syncwarp();
     if (lane < 8) ana_level5_pair(p, ll4, b, row0, col0, lane);
+  }
+}
+
+// fused2 with a dedicated tail warp: 288 threads (8 warps for levels 1 + 2, warp 8 for 3-5), so
+// the tail work is off the critical path of the per-tile barrier.  32 x 256 full tiles, LP = 5.
+__global__ void __launch_bounds__(288, 2) ana2d_fused3_kernel(const __grid_constant__ Ana2dParams p,
+                                                              const __grid_constant__ CUtensorMap in_map) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    prefetch_tmap(&in_map);
+    for (int s = 0; s < p.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  constexpr uint32_t row_bytes = 1024, tile_bytes = 32 * row_bytes;
+  uint64_t pol = 0;
+  if (tid < 32) {
+    pol = policy_evict_first();
+    for (int s = 0; s < p.stages; ++s) {
+      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
+      if (t < p.ntiles) ana_issue_tile(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, tile_bytes, row_bytes, pol);
+    }
+  }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+    const int s = it % p.stages;
+    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
+    const int64_t b = rt / p.tiles_r;
+    const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
+                        tile_bytes, row_bytes, pol};
+    ana_fused2_tile<true>(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b,
+                          (rt - b * p.tiles_r) * 32, ct * 256, it, refill);
+  }
+  if (p.tail > 0) {
+    cooperative_groups::this_grid().sync();
+    if (p.tail == 1) ana_coarse<1>(p);
+    else if (p.tail == 2) ana_coarse<2>(p);
+    else ana_coarse<3>(p);
   }
 }
 
@@ -1345,6 +1389,7 @@ static const void* ana2d_fn(bool in_f64, int fast) {
   if (fast == 0) return (const void*)ana2d_kernel<float, 0, 0, 0>;
   if (((fast >> 24) & 0xff) == 1) return warp_fn<AnaW>(fast & 15);
   if (((fast >> 24) & 0xff) == 4) return warp_fn<AnaW64>(fast & 15);
+  if (((fast >> 24) & 0xff) == 5) return (const void*)ana2d_fused3_kernel;
   return by_geometry<AnaF>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15);
 }
 
@@ -1361,7 +1406,7 @@ int fast_threads_rt(int fast) {   // threads of a compile-time fast variant (cod
 }
 int ana2d_threads(int fast) {
   const int mode = (fast >> 24) & 0xff;
-  return mode == 4 ? 128 : mode == 1 ? kThreads2d : fast_threads_rt(fast);
+  return mode == 5 ? 288 : mode == 4 ? 128 : mode == 1 ? kThreads2d : fast_threads_rt(fast);
 }
 int syn2d_threads(int fast) { return ((fast >> 24) & 0xff) == 3 ? kThreads2d : fast_threads_rt(fast); }
 
