@@ -258,7 +258,8 @@ int choose_tr(int64_t rows, int Lp) {
 // Tile width of a first pass: 256 or 128 columns (full tiles when w % 128 == 0); narrower images
 // use w itself (generic kernels).
 int choose_tc(int64_t w, int pref) {
-  if (w < 128 || pref < 256) return int(std::min<int64_t>(pref, w));
+  if (pref < 256) return int(std::min<int64_t>(pref, w));
+  if (w < 128) return env_int("FHWT_NARROW_FAST", 1) && w >= 16 && w % 16 == 0 ? 128 : int(w);   // one masked tile
   if (w % 256 == 0) return 256;
   if (w % 128 == 0) return 128;
   // ragged: 256-column tiles unless they would pad a row by more than 20 % (e.g. 800 -> 1024);
@@ -286,6 +287,51 @@ void shrink_for_small(int64_t batch, int64_t rows, int64_t cols, int Lp, int sms
   if (tiles() < sms && *TC == 256 && cols % 128 == 0) *TC = 128;
 }
 
+// ------------------------------------------------------------------ 2-D small images
+// Batches of images too narrow for 128-column tiles (w < 128, h * w <= 4096, w % 4 == 0): chunks
+// of whole images by 1-D bulk copies, all levels in shared memory (haar2d_small.cu).
+bool small_ok(const fhwt_plan_s* pl, const void* a, const void* b) {
+  return env_int("FHWT_SMALL_IMAGES", 1) != 0 && pl->w < 128 && pl->h * pl->w <= 4096 && pl->w % 4 == 0 &&
+         aligned16(a) && aligned16(b);
+}
+
+fhwt_status run_small2d(const fhwt_plan_s* pl, const float* in, float* out, cudaStream_t s, bool analysis) {
+  DevInfo di;
+  FHWT_TRY(device_info(&di));
+  Small2dParams p{};
+  p.in = in;
+  p.out = out;
+  p.batch = pl->batch;
+  p.H = int(pl->h);
+  p.W = int(pl->w);
+  p.L = pl->levels;
+  const int img = p.H * p.W;
+  p.G = std::max(1, std::min<int>(int(std::min<int64_t>(pl->batch, 1 << 20)),
+                                  env_int("FHWT_SMALL_CHUNK", 8192) / img));   // ~32 KB chunks
+  p.nchunks = (pl->batch + p.G - 1) / p.G;
+  p.stages = env_int("FHWT_SMALL_STAGES", 2);
+  p.stage_bytes = uint32_t(align_up(size_t(p.G) * img * 4, 1024));
+  size_t off = size_t(p.stages) * p.stage_bytes;
+  p.off_out = uint32_t(off);
+  off = align_up(off + size_t(p.G) * img * 4, 128);
+  for (int i = 0; i < 2; ++i) {
+    p.off_t[i] = uint32_t(off);
+    off = align_up(off + size_t(p.G) * (img / 4) * 4, 128);
+  }
+  for (int i = 0; i < 2; ++i) {
+    p.off_d[i] = uint32_t(off);
+    off = align_up(off + std::max<size_t>(8, size_t(p.G) * (img / 256) * 8), 128);
+  }
+  p.off_bar = uint32_t(off);
+  const size_t smem = off + 8 * size_t(p.stages);
+  int bps = 0;
+  FHWT_CUDA(small2d_occupancy(analysis, smem, &bps), "small2d occupancy");
+  if (bps < 1) return fail(FHWT_ERR_CUDA, "small-image kernel does not fit (%zu B shared memory)", smem);
+  const int64_t grid = std::min<int64_t>(p.nchunks, int64_t(bps) * di.sms);
+  FHWT_CUDA(launch_small2d(p, analysis, int(grid), smem, s), "small2d launch");
+  return FHWT_OK;
+}
+
 // ------------------------------------------------------------------ 2-D execution
 fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char* ws, cudaStream_t s) {
   const int64_t H = pl->h, W = pl->w, B = pl->batch;
@@ -295,6 +341,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     FHWT_CUDA(launch_ana2d_l1_scalar(d, coeffs, H, W, B, s), "ana2d_l1_scalar launch");
     return FHWT_OK;
   }
+  if (small_ok(pl, d, coeffs)) return run_small2d(pl, d, coeffs, s, true);
   DevInfo di;
   FHWT_TRY(device_info(&di));
   const size_t np = pl->passes.size();
@@ -392,6 +439,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     FHWT_CUDA(launch_syn2d_l1_scalar(coeffs, dR, H, W, B, s), "syn2d_l1_scalar launch");
     return FHWT_OK;
   }
+  if (small_ok(pl, coeffs, dR)) return run_small2d(pl, coeffs, dR, s, false);
   DevInfo di;
   FHWT_TRY(device_info(&di));
   const size_t np = pl->passes.size();

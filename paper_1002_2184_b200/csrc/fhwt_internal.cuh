@@ -85,6 +85,17 @@ struct TmaMaps2d {
   CUtensorMap ll;        // LL_{g0+Lp} source box
 };
 
+// ------------------------------------------------------------------ small 2-D images
+// (haar2d_small.cu) chunks of G whole images, each h * w <= 4096 samples, all levels in one pass
+struct Small2dParams {
+  const float* in;       // analysis: d; synthesis: coefficients (Mallat layout per image)
+  float* out;            // analysis: coefficients; synthesis: d_R
+  int64_t batch, nchunks;
+  int H, W, L, G;        // image dims, levels, images per chunk
+  int stages;
+  uint32_t stage_bytes, off_out, off_t[2], off_d[2], off_bar;
+};
+
 // ------------------------------------------------------------------ 1-D pass parameters
 struct Haar1dParams {
   const void* in;        // analysis: pass input (fp32 d or fp64 ws); synthesis: approx source
@@ -134,6 +145,9 @@ cudaError_t direct_synthesis_lines(const float* a, Lines_t la, const float* d, L
 size_t lowpass_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels);
 cudaError_t launch_lowpass_u8(const uint8_t* d, float* ll, int64_t h, int64_t w, int64_t batch, int levels, void* ws,
                               cudaStream_t s);
+
+cudaError_t small2d_occupancy(bool analysis, size_t smem, int* blocks_per_sm);
+cudaError_t launch_small2d(const Small2dParams& p, bool analysis, int grid, size_t smem, cudaStream_t s);
 
 void count_launch();
 

@@ -452,3 +452,24 @@ def test_ragged_widths_fast_geometry(monkeypatch, b, h, w, levels):
     rg = fhwt.synthesize_2d(c, levels)
     torch.cuda.synchronize()
     assert torch.equal(c, cg) and torch.equal(r, rg)
+
+
+@pytest.mark.parametrize("b,h,w,levels", [(7, 32, 32, 5), (300, 16, 64, 4), (5, 64, 64, 6), (9, 8, 8, 3), (3, 4, 4, 2),
+                                          (2, 48, 40, 3), (1000, 32, 32, 1), (33, 64, 32, 5)])
+def test_small_images_whole_image_kernels(monkeypatch, b, h, w, levels):
+    """Batches of small images (w < 128, h*w <= 4096) run the whole-image kernels (bulk copies of
+    image chunks, all levels in shared memory, a short last chunk): oracle parity and bitwise
+    equality with the tile kernels (FHWT_SMALL_IMAGES=0)."""
+    x = datagen.uniform((b, h, w), seed=b + h + w, lo=-1.0, hi=1.0)
+    xd = dev(x)
+    n0 = fhwt.launch_count()
+    c = fhwt.analyze_2d(xd, levels)
+    r = fhwt.synthesize_2d(c, levels)
+    assert fhwt.launch_count() - n0 == 2
+    assert_close(host(c), o.analyze_2d(x, levels), x, 2, what=f"small {h}x{w} L={levels}")
+    assert_close(host(r), x, x, 2, what="small round trip")
+    monkeypatch.setenv("FHWT_SMALL_IMAGES", "0")
+    cg = fhwt.analyze_2d(xd, levels)
+    rg = fhwt.synthesize_2d(c, levels)
+    torch.cuda.synchronize()
+    assert torch.equal(c, cg) and torch.equal(r, rg)
