@@ -13,6 +13,9 @@ LIB = os.path.join(HERE, "libfhwt.so")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
+    # IEEE per-operation rounding (R10): no a*b+c contraction across butterfly levels
+    # ((x0+x1)*s + (x2+x3)*s would otherwise fuse), so every kernel path rounds identically.
+    "-fmad=false",
     "-Xcompiler", "-fPIC,-O2", "-shared",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr", "-diag-suppress", "128",

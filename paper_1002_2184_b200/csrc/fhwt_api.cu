@@ -332,6 +332,53 @@ fhwt_status run_small2d(const fhwt_plan_s* pl, const float* in, float* out, cuda
   return FHWT_OK;
 }
 
+// Batches of 1-D signals shorter than the 1024-sample warp chunk (n < 1024, n % 4 == 0): the same
+// chunk machinery (haar2d_small.cu ana1d/syn1d_small_kernel).
+bool small1d_ok(const fhwt_plan_s* pl, const void* a, const void* b) {
+  const int64_t unit = int64_t(1) << std::min(3, pl->levels);   // values per thread in the first pass
+  return env_int("FHWT_SMALL_SIGNALS", 1) != 0 && pl->n < kChunk1d && pl->n % 4 == 0 && pl->n % unit == 0 &&
+         aligned16(a) && aligned16(b);
+}
+
+fhwt_status run_small1d(const fhwt_plan_s* pl, const float* in, float* out, cudaStream_t s, bool analysis) {
+  DevInfo di;
+  FHWT_TRY(device_info(&di));
+  Small2dParams p{};
+  p.in = in;
+  p.out = out;
+  p.batch = pl->batch;
+  p.H = 1;
+  p.W = int(pl->n);
+  p.L = pl->levels;
+  const int n = p.W;
+  p.G = std::max(1, std::min<int>(int(std::min<int64_t>(pl->batch, 1 << 20)), env_int("FHWT_SMALL1D_CHUNK", 8192) / n));
+  p.nchunks = (pl->batch + p.G - 1) / p.G;
+  p.stages = env_int("FHWT_SMALL_STAGES", 2);
+  p.stage_bytes = uint32_t(align_up(size_t(p.G) * n * 4, 1024));
+  size_t off = size_t(p.stages) * p.stage_bytes;
+  p.off_out = uint32_t(off);
+  off = align_up(off + size_t(p.G) * n * 4, 128);
+  // a_3 (fp32) and a_6 (analysis: fp64 in off_d[0]; synthesis: fp32 in off_t[1]) per signal
+  const size_t tb[2] = {size_t(p.G) * (n / 8) * 4, size_t(p.G) * (n / 64) * 4};
+  const size_t db[2] = {std::max<size_t>(8, size_t(p.G) * (n / 64) * 8), 8};
+  for (int i = 0; i < 2; ++i) {
+    p.off_t[i] = uint32_t(off);
+    off = align_up(off + std::max<size_t>(16, tb[i]), 128);
+  }
+  for (int i = 0; i < 2; ++i) {
+    p.off_d[i] = uint32_t(off);
+    off = align_up(off + db[i], 128);
+  }
+  p.off_bar = uint32_t(off);
+  const size_t smem = off + 8 * size_t(p.stages);
+  int bps = 0;
+  FHWT_CUDA(small2d_occupancy(analysis, smem, &bps, true), "small1d occupancy");
+  if (bps < 1) return fail(FHWT_ERR_CUDA, "short-signal kernel does not fit (%zu B shared memory)", smem);
+  const int64_t grid = std::min<int64_t>(p.nchunks, int64_t(bps) * di.sms);
+  FHWT_CUDA(launch_small2d(p, analysis, int(grid), smem, s, true), "small1d launch");
+  return FHWT_OK;
+}
+
 // ------------------------------------------------------------------ 2-D execution
 fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char* ws, cudaStream_t s) {
   const int64_t H = pl->h, W = pl->w, B = pl->batch;
@@ -578,6 +625,7 @@ fhwt_status run_ana1d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     FHWT_CUDA(launch_ana1d_l1_scalar(d, coeffs, n, B, s), "ana1d_l1_scalar launch");
     return FHWT_OK;
   }
+  if (small1d_ok(pl, d, coeffs)) return run_small1d(pl, d, coeffs, s, true);
   const size_t np = pl->passes.size();
   for (size_t k = 0; k < np; ++k) {
     const Pass ps = pl->passes[k];
@@ -608,6 +656,7 @@ fhwt_status run_syn1d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     FHWT_CUDA(launch_syn1d_l1_scalar(coeffs, dR, n, B, s), "syn1d_l1_scalar launch");
     return FHWT_OK;
   }
+  if (small1d_ok(pl, coeffs, dR)) return run_small1d(pl, coeffs, dR, s, false);
   const size_t np = pl->passes.size();
   for (size_t kk = np; kk-- > 0;) {
     const Pass ps = pl->passes[kk];

@@ -146,8 +146,10 @@ size_t lowpass_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels);
 cudaError_t launch_lowpass_u8(const uint8_t* d, float* ll, int64_t h, int64_t w, int64_t batch, int levels, void* ws,
                               cudaStream_t s);
 
-cudaError_t small2d_occupancy(bool analysis, size_t smem, int* blocks_per_sm);
-cudaError_t launch_small2d(const Small2dParams& p, bool analysis, int grid, size_t smem, cudaStream_t s);
+// one_d: the 1-D short-signal kernels (H = 1, W = n)
+cudaError_t small2d_occupancy(bool analysis, size_t smem, int* blocks_per_sm, bool one_d = false);
+cudaError_t launch_small2d(const Small2dParams& p, bool analysis, int grid, size_t smem, cudaStream_t s,
+                           bool one_d = false);
 
 void count_launch();
 

@@ -207,10 +207,205 @@ __global__ void __launch_bounds__(256, 2) syn2d_small_kernel(const __grid_consta
   if (tid == 0) bulk_wait_all();
 }
 
+// ------------------------------------------------------------------ 1-D: batches of short signals
+// Same chunk machinery for signals shorter than the 1024-sample warp chunk of haar1d.cu (which
+// would leave most of a warp idle): G signals of n samples per chunk (H = 1, W = n in the params).
+// Levels run in passes of up to three: one thread takes 2^K consecutive values of a signal, does
+// K levels in registers, and writes each level's details as one contiguous run, so only the pass
+// boundaries go through the approximation buffers.  Arithmetic exactly as haar1d.cu:
+// (x_e ± x_o) * fl(1/√2) in fp32 for levels 1-3, in fp64 with the fp64 constant from level 4
+// (analysis); synthesis in fp32.  Needs n % 2^min(3, J) == 0 (host check).
+template <typename T>
+__device__ __forceinline__ T sq();
+template <>
+__device__ __forceinline__ float sq<float>() { return kS32; }
+template <>
+__device__ __forceinline__ double sq<double>() { return kS64; }
+
+// Analysis levels g0+1..g0+K of g signals: source a_{g0} (length m per signal, stride ss, type TS),
+// details into the output chunk O (row pitch W), a_{g0+K} into dst (compact) or O (last pass).
+template <int K, typename TS, typename TC>
+__device__ __forceinline__ void small1d_ana_pass(const Small2dParams& p, const TS* src, int ss, float* O, TC* dst,
+                                                 int g, int m, int g0, bool last) {
+  constexpr int U = 1 << K;
+  const int upr = m >> K;
+  const uint32_t total = uint32_t(upr) * uint32_t(g);
+  const TC S = sq<TC>();
+  for (uint32_t u = threadIdx.x; u < total; u += blockDim.x) {
+    const uint32_t gi = u / uint32_t(upr), t = u - gi * uint32_t(upr);
+    TC v[U];
+    const TS* sp = src + gi * ss + t * U;
+#pragma unroll
+    for (int e = 0; e < U; ++e) v[e] = TC(sp[e]);
+    float* row = O + gi * p.W;
+#pragma unroll
+    for (int i = 1; i <= K; ++i) {   // level g0 + i: U >> i outputs
+      float* dp = row + (p.W >> (g0 + i)) + t * (U >> i);
+#pragma unroll
+      for (int e = 0; e < (U >> i); ++e) {
+        const TC a = v[2 * e], b = v[2 * e + 1];
+        dp[e] = float((a - b) * S);
+        v[e] = (a + b) * S;
+      }
+    }
+    if (last)
+      row[t] = float(v[0]);
+    else
+      dst[u] = v[0];
+  }
+}
+
+// Synthesis levels lo+K-1 .. lo of g signals: a_{lo+K-1} (stride ls) and the details of those
+// levels from the coefficient chunk S -> a_{lo-1} (mout per signal) into dst (stride ds).
+template <int K>
+__device__ __forceinline__ void small1d_syn_pass(const Small2dParams& p, const float* asrc, int ls, const float* S,
+                                                 float* dst, int ds, int g, int mout, int lo) {
+  constexpr int U = 1 << K;
+  const int upr = mout >> K;
+  const uint32_t total = uint32_t(upr) * uint32_t(g);
+  for (uint32_t u = threadIdx.x; u < total; u += blockDim.x) {
+    const uint32_t gi = u / uint32_t(upr), t = u - gi * uint32_t(upr);
+    const float* row = S + gi * p.W;
+    float v[U];
+    v[0] = asrc[gi * ls + t];
+#pragma unroll
+    for (int i = K; i >= 1; --i) {   // level lo + i - 1: (U >> i) values -> twice as many
+      const float* dp = row + (p.W >> (lo + i - 1)) + t * (U >> i);
+#pragma unroll
+      for (int e = (U >> i) - 1; e >= 0; --e) {
+        const float a = v[e], d = dp[e];
+        v[2 * e] = (a + d) * kS32;
+        v[2 * e + 1] = (a - d) * kS32;
+      }
+    }
+    float* op = dst + gi * ds + t * U;
+#pragma unroll
+    for (int e = 0; e < U; ++e) op[e] = v[e];
+  }
+}
+
+__global__ void __launch_bounds__(256, 2) ana1d_small_kernel(const __grid_constant__ Small2dParams p) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  float* O = reinterpret_cast<float*>(smem + p.off_out);
+  float* const A3 = reinterpret_cast<float*>(smem + p.off_t[0]);    // a_3 (fp32, n/8 per signal)
+  double* const A6 = reinterpret_cast<double*>(smem + p.off_d[0]);  // a_6 (fp64, n/64 per signal)
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < p.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < p.stages; ++s) {
+      const int64_t c = blockIdx.x + int64_t(s) * gridDim.x;
+      if (c < p.nchunks) issue_chunk(p, p.in, smem + s * p.stage_bytes, &bars[s], c);
+    }
+  int it = 0;
+  const int n = p.W, J = p.L;
+  for (int64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x, ++it) {
+    const int s = it % p.stages;
+    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    if (tid == 0) bulk_wait_read();   // the previous chunk's store has read O
+    __syncthreads();
+    const Chunk k = chunk_of(p, c);
+    const float* S = reinterpret_cast<const float*>(smem + s * p.stage_bytes);
+    // pass 1: levels 1..min(3, J), fp32, from the stage
+    if (J == 1) small1d_ana_pass<1, float, float>(p, S, n, O, A3, k.g, n, 0, true);
+    else if (J == 2) small1d_ana_pass<2, float, float>(p, S, n, O, A3, k.g, n, 0, true);
+    else small1d_ana_pass<3, float, float>(p, S, n, O, A3, k.g, n, 0, J == 3);
+    __syncthreads();
+    if (tid == 0) {   // the stage is free: refill it
+      const int64_t nc = c + int64_t(p.stages) * gridDim.x;
+      if (nc < p.nchunks) issue_chunk(p, p.in, smem + s * p.stage_bytes, &bars[s], nc);
+    }
+    if (J > 3) {   // pass 2: levels 4..min(6, J), fp64, from a_3
+      if (J == 4) small1d_ana_pass<1, float, double>(p, A3, n >> 3, O, A6, k.g, n >> 3, 3, true);
+      else if (J == 5) small1d_ana_pass<2, float, double>(p, A3, n >> 3, O, A6, k.g, n >> 3, 3, true);
+      else small1d_ana_pass<3, float, double>(p, A3, n >> 3, O, A6, k.g, n >> 3, 3, J == 6);
+      __syncthreads();
+    }
+    if (J > 6) {   // pass 3: levels 7..J (J <= 9 for n < 1024), fp64, from a_6
+      double* none = nullptr;
+      if (J == 7) small1d_ana_pass<1, double, double>(p, A6, n >> 6, O, none, k.g, n >> 6, 6, true);
+      else if (J == 8) small1d_ana_pass<2, double, double>(p, A6, n >> 6, O, none, k.g, n >> 6, 6, true);
+      else small1d_ana_pass<3, double, double>(p, A6, n >> 6, O, none, k.g, n >> 6, 6, true);
+      __syncthreads();
+    }
+    fence_proxy_async();   // O's generic-proxy writes -> the bulk store (async proxy)
+    __syncthreads();
+    if (tid == 0) bulk_store(p.out + k.first * int64_t(n), O, uint32_t(k.g) * uint32_t(n) * 4u);
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+__global__ void __launch_bounds__(256, 2) syn1d_small_kernel(const __grid_constant__ Small2dParams p) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  float* O = reinterpret_cast<float*>(smem + p.off_out);
+  float* const A3 = reinterpret_cast<float*>(smem + p.off_t[0]);   // a_3 (n/8 per signal)
+  float* const A6 = reinterpret_cast<float*>(smem + p.off_t[1]);   // a_6 (n/64 per signal)
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < p.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < p.stages; ++s) {
+      const int64_t c = blockIdx.x + int64_t(s) * gridDim.x;
+      if (c < p.nchunks) issue_chunk(p, p.in, smem + s * p.stage_bytes, &bars[s], c);
+    }
+  int it = 0;
+  const int n = p.W, J = p.L;
+  for (int64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x, ++it) {
+    const int s = it % p.stages;
+    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    const Chunk k = chunk_of(p, c);
+    const float* S = reinterpret_cast<const float*>(smem + s * p.stage_bytes);
+    const float* a = S;   // a_J: the first n >> J values of each coefficient row (stride n)
+    int ls = n;
+    if (J > 6) {   // levels J..7 -> a_6
+      if (J == 7) small1d_syn_pass<1>(p, a, ls, S, A6, n >> 6, k.g, n >> 6, 7);
+      else if (J == 8) small1d_syn_pass<2>(p, a, ls, S, A6, n >> 6, k.g, n >> 6, 7);
+      else small1d_syn_pass<3>(p, a, ls, S, A6, n >> 6, k.g, n >> 6, 7);
+      __syncthreads();
+      a = A6;
+      ls = n >> 6;
+    }
+    if (J > 3) {   // levels min(J, 6)..4 -> a_3
+      if (J == 4) small1d_syn_pass<1>(p, a, ls, S, A3, n >> 3, k.g, n >> 3, 4);
+      else if (J == 5) small1d_syn_pass<2>(p, a, ls, S, A3, n >> 3, k.g, n >> 3, 4);
+      else small1d_syn_pass<3>(p, a, ls, S, A3, n >> 3, k.g, n >> 3, 4);
+      __syncthreads();
+      a = A3;
+      ls = n >> 3;
+    }
+    if (tid == 0) bulk_wait_read();   // the previous chunk's store has read O
+    __syncthreads();
+    if (J == 1) small1d_syn_pass<1>(p, a, ls, S, O, n, k.g, n, 1);   // levels min(J, 3)..1 -> d_R
+    else if (J == 2) small1d_syn_pass<2>(p, a, ls, S, O, n, k.g, n, 1);
+    else small1d_syn_pass<3>(p, a, ls, S, O, n, k.g, n, 1);
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      bulk_store(p.out + k.first * int64_t(n), O, uint32_t(k.g) * uint32_t(n) * 4u);
+      const int64_t nc = c + int64_t(p.stages) * gridDim.x;
+      if (nc < p.nchunks) issue_chunk(p, p.in, smem + s * p.stage_bytes, &bars[s], nc);
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
 }  // namespace
 
-cudaError_t small2d_occupancy(bool analysis, size_t smem, int* blocks_per_sm) {
-  const void* fn = analysis ? (const void*)ana2d_small_kernel : (const void*)syn2d_small_kernel;
+static const void* small_fn(bool analysis, bool one_d) {
+  if (one_d) return analysis ? (const void*)ana1d_small_kernel : (const void*)syn1d_small_kernel;
+  return analysis ? (const void*)ana2d_small_kernel : (const void*)syn2d_small_kernel;
+}
+
+cudaError_t small2d_occupancy(bool analysis, size_t smem, int* blocks_per_sm, bool one_d) {
+  const void* fn = small_fn(analysis, one_d);
   int dev = 0, optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -219,11 +414,10 @@ cudaError_t small2d_occupancy(bool analysis, size_t smem, int* blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, 256, smem);
 }
 
-cudaError_t launch_small2d(const Small2dParams& p, bool analysis, int grid, size_t smem, cudaStream_t s) {
+cudaError_t launch_small2d(const Small2dParams& p, bool analysis, int grid, size_t smem, cudaStream_t s, bool one_d) {
   count_launch();
   void* args[] = {const_cast<Small2dParams*>(&p)};
-  return cudaLaunchKernel(analysis ? (const void*)ana2d_small_kernel : (const void*)syn2d_small_kernel, dim3(grid),
-                          dim3(256), args, smem, s);
+  return cudaLaunchKernel(small_fn(analysis, one_d), dim3(grid), dim3(256), args, smem, s);
 }
 
 }  // namespace fhwt

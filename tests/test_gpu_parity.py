@@ -473,3 +473,23 @@ def test_small_images_whole_image_kernels(monkeypatch, b, h, w, levels):
     rg = fhwt.synthesize_2d(c, levels)
     torch.cuda.synchronize()
     assert torch.equal(c, cg) and torch.equal(r, rg)
+
+
+@pytest.mark.parametrize("n,batch,levels", [(256, 1000, 8), (512, 77, 9), (4, 10000, 2), (12, 333, 2), (96, 55, 5),
+                                            (1020, 3, 2), (768, 17, 8), (64, 5000, 6)])
+def test_short_signals_chunk_kernels(monkeypatch, n, batch, levels):
+    """Batches of signals shorter than the 1024-sample warp chunk run the chunk kernels (bulk copies,
+    all levels in shared memory): oracle parity and bitwise equality with the warp kernels."""
+    x = datagen.uniform((batch, n), seed=n + batch, lo=-2.0, hi=1.0)
+    xd = dev(x)
+    n0 = fhwt.launch_count()
+    c = fhwt.analyze_1d(xd, levels)
+    r = fhwt.synthesize_1d(c, levels)
+    assert fhwt.launch_count() - n0 == 2
+    assert_close(host(c), o.decompose_1d(x, levels), x, 1, what=f"short 1-D n={n} J={levels}")
+    assert_close(host(r), x, x, 1, what="short 1-D round trip")
+    monkeypatch.setenv("FHWT_SMALL_SIGNALS", "0")
+    cg = fhwt.analyze_1d(xd, levels)
+    rg = fhwt.synthesize_1d(c, levels)
+    torch.cuda.synchronize()
+    assert torch.equal(c, cg) and torch.equal(r, rg)
