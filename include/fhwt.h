@@ -165,6 +165,16 @@ size_t fhwt_lowpass_workspace_bytes(int64_t h, int64_t w, int64_t batch, int lev
 fhwt_status fhwt_lowpass_2d_u8(const uint8_t *d, float *ll, int64_t h, int64_t w, int64_t batch, int levels,
                                void *workspace, fhwt_stream_t s);
 
+/* The same LL-only path from bfloat16 images (the "bf16 I/O" of SURVEY §8(f) f1): d is
+ * [batch][h][w] bf16 bit patterns (device, 16-byte aligned, w % 8 == 0), ll fp32 as above.  bf16 ->
+ * fp32 is exact and the levels are computed as fhwt_analyze_2d computes them (levels 1-3 fp32,
+ * from level 4 fp64), so ll equals the LL band of fhwt_analyze_2d on the fp32 image bitwise.
+ * workspace: fhwt_lowpass_bf16_workspace_bytes bytes (0 for levels <= 3), or NULL (stream-ordered
+ * allocation on s).  Errors as fhwt_lowpass_2d_u8 (MISALIGNED also for w % 8 != 0). */
+size_t fhwt_lowpass_bf16_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels);
+fhwt_status fhwt_lowpass_2d_bf16(const uint16_t *d, float *ll, int64_t h, int64_t w, int64_t batch, int levels,
+                                 void *workspace, fhwt_stream_t s);
+
 /* ------------------------------------------------------------------ direct-form baseline (§8(f) f3)
  * The paper's ORIGINAL structure, for comparison with the Fast structure on the same hardware:
  * analysis = full-rate filtering with b0/b1 then decimation keeping n = 2k+1 (Fig. 2, Eqs. (1)-(4),

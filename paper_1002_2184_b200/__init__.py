@@ -20,7 +20,7 @@ __all__ = [
     "analyze_1d", "synthesize_1d", "analyze_2d", "synthesize_2d", "Plan1d", "Plan2d",
     "pack_ll_2d", "roundtrip_2d_host", "roundtrip_1d_host", "band_offset_1d", "band_offset_2d",
     "direct_workspace_bytes", "direct_analyze_1d", "direct_synthesize_1d", "direct_analyze_2d",
-    "direct_synthesize_2d", "op_counts", "lowpass_2d_u8",
+    "direct_synthesize_2d", "op_counts", "lowpass_2d_u8", "lowpass_2d_bf16",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -135,6 +135,8 @@ def lib():
         "fhwt_direct_workspace_bytes": (ctypes.c_size_t, [c_int, i64, i64, i64]),
         "fhwt_lowpass_workspace_bytes": (ctypes.c_size_t, [i64, i64, i64, c_int]),
         "fhwt_lowpass_2d_u8": (st, [vp, vp, i64, i64, i64, c_int, vp, vp]),
+        "fhwt_lowpass_bf16_workspace_bytes": (ctypes.c_size_t, [i64, i64, i64, c_int]),
+        "fhwt_lowpass_2d_bf16": (st, [vp, vp, i64, i64, i64, c_int, vp, vp]),
         "fhwt_direct_analyze_1d": (st, [vp, vp, i64, i64, c_int, vp, vp]),
         "fhwt_direct_synthesize_1d": (st, [vp, vp, i64, i64, c_int, vp, vp]),
         "fhwt_direct_analyze_2d": (st, [vp, vp, i64, i64, i64, c_int, vp, vp]),
@@ -519,4 +521,20 @@ def lowpass_2d_u8(d, levels: int, out=None, stream=None):
     with torch.cuda.device(d.device):
         _check(lib().fhwt_lowpass_2d_u8(ctypes.c_void_p(d.data_ptr()), _dev_f32(out, "ll"), h, w, batch, int(levels),
                                         None, _stream(stream, d)))
+    return out
+
+
+def lowpass_2d_bf16(d, levels: int, out=None, stream=None):
+    """fhwt_lowpass_2d_bf16: LL_levels of bfloat16 images [..., h, w] (w % 8 == 0), fp32 output; equal
+    bitwise to analyze_2d(d.float(), levels)'s LL band."""
+    import torch
+    if not isinstance(d, torch.Tensor) or not d.is_cuda or d.dtype != torch.bfloat16 or not d.is_contiguous():
+        raise InvalidArgument("d must be a contiguous bfloat16 CUDA tensor")
+    h, w, batch = _shape_2d(d)
+    shape = tuple(d.shape[:-2]) + (h >> levels, w >> levels)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float32, device=d.device)
+    with torch.cuda.device(d.device):
+        _check(lib().fhwt_lowpass_2d_bf16(ctypes.c_void_p(d.data_ptr()), _dev_f32(out, "ll"), h, w, batch,
+                                          int(levels), None, _stream(stream, d)))
     return out

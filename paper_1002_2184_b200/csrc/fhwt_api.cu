@@ -1175,6 +1175,32 @@ extern "C" size_t fhwt_lowpass_workspace_bytes(int64_t h, int64_t w, int64_t bat
   return lowpass_workspace_bytes(h, w, batch, levels);
 }
 
+extern "C" size_t fhwt_lowpass_bf16_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels) {
+  if (check_2d(h, w, batch, levels) != FHWT_OK) return 0;
+  return lowpass_bf16_workspace_bytes(h, w, batch, levels);
+}
+
+extern "C" fhwt_status fhwt_lowpass_2d_bf16(const uint16_t* d, float* ll, int64_t h, int64_t w, int64_t batch,
+                                            int levels, void* workspace, fhwt_stream_t st) {
+  FHWT_TRY(check_2d(h, w, batch, levels));
+  if (!d || !ll) return fail(FHWT_ERR_INVALID_ARG, "null buffer pointer");
+  if (w % 8 != 0) return fail(FHWT_ERR_MISALIGNED, "bf16 lowpass reads rows in 8-pixel (16-B) vectors: w %% 8 != 0");
+  if ((reinterpret_cast<uintptr_t>(d) & 15) || (reinterpret_cast<uintptr_t>(ll) & 3))
+    return fail(FHWT_ERR_MISALIGNED, "bf16 input must be 16-byte aligned");
+  const char* a = reinterpret_cast<const char*>(d);
+  const char* b = reinterpret_cast<const char*>(ll);
+  const size_t in_bytes = size_t(batch) * h * w * 2, out_bytes = size_t(batch) * (h >> levels) * (w >> levels) * 4;
+  if (a < b + out_bytes && b < a + in_bytes) return fail(FHWT_ERR_INVALID_ARG, "input and output buffers overlap");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  const size_t wsb = lowpass_bf16_workspace_bytes(h, w, batch, levels);
+  void* ws = workspace;
+  if (wsb && !ws) FHWT_TRY(ws_alloc(&ws, wsb, s));
+  cudaError_t e = launch_lowpass_bf16(d, ll, h, w, batch, levels, ws, s);
+  if (wsb && !workspace) cudaFreeAsync(ws, s);
+  if (e != cudaSuccess) return cuda_fail(e, "lowpass bf16 launch");
+  return FHWT_OK;
+}
+
 extern "C" fhwt_status fhwt_lowpass_2d_u8(const uint8_t* d, float* ll, int64_t h, int64_t w, int64_t batch,
                                           int levels, void* workspace, fhwt_stream_t st) {
   FHWT_TRY(check_2d(h, w, batch, levels));

@@ -143,6 +143,9 @@ cudaError_t direct_synthesis_lines(const float* a, Lines_t la, const float* d, L
 
 // LL-only uint8 lowpass path (lowpass.cu, §8(f) f1)
 size_t lowpass_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels);
+size_t lowpass_bf16_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels);
+cudaError_t launch_lowpass_bf16(const uint16_t* d, float* ll, int64_t h, int64_t w, int64_t batch, int levels,
+                                void* ws, cudaStream_t s);
 cudaError_t launch_lowpass_u8(const uint8_t* d, float* ll, int64_t h, int64_t w, int64_t batch, int levels, void* ws,
                               cudaStream_t s);
 

@@ -224,6 +224,66 @@ __global__ void lowpass_stage_b(const double* __restrict__ in, int64_t rows, int
   }
 }
 
+// bf16 input (§8(f) f1, "uint8/bf16 I/O"): one thread per 2^M rows x 8 columns (M = min(L, 3));
+// every row is one 16-B load (8 bf16), all issued before the arithmetic.  bf16 -> fp32 is exact; the
+// levels run exactly as the fused analysis kernel (levels 1-3 fp32, LL_j = ((a+b)+(c+d)) * 0.5),
+// so LL_M is bitwise the fused transform's LL of the same fp32 image.  Writes 8 >> M LL_M values
+// (fp32 output, or the fp64 chain when L > 3: level 4 on in fp64 by lowpass_stage_b).
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+template <int M>
+__global__ void __launch_bounds__(256) lowpass_stage_a_bf16(const uint16_t* __restrict__ d, float* __restrict__ out32,
+                                                            double* __restrict__ out64, int64_t h, int64_t w,
+                                                            int64_t batch) {
+  constexpr int N = 1 << M, OUT = 8 >> M;
+  const int64_t bh = h >> M, bw = w >> 3;   // thread blocks of N rows x 8 columns
+  const int64_t total = batch * bh * bw;
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= total) return;
+  const int64_t b = i / (bh * bw), rem = i - b * bh * bw;
+  const int64_t r = rem / bw, c = rem - r * bw;
+  const uint16_t* src = d + (b * h + r * N) * w + c * 8;
+  uint4 raw[N];
+#pragma unroll
+  for (int y = 0; y < N; ++y)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(raw[y].x), "=r"(raw[y].y), "=r"(raw[y].z), "=r"(raw[y].w)
+                 : "l"(src + int64_t(y) * w));
+  float v[N][8];
+#pragma unroll
+  for (int y = 0; y < N; ++y) {
+    const uint32_t q[4] = {raw[y].x, raw[y].y, raw[y].z, raw[y].w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[y][2 * k] = bf16lo(q[k]);
+      v[y][2 * k + 1] = bf16hi(q[k]);
+    }
+  }
+  int rows = N, cols = 8;
+#pragma unroll
+  for (int lev = 1; lev <= M; ++lev) {   // in place: LL_lev[y][x] into v[y][x]
+#pragma unroll
+    for (int y = 0; y < (N >> lev); ++y)
+#pragma unroll
+      for (int x = 0; x < (8 >> lev); ++x)
+        v[y][x] = ((v[2 * y][2 * x] + v[2 * y][2 * x + 1]) + (v[2 * y + 1][2 * x] + v[2 * y + 1][2 * x + 1])) * 0.5f;
+    rows >>= 1;
+    cols >>= 1;
+  }
+  (void)rows;
+  (void)cols;
+  const int64_t orow_w = w >> M;   // LL_M row length
+  const int64_t o = (b * (h >> M) + r) * orow_w + c * OUT;
+#pragma unroll
+  for (int x = 0; x < OUT; ++x) {
+    if (out64)
+      out64[o + x] = double(v[0][x]);
+    else
+      out32[o + x] = v[0][x];
+  }
+}
+
 int grid_lp(int64_t total) {   // grid-stride kernels: at most ~64 waves of resident CTAs
   int64_t g = (total + 255) / 256;
   if (g > 148 * 64) g = 148 * 64;
@@ -233,6 +293,46 @@ int grid_lp(int64_t total) {   // grid-stride kernels: at most ~64 waves of resi
 int grid_exact(int64_t total) { return int((total + 255) / 256); }
 
 }  // namespace
+
+size_t lowpass_bf16_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels) {
+  if (levels <= 3) return 0;
+  const int64_t n3 = batch * (h >> 3) * (w >> 3);
+  return size_t(n3 + n3 / 4 + 16) * sizeof(double);   // LL_3 chain + one ping-pong partner
+}
+
+cudaError_t launch_lowpass_bf16(const uint16_t* d, float* ll, int64_t h, int64_t w, int64_t batch, int levels,
+                                void* ws, cudaStream_t s) {
+  const int M = levels < 3 ? levels : 3;
+  const int64_t threads = batch * (h >> M) * (w >> 3);
+  double* chain = levels > 3 ? static_cast<double*>(ws) : nullptr;
+  float* out_a = levels > 3 ? nullptr : ll;
+  count_launch();
+  const int g = grid_exact(threads);
+  switch (M) {
+    case 1: lowpass_stage_a_bf16<1><<<g, 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
+    case 2: lowpass_stage_a_bf16<2><<<g, 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
+    default: lowpass_stage_a_bf16<3><<<g, 256, 0, s>>>(d, out_a, chain, h, w, batch); break;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || levels <= 3) return e;
+  const int64_t n3 = batch * (h >> 3) * (w >> 3);
+  double* buf[2] = {chain, chain + n3};
+  int64_t rows = h >> 3, cols = w >> 3;
+  int cur = 0;
+  for (int j = 4; j <= levels; ++j) {   // levels >= 4 in fp64
+    const bool last = j == levels;
+    const int64_t total = batch * (rows / 2) * (cols / 2);
+    count_launch();
+    lowpass_stage_b<<<grid_lp(total), 256, 0, s>>>(buf[cur], rows, cols, batch, last ? nullptr : buf[cur ^ 1],
+                                                    last ? ll : nullptr);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    cur ^= 1;
+    rows /= 2;
+    cols /= 2;
+  }
+  return cudaSuccess;
+}
 
 size_t lowpass_workspace_bytes(int64_t h, int64_t w, int64_t batch, int levels) {
   if (levels <= 4) return 0;

@@ -292,6 +292,31 @@ def test_lowpass_u8_errors():
         fhwt.lowpass_2d_u8(torch.zeros(16, 16, device="cuda"), 2)
 
 
+@pytest.mark.parametrize("b,h,w,levels", [(3, 64, 64, 1), (2, 128, 256, 3), (1, 512, 512, 5), (4, 256, 128, 7),
+                                          (2, 72, 1000, 3), (1, 2048, 2048, 8)])
+def test_lowpass_bf16_equals_fused_transform_ll(b, h, w, levels):
+    """§8(f) f1 with bf16 input: LL_levels equals the fused analysis of the same image in fp32
+    bitwise (bf16 -> fp32 exact, same level arithmetic), and the fp64 oracle's LL within the bar."""
+    x = datagen.uniform((b, h, w), seed=h * w + levels, lo=-3.0, hi=5.0)
+    xb = dev(x).to(torch.bfloat16)
+    ll = fhwt.lowpass_2d_bf16(xb, levels)
+    xf = xb.float().contiguous()
+    full = fhwt.analyze_2d(xf, levels)
+    torch.cuda.synchronize()
+    assert torch.equal(ll, full[:, : h >> levels, : w >> levels])
+    ref = o.analyze_2d(host(xf), levels)[:, : h >> levels, : w >> levels]
+    assert_close(host(ll), ref, host(xf), 2, what=f"bf16 lowpass {h}x{w} L={levels}")
+
+
+def test_lowpass_bf16_errors():
+    with pytest.raises(fhwt.Misaligned):   # w % 8 != 0
+        fhwt.lowpass_2d_bf16(torch.zeros(16, 12, dtype=torch.bfloat16, device="cuda"), 2)
+    with pytest.raises(fhwt.InsufficientLength):
+        fhwt.lowpass_2d_bf16(torch.zeros(24, 24, dtype=torch.bfloat16, device="cuda"), 4)
+    with pytest.raises(fhwt.InvalidArgument):
+        fhwt.lowpass_2d_bf16(torch.zeros(16, 16, device="cuda"), 2)
+
+
 # ------------------------------------------------------------------ degenerate cases
 @pytest.mark.parametrize("shape,levels", [((3, 2048), 11), ((2, 256, 512), 8), ((4, 64, 64), 6)])
 def test_constant_input_gives_exactly_zero_details(shape, levels):
