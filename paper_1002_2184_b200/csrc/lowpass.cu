@@ -10,6 +10,8 @@
 // M = 4: a warp reads 512 contiguous bytes per row), runs M levels in registers (levels 1-3 in fp32,
 // level 4 in fp64 — exact for uint8 either way) and writes one LL_M value.  Stage B (L > 4): one
 // tiny pass per further level on the fp64 LL chain.  Outputs are rounded to fp32 once.
+#include <cstdlib>
+
 #include "fhwt_internal.cuh"
 
 namespace fhwt {
@@ -190,6 +192,52 @@ __global__ void __launch_bounds__(256) lowpass_stage_a_wide(const uint8_t* __res
   }
 }
 
+// L = 5 in one launch (h % 32 == 0, w % 256 == 0): each thread forms the exact S4 of a 16 x 16 block
+// as the wide kernel does (SWAR level 1, integer levels 2-4), and S5 = the sum of the S4 of a 2 x 2
+// group of lanes by warp shuffles (lane bits: x = (b0, b2, b3, b4), y = b1: a warp covers 32 rows x
+// 256 columns and lanes with equal y read one 256-B row segment per load).  LL5 = S5 / 32, exact.
+__global__ void __launch_bounds__(256) lowpass_u8_warp5(const uint8_t* __restrict__ d, float* __restrict__ out,
+                                                        int64_t h, int64_t w, int64_t batch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t wr = h >> 5, wc = w >> 8, total = batch * wr * wc;
+  if (wid >= total) return;
+  const int64_t b = wid / (wr * wc), rem = wid - b * wr * wc;
+  const int64_t tr = rem / wc, tc = rem - tr * wc;
+  const int x = (lane & 1) | ((lane >> 1) & 14);   // bits 0, 2, 3, 4
+  const int y = (lane >> 1) & 1;
+  const uint8_t* src = d + (b * h + tr * 32 + y * 16) * w + tc * 256 + x * 16;
+  uint4 raw[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) raw[r] = load_row<4>(src + int64_t(r) * w);
+  uint32_t s1[8][4];
+#pragma unroll
+  for (int yy = 0; yy < 8; ++yy) {
+    const uint32_t t[4] = {raw[2 * yy].x, raw[2 * yy].y, raw[2 * yy].z, raw[2 * yy].w};
+    const uint32_t u[4] = {raw[2 * yy + 1].x, raw[2 * yy + 1].y, raw[2 * yy + 1].z, raw[2 * yy + 1].w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s1[yy][k] = pair_sums(t[k]) + pair_sums(u[k]);
+  }
+  uint32_t s2[4][4];
+#pragma unroll
+  for (int yy = 0; yy < 4; ++yy)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      s2[yy][k] = ((s1[2 * yy][k] & 0xFFFFu) + (s1[2 * yy][k] >> 16)) +
+                  ((s1[2 * yy + 1][k] & 0xFFFFu) + (s1[2 * yy + 1][k] >> 16));
+  uint32_t s3[2][2];
+#pragma unroll
+  for (int yy = 0; yy < 2; ++yy)
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      s3[yy][k] = (s2[2 * yy][2 * k] + s2[2 * yy][2 * k + 1]) + (s2[2 * yy + 1][2 * k] + s2[2 * yy + 1][2 * k + 1]);
+  const uint32_t s4 = (s3[0][0] + s3[0][1]) + (s3[1][0] + s3[1][1]);
+  const uint32_t s5 = s4 + __shfl_xor_sync(0xffffffffu, s4, 1) + __shfl_xor_sync(0xffffffffu, s4, 2) +
+                      __shfl_xor_sync(0xffffffffu, s4, 3);
+  if ((lane & 3) != 0) return;
+  out[(b * (h >> 5) + tr) * (w >> 5) + tc * 8 + (x >> 1)] = float(double(s5) * 0.03125);
+}
+
 // Levels 5..L in one launch, from the exact S4 = 16 LL_4 sums of the wide stage A: one thread per
 // LL_L value sums its 2^(L-4) x 2^(L-4) block of S4 (S_L = sum of the four S_{L-1}, recursively:
 // integer addition is exact, so the association order does not matter) and scales by 2^-L in fp64.
@@ -284,6 +332,70 @@ __global__ void __launch_bounds__(256) lowpass_stage_a_bf16(const uint16_t* __re
   }
 }
 
+// L >= 4 (h % 32 == 0, w % 64 == 0): levels 1-3 per thread on an 8 x 8 block as above, then
+// level 4 (fp64) over 2 x 2 blocks and level 5 over 2 x 2 of those by warp shuffles, in one launch.
+// Lane bits: x = (b0, b2, b4), y = (b1, b3) -> a warp covers 32 rows x 64 columns; lanes with equal
+// y read 8 consecutive 16-B chunks of a row (128 B).  LF = min(L, 5) levels; L > 5 continues on
+// the fp64 chain (lowpass_stage_b) from LL_5.
+template <int LF>
+__global__ void __launch_bounds__(256) lowpass_bf16_warp(const uint16_t* __restrict__ d, float* __restrict__ out32,
+                                                         double* __restrict__ out64, int64_t h, int64_t w,
+                                                         int64_t batch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t wr = h >> 5, wc = w >> 6, total = batch * wr * wc;   // warp tiles of 32 x 64
+  if (wid >= total) return;
+  const int64_t b = wid / (wr * wc), rem = wid - b * wr * wc;
+  const int64_t tr = rem / wc, tc = rem - tr * wc;
+  const int x = (lane & 1) | ((lane >> 1) & 2) | ((lane >> 2) & 4);   // bits 0, 2, 4
+  const int y = ((lane >> 1) & 1) | ((lane >> 2) & 2);                // bits 1, 3
+  const uint16_t* src = d + (b * h + tr * 32 + y * 8) * w + tc * 64 + x * 8;
+  uint4 raw[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(raw[r].x), "=r"(raw[r].y), "=r"(raw[r].z), "=r"(raw[r].w)
+                 : "l"(src + int64_t(r) * w));
+  float v[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const uint32_t q[4] = {raw[r].x, raw[r].y, raw[r].z, raw[r].w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[r][2 * k] = bf16lo(q[k]);
+      v[r][2 * k + 1] = bf16hi(q[k]);
+    }
+  }
+#pragma unroll
+  for (int lev = 1; lev <= 3; ++lev)
+#pragma unroll
+    for (int yy = 0; yy < (8 >> lev); ++yy)
+#pragma unroll
+      for (int xx = 0; xx < (8 >> lev); ++xx)
+        v[yy][xx] = ((v[2 * yy][2 * xx] + v[2 * yy][2 * xx + 1]) + (v[2 * yy + 1][2 * xx] + v[2 * yy + 1][2 * xx + 1])) *
+                    0.5f;
+  // level 4 (fp64): partners right (lane ^ 1), below (^ 2), diagonal (^ 3)
+  double l = double(v[0][0]);
+  {
+    const double rr = __shfl_xor_sync(0xffffffffu, l, 1), dd = __shfl_xor_sync(0xffffffffu, l, 2),
+                 dr = __shfl_xor_sync(0xffffffffu, l, 3);
+    l = ((l + rr) + (dd + dr)) * 0.5;
+  }
+  if constexpr (LF >= 5) {   // level 5: partners lane ^ 4 (right), ^ 8 (below), ^ 12
+    const double rr = __shfl_xor_sync(0xffffffffu, l, 4), dd = __shfl_xor_sync(0xffffffffu, l, 8),
+                 dr = __shfl_xor_sync(0xffffffffu, l, 12);
+    l = ((l + rr) + (dd + dr)) * 0.5;
+  }
+  const int m = LF == 4 ? 3 : 15;   // lanes holding a result: x0 = y0 = 0 (and x1 = y1 = 0 for LF = 5)
+  if ((lane & m) != 0) return;
+  const int64_t oc = (tc * 64 >> LF) + (x >> (LF - 3)), orr = (tr * 32 >> LF) + (y >> (LF - 3));
+  const int64_t o = (b * (h >> LF) + orr) * (w >> LF) + oc;
+  if (out64)
+    out64[o] = l;
+  else
+    out32[o] = float(l);
+}
+
 int grid_lp(int64_t total) {   // grid-stride kernels: at most ~64 waves of resident CTAs
   int64_t g = (total + 255) / 256;
   if (g > 148 * 64) g = 148 * 64;
@@ -291,6 +403,11 @@ int grid_lp(int64_t total) {   // grid-stride kernels: at most ~64 waves of resi
 }
 
 int grid_exact(int64_t total) { return int((total + 255) / 256); }
+
+bool env_lowpass_warp() {   // A/B knob: FHWT_LOWPASS_WARP=0 keeps the two-launch wide path
+  const char* v = std::getenv("FHWT_LOWPASS_WARP");
+  return !(v && *v == '0');
+}
 
 }  // namespace
 
@@ -302,6 +419,35 @@ size_t lowpass_bf16_workspace_bytes(int64_t h, int64_t w, int64_t batch, int lev
 
 cudaError_t launch_lowpass_bf16(const uint16_t* d, float* ll, int64_t h, int64_t w, int64_t batch, int levels,
                                 void* ws, cudaStream_t s) {
+  if (levels >= 4 && h % 32 == 0 && w % 64 == 0) {   // levels 4-5 by warp shuffles, one launch
+    const int LF = levels < 5 ? levels : 5;
+    double* chain = levels > 5 ? static_cast<double*>(ws) : nullptr;
+    float* out_a = levels > 5 ? nullptr : ll;
+    const int64_t warps = batch * (h >> 5) * (w >> 6);
+    count_launch();
+    if (LF == 4)
+      lowpass_bf16_warp<4><<<grid_exact(warps * 32), 256, 0, s>>>(d, out_a, chain, h, w, batch);
+    else
+      lowpass_bf16_warp<5><<<grid_exact(warps * 32), 256, 0, s>>>(d, out_a, chain, h, w, batch);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || levels <= 5) return e;
+    const int64_t n5 = batch * (h >> 5) * (w >> 5);
+    double* buf[2] = {chain, chain + n5};
+    int64_t rows = h >> 5, cols = w >> 5;
+    int cur = 0;
+    for (int j = 6; j <= levels; ++j) {
+      const bool last = j == levels;
+      count_launch();
+      lowpass_stage_b<<<grid_lp(batch * (rows / 2) * (cols / 2)), 256, 0, s>>>(
+          buf[cur], rows, cols, batch, last ? nullptr : buf[cur ^ 1], last ? ll : nullptr);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      cur ^= 1;
+      rows /= 2;
+      cols /= 2;
+    }
+    return cudaSuccess;
+  }
   const int M = levels < 3 ? levels : 3;
   const int64_t threads = batch * (h >> M) * (w >> 3);
   double* chain = levels > 3 ? static_cast<double*>(ws) : nullptr;
@@ -347,6 +493,12 @@ cudaError_t launch_lowpass_u8(const uint8_t* d, float* ll, int64_t h, int64_t w,
   double* chain = levels > 4 ? static_cast<double*>(ws) : nullptr;
   float* out_a = levels > 4 ? nullptr : ll;
   count_launch();
+  if (levels == 5 && h % 32 == 0 && w % 256 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0 &&
+      env_lowpass_warp()) {
+    count_launch();
+    lowpass_u8_warp5<<<grid_exact(batch * (h >> 5) * (w >> 8) * 32), 256, 0, s>>>(d, ll, h, w, batch);
+    return cudaGetLastError();
+  }
   const int64_t n_wide = batch * (h >> M) * (w >> 4);
   if (w % 16 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0 && (reinterpret_cast<uintptr_t>(ll) & 15) == 0 &&
       n_wide < (int64_t(1) << 31) - 256) {

@@ -282,6 +282,19 @@ def test_lowpass_u8_c3_and_c4_images():
     assert np.abs(got - ref).max() <= 1e-9 * 255 * 32
 
 
+@pytest.mark.parametrize("warp", ["1", "0"])
+def test_lowpass_u8_c4_level5_paths(monkeypatch, warp):
+    """L = 5 on 256-multiple widths: the one-launch warp-shuffle kernel and the two-launch wide path
+    agree bitwise with the fused transform's LL."""
+    monkeypatch.setenv("FHWT_LOWPASS_WARP", warp)
+    u8 = np.stack([datagen.c4_image_u8(i, 512) for i in range(3)])
+    d = dev(u8)
+    ll = fhwt.lowpass_2d_u8(d, 5)
+    full = fhwt.analyze_2d(d.float().contiguous(), 5)[:, :16, :16]
+    torch.cuda.synchronize()
+    assert torch.equal(ll, full)
+
+
 def test_lowpass_u8_errors():
     buf = torch.zeros(1 + 64 * 64, dtype=torch.uint8, device="cuda")
     with pytest.raises(fhwt.Misaligned):
