@@ -442,26 +442,16 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     // ragged widths: compile-time tile geometry with masked edge tiles (TMA zero-fills past the
     // edge); band rows are 8-B aligned when every band offset W >> j (j <= Lp) is even
     p.mask_mode = (W % (int64_t(2) << ps.Lp)) != 0 ? 2 : (p.Win % p.TC != 0 ? 1 : 0);
-    // warp-decoupled variant (haar2d.cu ana2d_warp_kernel): 32 x 256 full tiles, one-row boxes
-    // FHWT_ANA_WARP: 0 = CTA-synchronous kernel, 1 = 32-column warp blocks, 2 = 64-column warp blocks
-    const int wmode = env_int("FHWT_ANA_WARP", 0);
-    const bool warp_ok = fast_ok && p.mask_mode == 0 && p.TR == 32 && p.TC == 256 && p.row_boxes && wmode != 0;
     size_t off = size_t(p.stages) * p.stage_bytes;
     p.p_off[0] = uint32_t(off);
-    if (warp_ok) {
-      off = align_up(off + size_t(wmode == 2 ? 4 : 8) * kWarpScratchBytes, 128);   // see AnaScratch
-      p.p_off[1] = p.p_off[0];
-    } else {
-      off = align_up(off + pb[0], 128);
-      p.p_off[1] = uint32_t(off);
-      off = align_up(off + pb[1], 128);
-    }
+    off = align_up(off + pb[0], 128);
+    p.p_off[1] = uint32_t(off);
+    off = align_up(off + pb[1], 128);
     p.bar_off = uint32_t(off);
     const size_t smem = off + 12 * size_t(p.stages);   // mbarriers + stage-release counters
     // FHWT_ANA_FUSED=3: the fused2 path with a dedicated 9th tail warp (ana2d_fused3_kernel)
-    const bool fused3 = fast_ok && !warp_ok && p.fused == 3 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 &&
-                        p.mask_mode == 0;
-    const int vmode = warp_ok ? (wmode == 2 ? 4 : 1) : fused3 ? 5 : 0;
+    const bool fused3 = fast_ok && p.fused == 3 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 && p.mask_mode == 0;
+    const int vmode = fused3 ? 5 : 0;
     const int fast = fast_ok ? (vmode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
     FHWT_TRY(occupancy(in64 ? 1 : 0, fast, smem, &bps));
@@ -469,7 +459,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
     // 5 < L <= 8 on the 32-row fast path: the coarse levels run after a grid barrier in the same,
     // cooperative, launch (haar2d.cu ana_coarse) instead of a second small-grid pass.
-    const bool coop = k == 0 && np == 2 && pl->passes[1].Lp <= 3 && ps.Lp == 5 && fast_ok && !warp_ok &&
+    const bool coop = k == 0 && np == 2 && pl->passes[1].Lp <= 3 && ps.Lp == 5 && fast_ok &&
                       env_int("FHWT_COOP", 1) != 0;
     p.tail = coop ? pl->passes[1].Lp : 0;
     FHWT_CUDA(launch_ana2d(p, map, in64, fast, int(grid), smem, s), "ana2d launch");

@@ -19,10 +19,9 @@ constexpr int kChunk1d = 1024;
 constexpr int kThreads2d = 256;
 constexpr int kThreads1d = 256;
 
-// Warp-decoupled 2-D variants (haar2d.cu): 32 x 256 tiles, warp w owns the 32 x 32 block at
-// columns [32w, 32w + 32); per-warp LL scratch (LL1 16x16 f32, LL2 8x8 f32, LL3 4x4 f32, LL4 2x2 f64).
-constexpr int kWarpScratchBytes = 2560;   // analysis (AnaScratch<64>)
-constexpr int kSynScratchBytes = 1408;    // synthesis (WarpScratch)
+// Warp-decoupled 2-D synthesis (haar2d.cu syn2d_warp_kernel): 32 x 256 tiles, warp w owns the
+// 32 x 32 block at columns [32w, 32w + 32); per-warp LL scratch (LL1 16x16, LL2 8x8, LL3 4x4, LL4 2x2).
+constexpr int kSynScratchBytes = 1408;
 
 // First global level computed in fp64 (levels 1..3 fp32).  DESIGN.md "Precision".
 constexpr int kFirstF64Level = 4;

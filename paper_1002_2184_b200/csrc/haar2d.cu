@@ -461,11 +461,11 @@ __device__ __forceinline__ void syn_coarse(const Syn2dParams& p) {
   }
 }
 
-// Level-pair fused path v2 for 32 x 256 tiles, LP = 5: levels 1+2 in registers (every thread, two
-// 4 x 4 input blocks), so LL1 never touches shared memory; one CTA barrier per tile (LL2 complete,
-// stage free); levels 3+4 and then 5 by one "tail" warp (warp 7 / 6 on alternate tiles, LL2 and
-// LL4 double-buffered) while the other warps start the next tile.  Same operations on the same
-// operands as the level-by-level kernel: bitwise identical output.
+// Dedicated-tail-warp variant for 32 x 256 tiles, LP = 5 (FHWT_ANA_FUSED=3, ana2d_fused3_kernel):
+// levels 1+2 in registers (every thread of warps 0-7 takes two 4 x 4 input blocks), so LL1 never
+// touches shared memory; one CTA barrier per tile (LL2 complete, stage free); levels 3+4 and then
+// 5 by a 9th warp while warps 0-7 start the next tile (LL2 and LL4 double-buffered).  Same
+// operations on the same operands as the level-by-level kernel: bitwise identical output.
 __device__ __forceinline__ void ana_level5_pair(const Ana2dParams& p, const double* ll4, int64_t b, int64_t row0,
                                                 int64_t col0, int q) {
   const double2 r0 = *reinterpret_cast<const double2*>(ll4 + 2 * q);
@@ -486,16 +486,14 @@ __device__ __forceinline__ void ana_level5_pair(const Ana2dParams& p, const doub
   }
 }
 
-// DEDICATED: a 9th warp (threads 256..287) is the tail warp of every tile and skips levels 1 + 2.
-template <bool DEDICATED = false>
-__device__ __forceinline__ void ana_fused2_tile(const Ana2dParams& p, const float* stage, unsigned char* smem, int64_t b,
+__device__ __forceinline__ void ana_fused3_tile(const Ana2dParams& p, const float* stage, unsigned char* smem, int64_t b,
                                                 int64_t row0, int64_t col0, int it, const Refill& refill) {
   float* ll2 = reinterpret_cast<float*>(smem + p.p_off[1]) + (it & 1) * 512;                  // 8 x 64
   double* ll4 = reinterpret_cast<double*>(smem + p.p_off[1] + 4096) + (it & 1) * 32;          // 2 x 16
   const int tid = threadIdx.x;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {   // levels 1 + 2: 8 x 64 blocks of 4 x 4 input pixels
-    if (DEDICATED && tid >= 256) break;
+    if (tid >= 256) break;   // warp 8 is the tail warp
     const int u = tid + 256 * k, rb = u >> 6, cb = u & 63;
     float x[4][4];
 #pragma unroll
@@ -507,7 +505,7 @@ __device__ __forceinline__ void ana_fused2_tile(const Ana2dParams& p, const floa
   }
   __syncthreads();   // LL2 complete; every warp is done with the stage
   refill();
-  if ((tid >> 5) == (DEDICATED ? 8 : 7 - (it & 1))) {   // tail warp: levels 3 + 4 (one 4 x 4 LL2 block per lane), then 5
+  if ((tid >> 5) == 8) {   // tail warp: levels 3 + 4 (one 4 x 4 LL2 block per lane), then 5
     const int lane = tid & 31, br = lane >> 4, bc = lane & 15;
     float x[4][4];
 #pragma unroll
@@ -551,7 +549,7 @@ __global__ void __launch_bounds__(288, 2) ana2d_fused3_kernel(const __grid_const
     const int64_t b = rt / p.tiles_r;
     const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
                         tile_bytes, row_bytes, pol};
-    ana_fused2_tile<true>(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b,
+    ana_fused3_tile(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b,
                           (rt - b * p.tiles_r) * 32, ct * 256, it, refill);
   }
   if (p.tail > 0) {
@@ -606,13 +604,6 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
         continue;
       }
     }
-    if constexpr (LPFAST == 5 && TRF == 32 && TCF == 256) {
-      if (p.fused == 2) {   // 1 barrier per tile (see ana_fused2_tile)
-        ana_fused2_tile(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC, it,
-                        refill);
-        continue;
-      }
-    }
     if constexpr (LPFAST >= 3 && TRF == 32 && TCF == 256) {
       if (p.fused) {   // 2 barriers per tile (see ana_fused_tile)
         ana_fused_tile<LPFAST>(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC,
@@ -641,13 +632,8 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
   }
 }
 
-// ------------------------------------------------------ warp-decoupled analysis (32 x 256 tiles)
-// Haar's 2-tap support (reading R1) makes every 32 x 32 input block independent for all 5 levels,
-// so warp w of the CTA takes columns [32w, 32w + 32) of each TMA-staged 32 x 256 tile and runs
-// levels 1..LP on its block with only __syncwarp between levels (LL in per-warp scratch).  No
-// CTA-wide barrier remains: the stage is released by the last warp to finish level 1 (a shared
-// counter), which also issues the refill, so one warp's coarse levels overlap the other warps'
-// level 1 instead of idling the CTA at a barrier.
+// ---------------------------------------------------------- shared helpers of the warp kernels
+// Per-warp LL scratch of the warp-decoupled synthesis kernel (syn2d_warp_kernel).
 struct WarpScratch {
   float ll1[16 * 16];
   float ll2[8 * 8];
@@ -675,160 +661,6 @@ __device__ __forceinline__ TileXY tile_xy(int64_t tile, int64_t tiles_c, int64_t
     t.col0 = ct * TC;
   }
   return t;
-}
-
-// Per-warp LL scratch of the analysis variant with BW-column warp blocks (BW = 32 or 64):
-// LL1 16 x BW/2 f32 | LL2 8 x BW/4 f32 | LL3 4 x BW/8 f32 | LL4 2 x BW/16 f64.
-// LL1/LL3 share one buffer and LL2/LL4 the other (a level reads LL_{j-1} and writes LL_j).
-template <int BW>
-struct AnaScratch {
-  static constexpr int off(int j) {   // byte offset of LL_j
-    return (j & 1) ? 0 : 16 * (BW / 2) * 4;
-  }
-  static constexpr int bytes = 16 * (BW / 2) * 4 + 8 * (BW / 4) * 4;
-};
-static_assert(AnaScratch<64>::bytes <= kWarpScratchBytes && AnaScratch<32>::bytes <= kWarpScratchBytes, "host layout");
-
-template <typename T, int N>
-__device__ __forceinline__ void load_row8(const T* src, T (&v)[N]) {
-  if constexpr (sizeof(T) == 4 && N == 8) {
-    const float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-  } else {
-    load_row<T, N, true>(src, v);
-  }
-}
-
-// One level J of a warp's block: (32 >> (J-1)) x (BW >> (J-1)) source -> half that per band.
-template <int J, int LP, int BW>
-__device__ __forceinline__ void warp_ana_level(const Ana2dParams& p, const void* srcv, unsigned char* sc, int64_t b,
-                                               int64_t row0, int64_t colw) {
-  constexpr int NR = 32 >> (J - 1), NC = BW >> (J - 1);
-  constexpr int SP = J == 1 ? 256 : NC;                      // J = 1 reads the TMA stage (pitch TC)
-  constexpr bool src64 = J - 1 >= kFirstF64Level;
-  constexpr bool cmp64 = J >= kFirstF64Level;
-  using TS = typename std::conditional<src64, double, float>::type;
-  using TC = typename std::conditional<cmp64, double, float>::type;
-  constexpr int OC = NC / 2, V = OC >= 2 ? 2 : 1, UPR = OC / V, NU = (NR / 2) * UPR;
-  const TS* src = static_cast<const TS*>(srcv);
-  const int lane = threadIdx.x & 31;
-  const int64_t W = p.W;
-  const int64_t brow = row0 >> J, bcol = colw >> J;
-  float* const base = p.out + (b * p.H + brow) * W + bcol;
-  const int64_t wg = W >> J, hgW = (p.H >> J) * W;
-  TC* lldst = nullptr;
-  if constexpr (J < LP) lldst = reinterpret_cast<TC*>(sc + AnaScratch<BW>::off(J));
-  const TC half = TC(0.5);
-#pragma unroll
-  for (int it = 0; it < (NU + 31) / 32; ++it) {
-    const int u = lane + 32 * it;
-    if (NU % 32 != 0 && u >= NU) break;
-    const int orow = u / UPR, oc = (u - orow * UPR) * V;
-    TS t0[2 * V], t1[2 * V];
-    load_row<TS, 2 * V, true>(src + (2 * orow) * SP + 2 * oc, t0);
-    load_row<TS, 2 * V, true>(src + (2 * orow + 1) * SP + 2 * oc, t1);
-    float hl[V], lh[V], hh[V];
-    TC ll[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const TC a = TC(t0[2 * v]), bb = TC(t0[2 * v + 1]), c = TC(t1[2 * v]), d = TC(t1[2 * v + 1]);
-      const TC s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
-      ll[v] = (s1 + s2) * half;
-      lh[v] = float((s1 - s2) * half);
-      hl[v] = float((d1 + d2) * half);
-      hh[v] = float((d1 - d2) * half);
-    }
-    float* const pr = base + int64_t(orow) * W + oc;
-    store_row<V, true>(pr + wg, hl, V);
-    store_row<V, true>(pr + hgW, lh, V);
-    store_row<V, true>(pr + hgW + wg, hh, V);
-    if constexpr (J < LP) {
-      store_ll_smem<TC, V>(lldst + orow * OC + oc, ll);
-    } else {
-      if (p.final_pass) {
-        float llf[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) llf[v] = float(ll[v]);
-        store_row<V, true>(pr, llf, V);
-      } else {   // fp64 hand-off of LL_LP (pitch = padded Win >> LP, see fhwt_api.cu)
-        const int64_t wpitch = ((p.Win >> LP) + 3) & ~int64_t(3);
-        double* w = p.ws_out + (b * (p.Hin >> LP) + brow + orow) * wpitch + bcol + oc;
-#pragma unroll
-        for (int v = 0; v < V; ++v) w[v] = double(ll[v]);
-      }
-    }
-  }
-}
-
-template <int J, int LP, int BW>
-__device__ __forceinline__ void warp_ana_rest(const Ana2dParams& p, unsigned char* sc, int64_t b, int64_t row0,
-                                              int64_t colw) {
-  if constexpr (J <= LP) {
-    __syncwarp();
-    warp_ana_level<J, LP, BW>(p, sc + AnaScratch<BW>::off(J - 1), sc, b, row0, colw);
-    warp_ana_rest<J + 1, LP, BW>(p, sc, b, row0, colw);
-  }
-}
-
-// lane-0 version of ana_issue_tile (the releasing warp's lane 0 refills the stage)
-__device__ __forceinline__ void ana_issue_tile_lane(const Ana2dParams& p, const CUtensorMap* map, unsigned char* dst,
-                                                    uint64_t* bar, int64_t t, uint32_t bytes, uint32_t row_bytes,
-                                                    uint64_t pol) {
-  const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
-  mbar_arrive_expect_tx(bar, bytes);
-  if (p.l2hint)
-    for (int r = 0; r < 32; ++r) tma_load_2d(dst + r * row_bytes, map, int(ct * 256), int(rt * 32 + r), bar, pol);
-  else
-    for (int r = 0; r < 32; ++r) tma_load_2d_nohint(dst + r * row_bytes, map, int(ct * 256), int(rt * 32 + r), bar);
-}
-
-// BW = columns per warp block (32: 8 warps per 32 x 256 tile; 64: 4 warps, level-1 band rows of
-// 128 B per warp and full 32-B sectors down to level 3).
-template <int LP, int BW>
-__global__ void __launch_bounds__(32 * (256 / BW), BW == 64 ? 4 : FHWT_MINB_ANA)
-    ana2d_warp_kernel(const __grid_constant__ Ana2dParams p, const __grid_constant__ CUtensorMap in_map) {
-  constexpr unsigned NW = 256 / BW;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
-  unsigned* cnt = reinterpret_cast<unsigned*>(smem + p.bar_off + 8 * p.stages);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  unsigned char* sc = smem + p.p_off[0] + warp * kWarpScratchBytes;
-  constexpr uint32_t row_bytes = 256 * 4, tile_bytes = 32 * row_bytes;
-  if (tid == 0) {
-    prefetch_tmap(&in_map);
-    for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&bars[s], 1);
-      cnt[s] = 0;
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const uint64_t pol = policy_evict_first();
-  if (tid == 0)
-    for (int s = 0; s < p.stages; ++s) {
-      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
-      if (t < p.ntiles) ana_issue_tile_lane(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, tile_bytes, row_bytes, pol);
-    }
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
-    const int s = it % p.stages;
-    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
-    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256);
-    const int64_t colw = xy.col0 + BW * warp;
-    warp_ana_level<1, LP, BW>(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes) + BW * warp, sc, xy.b,
-                              xy.row0, colw);
-    __syncwarp();
-    if (lane == 0) {   // stage release: the last warp through level 1 refills it
-      __threadfence_block();
-      if ((atomicAdd(&cnt[s], 1u) % NW) == NW - 1) {
-        const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
-        if (nt < p.ntiles)
-          ana_issue_tile_lane(p, &in_map, smem + s * p.stage_bytes, &bars[s], nt, tile_bytes, row_bytes, pol);
-      }
-    }
-    warp_ana_rest<2, LP, BW>(p, sc, xy.b, xy.row0, colw);
-    __syncwarp();   // scratch is rewritten by the next tile
-  }
 }
 
 // ------------------------------------------------------------------------------------ synthesis
@@ -1372,14 +1204,6 @@ static const void* warp_fn(int lp) {
   }
 }
 template <int LP>
-struct AnaW {
-  static const void* get() { return (const void*)ana2d_warp_kernel<LP, 32>; }
-};
-template <int LP>
-struct AnaW64 {
-  static const void* get() { return (const void*)ana2d_warp_kernel<LP, 64>; }
-};
-template <int LP>
 struct SynW {
   static const void* get() { return (const void*)syn2d_warp_kernel<LP>; }
 };
@@ -1387,8 +1211,6 @@ struct SynW {
 static const void* ana2d_fn(bool in_f64, int fast) {
   if (in_f64) return (const void*)ana2d_kernel<double, 0, 0, 0>;
   if (fast == 0) return (const void*)ana2d_kernel<float, 0, 0, 0>;
-  if (((fast >> 24) & 0xff) == 1) return warp_fn<AnaW>(fast & 15);
-  if (((fast >> 24) & 0xff) == 4) return warp_fn<AnaW64>(fast & 15);
   if (((fast >> 24) & 0xff) == 5) return (const void*)ana2d_fused3_kernel;
   return by_geometry<AnaF>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15);
 }
@@ -1406,7 +1228,7 @@ int fast_threads_rt(int fast) {   // threads of a compile-time fast variant (cod
 }
 int ana2d_threads(int fast) {
   const int mode = (fast >> 24) & 0xff;
-  return mode == 5 ? 288 : mode == 4 ? 128 : mode == 1 ? kThreads2d : fast_threads_rt(fast);
+  return mode == 5 ? 288 : fast_threads_rt(fast);
 }
 int syn2d_threads(int fast) { return ((fast >> 24) & 0xff) == 3 ? kThreads2d : fast_threads_rt(fast); }
 

@@ -420,14 +420,15 @@ def test_long_signal_segments_bitwise_equal(world):
             assert torch.equal(seg[lo:lo + ln], full[go:go + ln]), (r, band)
 
 
-@pytest.mark.parametrize("knob,values", [("FHWT_ANA_WARP", ["0", "1", "2"]), ("FHWT_ANA_FUSED", ["1", "0", "2", "3"]),
+@pytest.mark.parametrize("knob,values", [("FHWT_ANA_FUSED", ["1", "0", "3"]),
                                          ("FHWT_SYN_MODE", ["0", "2", "3"]),
                                          ("FHWT_COOP", ["1", "0"])])
 @pytest.mark.parametrize("levels", [1, 3, 5, 7])
 def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
-    """Every selectable 2-D kernel variant (CTA-synchronous, warp-decoupled 32/64-column blocks for
-    analysis; TMA boxes, cp.async, warp-decoupled for synthesis) performs the same arithmetic in the
-    same order, so outputs agree bitwise; the default is also checked against the oracle.  Shape:
+    """Every selectable 2-D kernel variant (analysis: level by level, fused level pairs, dedicated
+    tail warp; synthesis: TMA boxes, cp.async, warp-decoupled; cooperative coarse levels on/off)
+    performs the same arithmetic in the same order, so outputs agree bitwise; the default is also
+    checked against the oracle.  Shape:
     3 images 128 x 512 (full 32 x 256 tiles, several per image, and the L > 5 second pass)."""
     x = np.stack([datagen.c4_image(i, 512)[:128] for i in range(3)])
     xd = dev(x)
