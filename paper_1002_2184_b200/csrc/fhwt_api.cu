@@ -537,12 +537,31 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       FHWT_TRY(encode_2d(&maps.ll, ws + pl->ws_off[kk], false, wl, B * hl, pitch4(wl), bw[ps.Lp],
                          p.row_boxes[ps.Lp] ? 1 : p.TR >> ps.Lp));
     }
-    // Fast variant: 32 x TC full aligned tiles.
     // compile-time tile geometry (fast variants); full = no ragged edge and every box 16-B aligned
     const bool geom = (p.TR == 32 || p.TR == 16 || p.TR == 8) && (p.TC == 256 || p.TC == 128) &&
                       p.out_pitch % 4 == 0;
-    bool full = geom && p.Win % p.TC == 0 && (W >> (ps.g0 + 1)) % 2 == 0;
-    for (int j = 1; j <= ps.Lp; ++j) full = full && p.hoff[j] == 0 && bw[j] == (p.TC >> j);
+    bool aligned = geom && (W >> (ps.g0 + 1)) % 2 == 0;
+    for (int j = 1; j <= ps.Lp; ++j) aligned = aligned && p.hoff[j] == 0 && bw[j] == (p.TC >> j);
+    // A ragged width with aligned boxes runs as two launches: the full tiles on the fast path
+    // (cp.async / warp-decoupled) and the last column of tiles on the masked TMA variant.
+    const bool ragged = p.Win % p.TC != 0;
+    const bool split = aligned && ragged && !coop && p.Win >= p.TC && env_int("FHWT_SYN_SPLIT", 1) != 0;
+    struct Part {
+      int64_t ct0, tiles_c;
+      bool full;
+    };
+    Part parts[2] = {{0, p.tiles_c, aligned && !ragged}, {0, 0, false}};
+    int nparts = 1;
+    if (split) {
+      parts[0] = {0, p.Win / p.TC, true};
+      parts[1] = {p.Win / p.TC, 1, false};
+      nparts = 2;
+    }
+    for (int part = 0; part < nparts; ++part) {
+    const bool full = parts[part].full;
+    p.ct0 = parts[part].ct0;
+    p.tiles_c = parts[part].tiles_c;
+    p.ntiles = B * p.tiles_r * p.tiles_c;
     const bool fast = full || (geom && env_int("FHWT_SYN_RAGGED_FAST", 1) != 0);
     p.mask_mode = full ? 0 : 1;   // ragged or shifted boxes: masked variant, TMA boxes (mode 0)
     // load path of the fast variant: 0 TMA boxes, 2 cp.async (LDGSTS) for all boxes.  Measured on
@@ -602,6 +621,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       p.ll_ws_out = reinterpret_cast<float*>(ws + pl->ws_off[0]);
     }
     FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
+    }   // parts
   }
   return FHWT_OK;
 }

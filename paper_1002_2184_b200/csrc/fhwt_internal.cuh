@@ -63,6 +63,7 @@ struct Syn2dParams {
   int Lp, g0;
   int TR, TC;
   int64_t tiles_r, tiles_c, ntiles;
+  int64_t ct0;             // first column tile of this launch (a ragged width runs as two launches)
   int stages;
   uint32_t stage_bytes, bar_off;
   uint32_t box_off[6][3];  // per pass-level j (1..Lp): offsets of HL, LH, HH boxes; [0][0] = LL box

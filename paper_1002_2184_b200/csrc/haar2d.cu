@@ -777,7 +777,7 @@ template <int LP, int TRF, int TCF>
 __device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned char* base, int64_t t) {
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
-  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = ct * p.TC;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = (ct + p.ct0) * p.TC;
   int q0 = 0;
 #pragma unroll
   for (int j = 1; j <= LP; ++j) {
@@ -820,7 +820,7 @@ __device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMa
   const int lane = threadIdx.x & 31;
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
-  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = ct * p.TC;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = (ct + p.ct0) * p.TC;
   if (lane == 0) mbar_arrive_expect_tx(bar, p.tx_bytes);
   __syncwarp();
   if (lane != 0) return;
@@ -851,7 +851,7 @@ __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const 
                                                     uint64_t* bar, int64_t t, uint64_t pol) {
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
-  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = ct * p.TC;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = (ct + p.ct0) * p.TC;
   mbar_arrive_expect_tx(bar, p.tx_bytes);
   const int L = p.Lp;
   const int64_t llrow = p.ll_from_ws ? b * (p.Hin >> L) + (row0 >> L) : b * p.H + (row0 >> L);
@@ -974,7 +974,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(c
     const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256);
     const unsigned char* stage = smem + s * p.stage_bytes;
     const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> LP);
-    warp_syn_steps<LP, LP>(p, ll, 256 >> LP, stage, warp, sc, xy.b, xy.row0, xy.col0 + 32 * warp);
+    warp_syn_steps<LP, LP>(p, ll, 256 >> LP, stage, warp, sc, xy.b, xy.row0, xy.col0 + p.ct0 * 256 + 32 * warp);
     __syncwarp();
     if (lane == 0) {   // stage release: the 8th warp through level 1 refills it
       __threadfence_block();
@@ -1049,11 +1049,11 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
     if constexpr (LPFAST > 0) {
       const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]);
       if (p.mask_mode == 0)
-        syn_fast_step<LPFAST, TRF, TCF>(p, stage, smem, ll, TCF >> LPFAST, b, row0, ct * p.TC);
+        syn_fast_step<LPFAST, TRF, TCF>(p, stage, smem, ll, TCF >> LPFAST, b, row0, (ct + p.ct0) * p.TC);
       else
-        syn_fast_step<LPFAST, TRF, TCF, false>(p, stage, smem, ll, p.box_pitch[LPFAST], b, row0, ct * p.TC);
+        syn_fast_step<LPFAST, TRF, TCF, false>(p, stage, smem, ll, p.box_pitch[LPFAST], b, row0, (ct + p.ct0) * p.TC);
     } else {
-      syn_tile(p, stage, smem, b, row0, ct * p.TC);
+      syn_tile(p, stage, smem, b, row0, (ct + p.ct0) * p.TC);
     }
     __syncthreads();
     const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
