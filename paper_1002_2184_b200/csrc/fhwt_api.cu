@@ -267,6 +267,10 @@ int choose_tc(int64_t w, int pref) {
   return ((w + 255) / 256 * 256 - w) * 5 > w ? 128 : 256;
 }
 
+// Analysis 8-row tiles (heights with a single factor 8, e.g. 1000 or 1080 rows) run faster 128
+// columns wide: 1000 x 1024 images 4.7 -> 5.5 TB/s, 1000 x 1000 4.0 -> 4.5 (tools/iso_1000.py,
+// tools/ab_shapes.py); synthesis is slower that way (3.65 -> 2.94) and keeps 256.
+
 // Ring depth by stage size (tools/generic_shapes.py sweeps): analysis keeps >= 64 KB of input
 // staged per CTA (2 .. 8 stages: 8 x 128 tiles 5.1 -> 6.1 TB/s at 8 stages); synthesis peaks near
 // 48 KB (2 .. 4 stages; 8 stages of 8 x 128 tiles fall to 3.8 TB/s from 4.9 at 4).
@@ -408,6 +412,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     p.TR = choose_tr(p.Hin, ps.Lp);
     p.TC = in64 ? int(std::min<int64_t>(128, p.Win)) : choose_tc(p.Win, env_int("FHWT_ANA_TC", 256));
     if (!in64) shrink_for_small(B, p.Hin, p.Win, ps.Lp, di.sms, &p.TR, &p.TC);
+    if (!in64 && p.TR == 8 && p.TC == 256 && env_int("FHWT_TR8_TC128", 1) != 0) p.TC = 128;   // see tr8_tc
     p.tiles_r = p.Hin / p.TR;
     p.tiles_c = (p.Win + p.TC - 1) / p.TC;
     p.ntiles = B * p.tiles_r * p.tiles_c;
@@ -441,7 +446,13 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
                          (p.TC == 256 || p.TC == 128) && (p.Win % p.TC == 0 || env_int("FHWT_ANA_RAGGED_FAST", 1) != 0);
     // ragged widths: compile-time tile geometry with masked edge tiles (TMA zero-fills past the
     // edge); band rows are 8-B aligned when every band offset W >> j (j <= Lp) is even
-    p.mask_mode = (W % (int64_t(2) << ps.Lp)) != 0 ? 2 : (p.Win % p.TC != 0 ? 1 : 0);
+    // ragged width: clamp the last tile to Win - TC (full, overlapping) when Win > TC, else masked
+    p.clamp_last = p.Win % p.TC != 0 && p.Win > p.TC && env_int("FHWT_CLAMP_LAST", 1) != 0;
+    p.mask_mode = (p.Win % p.TC != 0 && !p.clamp_last) ? 1 : 0;
+    p.aligned_levels = 0;   // band offsets W >> j and tile starts col0 >> j even for j <= aligned_levels
+    while (p.aligned_levels < ps.Lp && (W >> (p.aligned_levels + 1)) % 2 == 0 &&
+           (!p.clamp_last || ((p.Win - p.TC) >> (p.aligned_levels + 1)) % 2 == 0))
+      ++p.aligned_levels;
     size_t off = size_t(p.stages) * p.stage_bytes;
     p.p_off[0] = uint32_t(off);
     off = align_up(off + pb[0], 128);
@@ -450,7 +461,8 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     p.bar_off = uint32_t(off);
     const size_t smem = off + 12 * size_t(p.stages);   // mbarriers + stage-release counters
     // FHWT_ANA_FUSED=3: the fused2 path with a dedicated 9th tail warp (ana2d_fused3_kernel)
-    const bool fused3 = fast_ok && p.fused == 3 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 && p.mask_mode == 0;
+    const bool fused3 = fast_ok && p.fused == 3 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 && p.mask_mode == 0 &&
+                        p.aligned_levels >= ps.Lp && !p.clamp_last;
     const int vmode = fused3 ? 5 : 0;
     const int fast = fast_ok ? (vmode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
@@ -545,12 +557,17 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     // A ragged width with aligned boxes runs as two launches: the full tiles on the fast path
     // (cp.async / warp-decoupled) and the last column of tiles on the masked TMA variant.
     const bool ragged = p.Win % p.TC != 0;
-    const bool split = aligned && ragged && !coop && p.Win >= p.TC && env_int("FHWT_SYN_SPLIT", 1) != 0;
+    // clamp_last: the last tile starts at Win - TC, full and on the fast path (needs those tile
+    // starts 16-B aligned at every level too); otherwise the split below
+    p.clamp_last = aligned && ragged && p.Win > p.TC && env_int("FHWT_CLAMP_LAST", 1) != 0;
+    for (int j = 1; j <= ps.Lp && p.clamp_last; ++j) p.clamp_last = ((p.Win - p.TC) >> j) % 4 == 0;
+    const bool split = aligned && ragged && !p.clamp_last && !coop && p.Win >= p.TC &&
+                       env_int("FHWT_SYN_SPLIT", 1) != 0;
     struct Part {
       int64_t ct0, tiles_c;
       bool full;
     };
-    Part parts[2] = {{0, p.tiles_c, aligned && !ragged}, {0, 0, false}};
+    Part parts[2] = {{0, p.tiles_c, aligned && (!ragged || p.clamp_last)}, {0, 0, false}};
     int nparts = 1;
     if (split) {
       parts[0] = {0, p.Win / p.TC, true};

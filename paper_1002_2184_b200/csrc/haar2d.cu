@@ -31,6 +31,15 @@ namespace fhwt {
 
 namespace {
 
+// First column of column-tile ct: ct * TC, except that with clamp_last the last tile of a ragged
+// width starts at Win - TC (a full tile overlapping its neighbour; Win - TC is a multiple of the
+// Haar block, so the overlapped coefficients are recomputed from the same inputs: same values).
+template <typename P>
+__device__ __forceinline__ int64_t tile_col0(const P& p, int64_t ct) {
+  const int64_t c = ct * p.TC;
+  return (p.clamp_last && c + p.TC > p.Win) ? p.Win - p.TC : c;
+}
+
 // Threads per CTA of a compile-time fast variant: one 2 x 2V unit per thread on level 1 of the
 // smallest tiles (8 x 128: 64 threads), so small-tile shapes (e.g. 1080-row frames) run many
 // independent CTAs per SM instead of a few latency-bound 256-thread ones; 256 from 32 x 128 up.
@@ -206,13 +215,13 @@ __device__ __forceinline__ void ana_issue_tile(const Ana2dParams& p, const CUten
     if (lane == 0) {
       if (p.l2hint)
         for (int r = 0; r < p.TR; ++r)
-          tma_load_2d(dst + r * row_bytes, map, int(ct * p.TC), int(rt * p.TR + r), bar, pol);
+          tma_load_2d(dst + r * row_bytes, map, int(tile_col0(p, ct)), int(rt * p.TR + r), bar, pol);
       else
         for (int r = 0; r < p.TR; ++r)
-          tma_load_2d_nohint(dst + r * row_bytes, map, int(ct * p.TC), int(rt * p.TR + r), bar);
+          tma_load_2d_nohint(dst + r * row_bytes, map, int(tile_col0(p, ct)), int(rt * p.TR + r), bar);
     }
   } else if (lane == 0) {
-    tma_load_2d(dst, map, int(ct * p.TC), int(rt * p.TR), bar, pol);
+    tma_load_2d(dst, map, int(tile_col0(p, ct)), int(rt * p.TR), bar, pol);
   }
 }
 
@@ -243,8 +252,13 @@ __device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* 
   constexpr bool cmp64 = J >= kFirstF64Level;
   using TS = typename std::conditional<src64, double, float>::type;
   using TC = typename std::conditional<cmp64, double, float>::type;
-  ana_level<TS, TC, 2, R, C, FULL, fast_threads(TRF, TCF)>(p, static_cast<const TS*>(src), R, C, J, b, row0, col0,
-                                   reinterpret_cast<TC*>(smem + p.p_off[J & 1]), J == LP);
+  // unchecked 8-B band stores need even band offsets: W >> J and col0 >> J (levels 1..aligned_levels)
+  if (FULL && J <= p.aligned_levels)
+    ana_level<TS, TC, 2, R, C, true, fast_threads(TRF, TCF)>(p, static_cast<const TS*>(src), R, C, J, b, row0, col0,
+                                                             reinterpret_cast<TC*>(smem + p.p_off[J & 1]), J == LP);
+  else
+    ana_level<TS, TC, 2, R, C, false, fast_threads(TRF, TCF)>(p, static_cast<const TS*>(src), R, C, J, b, row0, col0,
+                                                              reinterpret_cast<TC*>(smem + p.p_off[J & 1]), J == LP);
   if constexpr (J < LP) {
     __syncthreads();
     if constexpr (J == 1) refill();   // level 1 was the last reader of the TMA stage
@@ -593,11 +607,17 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
     const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
     const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
                         tile_bytes, row_bytes, pol};
-    // mask_mode 0: every tile full and aligned; 1: the last column tile is ragged; 2: masked throughout
-    const bool full = p.mask_mode == 0 || (p.mask_mode == 1 && ct + 1 < p.tiles_c);
+    // mask_mode 1: the last column tile is ragged (masked stores); aligned_levels < LP: the coarse
+    // levels' band offsets are odd (alignment-checked stores there).  With clamp_last the last tile
+    // instead starts at Win - TC (full, overlapping its neighbour: identical values stored twice).
+    const bool full = p.mask_mode == 0 || ct + 1 < p.tiles_c;
+    const int64_t col0 = tile_col0(p, ct);
     if constexpr (LPFAST > 0) {
-      if (!full) {
-        ana_fast_step<1, LPFAST, TRF, TCF, false>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC, refill);
+      if (!full || p.aligned_levels < LPFAST) {
+        if (full)
+          ana_fast_step<1, LPFAST, TRF, TCF, true>(p, smem + s * p.stage_bytes, smem, b, row0, col0, refill);
+        else
+          ana_fast_step<1, LPFAST, TRF, TCF, false>(p, smem + s * p.stage_bytes, smem, b, row0, col0, refill);
         __syncthreads();  // LL buffers free again
         if constexpr (LPFAST == 1) refill();
         continue;
@@ -605,18 +625,18 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
     }
     if constexpr (LPFAST >= 3 && TRF == 32 && TCF == 256) {
       if (p.fused) {   // 2 barriers per tile (see ana_fused_tile)
-        ana_fused_tile<LPFAST>(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC,
+        ana_fused_tile<LPFAST>(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, row0, col0,
                                refill);
       } else {
-        ana_fast_step<1, LPFAST, TRF, TCF>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC, refill);
+        ana_fast_step<1, LPFAST, TRF, TCF>(p, smem + s * p.stage_bytes, smem, b, row0, col0, refill);
         __syncthreads();  // LL buffers free again
       }
     } else if constexpr (LPFAST > 0) {
-      ana_fast_step<1, LPFAST, TRF, TCF>(p, smem + s * p.stage_bytes, smem, b, row0, ct * p.TC, refill);
+      ana_fast_step<1, LPFAST, TRF, TCF>(p, smem + s * p.stage_bytes, smem, b, row0, col0, refill);
       __syncthreads();  // LL buffers free again
       if constexpr (LPFAST == 1) refill();
     } else {
-      ana_tile<TIn>(p, reinterpret_cast<const TIn*>(smem + s * p.stage_bytes), smem, b, row0, ct * p.TC);
+      ana_tile<TIn>(p, reinterpret_cast<const TIn*>(smem + s * p.stage_bytes), smem, b, row0, col0);
       __syncthreads();  // stage s and the LL buffers are free again
       refill();
     }
@@ -777,7 +797,7 @@ template <int LP, int TRF, int TCF>
 __device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned char* base, int64_t t) {
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
-  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = (ct + p.ct0) * p.TC;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = tile_col0(p, ct + p.ct0);
   int q0 = 0;
 #pragma unroll
   for (int j = 1; j <= LP; ++j) {
@@ -820,7 +840,7 @@ __device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMa
   const int lane = threadIdx.x & 31;
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
-  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = (ct + p.ct0) * p.TC;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = tile_col0(p, ct + p.ct0);
   if (lane == 0) mbar_arrive_expect_tx(bar, p.tx_bytes);
   __syncwarp();
   if (lane != 0) return;
@@ -851,7 +871,7 @@ __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const 
                                                     uint64_t* bar, int64_t t, uint64_t pol) {
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
-  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = (ct + p.ct0) * p.TC;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = tile_col0(p, ct + p.ct0);
   mbar_arrive_expect_tx(bar, p.tx_bytes);
   const int L = p.Lp;
   const int64_t llrow = p.ll_from_ws ? b * (p.Hin >> L) + (row0 >> L) : b * p.H + (row0 >> L);
@@ -974,7 +994,8 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(c
     const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256);
     const unsigned char* stage = smem + s * p.stage_bytes;
     const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> LP);
-    warp_syn_steps<LP, LP>(p, ll, 256 >> LP, stage, warp, sc, xy.b, xy.row0, xy.col0 + p.ct0 * 256 + 32 * warp);
+    warp_syn_steps<LP, LP>(p, ll, 256 >> LP, stage, warp, sc, xy.b, xy.row0,
+                           tile_col0(p, xy.col0 / 256 + p.ct0) + 32 * warp);
     __syncwarp();
     if (lane == 0) {   // stage release: the 8th warp through level 1 refills it
       __threadfence_block();
@@ -1049,11 +1070,12 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
     if constexpr (LPFAST > 0) {
       const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]);
       if (p.mask_mode == 0)
-        syn_fast_step<LPFAST, TRF, TCF>(p, stage, smem, ll, TCF >> LPFAST, b, row0, (ct + p.ct0) * p.TC);
+        syn_fast_step<LPFAST, TRF, TCF>(p, stage, smem, ll, TCF >> LPFAST, b, row0, tile_col0(p, ct + p.ct0));
       else
-        syn_fast_step<LPFAST, TRF, TCF, false>(p, stage, smem, ll, p.box_pitch[LPFAST], b, row0, (ct + p.ct0) * p.TC);
+        syn_fast_step<LPFAST, TRF, TCF, false>(p, stage, smem, ll, p.box_pitch[LPFAST], b, row0,
+                                               tile_col0(p, ct + p.ct0));
     } else {
-      syn_tile(p, stage, smem, b, row0, (ct + p.ct0) * p.TC);
+      syn_tile(p, stage, smem, b, row0, tile_col0(p, ct + p.ct0));
     }
     __syncthreads();
     const int64_t nt = tile + int64_t(p.stages) * gridDim.x;

@@ -11,6 +11,9 @@ import paper_1002_2184_b200 as fhwt  # noqa: E402
 def main():
     shapes = ((64, 1080, 1920, 3), (32, 2160, 3840, 4), (256, 2048, 2048, 3), (256, 2048, 2048, 7),
               (16, 4096, 4096, 8), (1024, 512, 768, 6))
+    if os.environ.get("SMALL"):
+        shapes = ((65536, 32, 32, 5), (16384, 64, 64, 6), (16384, 64, 64, 3), (4096, 128, 128, 7), (4096, 128, 128, 5),
+                  (1024, 256, 256, 8), (65536, 16, 64, 4))
     if os.environ.get("RAGGED"):
         shapes = ((256, 1000, 1000, 3), (128, 720, 1280, 4), (512, 600, 800, 3), (64, 1200, 1600, 4), (32, 3000, 4000, 3))
     for (b, h, w, L) in shapes:
