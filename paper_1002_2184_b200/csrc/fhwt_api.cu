@@ -928,26 +928,30 @@ fhwt_status roundtrip_host(fhwt_plan_s* full, const float* h_d, float* h_c, floa
   const int64_t B = full->batch;
   if (!h_d || !h_r) return fail(FHWT_ERR_INVALID_ARG, "null host buffer");
   const int64_t unit_bytes = unit_elems * int64_t(sizeof(float));
-  if (chunk <= 0) chunk = std::max<int64_t>(1, (int64_t(256) << 20) / std::max<int64_t>(unit_bytes, 1));
+  // Default chunk ~128 MB (pipeline fill/drain = one chunk each way), NS streams in rotation so an
+  // H2D of chunk i+1 never waits behind the D2H of chunk i-1 on the same stream.
+  const int64_t mb = env_int("FHWT_RT_CHUNK_MB", 128);
+  if (chunk <= 0) chunk = std::max<int64_t>(1, (mb << 20) / std::max<int64_t>(unit_bytes, 1));
   chunk = std::min(chunk, B);
+  constexpr int kMaxStreams = 4;
+  const int NS = std::max(2, std::min(kMaxStreams, env_int("FHWT_RT_STREAMS", 3)));
   // chunk-sized plan (same shape, fewer units)
   fhwt_plan_s cp = *full;
   cp.batch = chunk;
   plan_layout(&cp);
-  cudaStream_t st[2];
-  FHWT_CUDA(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking), "stream create");
-  FHWT_CUDA(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking), "stream create");
+  cudaStream_t st[kMaxStreams];
+  for (int i = 0; i < NS; ++i) FHWT_CUDA(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "stream create");
   const size_t cbytes = size_t(chunk) * size_t(unit_bytes);
   const size_t wsb = align_up(cp.ws_bytes, 256);
-  char* buf[2] = {nullptr, nullptr};
+  char* buf[kMaxStreams] = {nullptr, nullptr, nullptr, nullptr};
   fhwt_status rs = FHWT_OK;
-  for (int i = 0; i < 2 && rs == FHWT_OK; ++i) {
+  for (int i = 0; i < NS && rs == FHWT_OK; ++i) {
     void* t = nullptr;
     rs = ws_alloc(&t, 3 * align_up(cbytes, 256) + wsb, st[i]);
     buf[i] = static_cast<char*>(t);
   }
   for (int64_t u0 = 0, it = 0; u0 < B && rs == FHWT_OK; u0 += chunk, ++it) {
-    const int k = int(it & 1);
+    const int k = int(it % NS);
     const int64_t cnt = std::min(chunk, B - u0);
     cudaStream_t s = st[k];
     float* dd = reinterpret_cast<float*>(buf[k]);
@@ -973,7 +977,7 @@ fhwt_status roundtrip_host(fhwt_plan_s* full, const float* h_d, float* h_c, floa
     e = cudaMemcpyAsync(h_r + u0 * unit_elems, dr, bytes, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) { rs = cuda_fail(e, "D2H copy"); break; }
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < NS; ++i) {
     if (buf[i]) cudaFreeAsync(buf[i], st[i]);
     cudaError_t e = cudaStreamSynchronize(st[i]);
     if (rs == FHWT_OK && e != cudaSuccess) rs = cuda_fail(e, "stream synchronize");
