@@ -235,8 +235,23 @@ __device__ __forceinline__ void small1d_ana_pass(const Small2dParams& p, const T
     const uint32_t gi = u / uint32_t(upr), t = u - gi * uint32_t(upr);
     TC v[U];
     const TS* sp = src + gi * ss + t * U;
+    if constexpr (U == 8 && sizeof(TS) == 4) {
+      if ((ss & 3) == 0) {   // 16-B aligned rows: two float4 loads, halves swapped on lanes 4-7 of
+                             // each quarter-warp so every phase covers all 32 banks
+        const bool sw = (threadIdx.x >> 2) & 1;
+        const float4 x0 = *reinterpret_cast<const float4*>(sp + (sw ? 4 : 0));
+        const float4 x1 = *reinterpret_cast<const float4*>(sp + (sw ? 0 : 4));
+        const float4 lo = sw ? x1 : x0, hi = sw ? x0 : x1;
+        v[0] = TC(lo.x); v[1] = TC(lo.y); v[2] = TC(lo.z); v[3] = TC(lo.w);
+        v[4] = TC(hi.x); v[5] = TC(hi.y); v[6] = TC(hi.z); v[7] = TC(hi.w);
+      } else {
 #pragma unroll
-    for (int e = 0; e < U; ++e) v[e] = TC(sp[e]);
+        for (int e = 0; e < U; ++e) v[e] = TC(sp[e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < U; ++e) v[e] = TC(sp[e]);
+    }
     float* row = O + gi * p.W;
 #pragma unroll
     for (int i = 1; i <= K; ++i) {   // level g0 + i: U >> i outputs
@@ -279,8 +294,15 @@ __device__ __forceinline__ void small1d_syn_pass(const Small2dParams& p, const f
       }
     }
     float* op = dst + gi * ds + t * U;
+    if (U == 8 && (ds & 3) == 0) {   // two float4 stores, halves swapped as in the analysis loads
+      const bool sw = (threadIdx.x >> 2) & 1;
+      const float4 lo = make_float4(v[0], v[1], v[2], v[3]), hi = make_float4(v[4 % U], v[5 % U], v[6 % U], v[7 % U]);
+      *reinterpret_cast<float4*>(op + (sw ? 4 : 0)) = sw ? hi : lo;
+      *reinterpret_cast<float4*>(op + (sw ? 0 : 4)) = sw ? lo : hi;
+    } else {
 #pragma unroll
-    for (int e = 0; e < U; ++e) op[e] = v[e];
+      for (int e = 0; e < U; ++e) op[e] = v[e];
+    }
   }
 }
 
