@@ -60,8 +60,15 @@ __device__ __forceinline__ void small_ana_level(const Small2dParams& p, const TS
   const int imgO = p.H * p.W;
   for (uint32_t u = threadIdx.x; u < total; u += blockDim.x) {
     const uint32_t gi = u / per, rem = u - gi * per, r = rem / uint32_t(w2), c = rem - r * uint32_t(w2);
-    const TS* s = src + gi * ss + (2 * r) * sp + 2 * c;
-    const TD a = TD(s[0]), bb = TD(s[1]), cc = TD(s[sp]), d = TD(s[sp + 1]);
+    const TS* s = src + gi * ss + (2 * r) * sp + 2 * c;   // even offset: pairs load as one 8/16-B word
+    TD a, bb, cc, d;
+    if constexpr (sizeof(TS) == 4) {
+      const float2 r0 = *reinterpret_cast<const float2*>(s), r1 = *reinterpret_cast<const float2*>(s + sp);
+      a = TD(r0.x); bb = TD(r0.y); cc = TD(r1.x); d = TD(r1.y);
+    } else {
+      const double2 r0 = *reinterpret_cast<const double2*>(s), r1 = *reinterpret_cast<const double2*>(s + sp);
+      a = r0.x; bb = r0.y; cc = r1.x; d = r1.y;
+    }
     const TD s1 = a + bb, s2 = cc + d, d1 = a - bb, d2 = cc - d;
     float* o = O + gi * imgO + r * p.W + c;
     o[w2] = float((d1 + d2) * TD(0.5));
@@ -146,11 +153,9 @@ __device__ __forceinline__ void small_syn_level(const Small2dParams& p, const fl
     const float* b = S + gi * imgS + r * p.W + c;
     const float vll = ll[gi * ls + r * lp + c], vhl = b[w2], vlh = b[h2 * p.W], vhh = b[h2 * p.W + w2];
     const float s = vll + vlh, t = vhl + vhh, s2 = vll - vlh, t2 = vhl - vhh;
-    float* o = dst + gi * ds + (2 * r) * dp + 2 * c;
-    o[0] = (s + t) * 0.5f;
-    o[1] = (s - t) * 0.5f;
-    o[dp] = (s2 + t2) * 0.5f;
-    o[dp + 1] = (s2 - t2) * 0.5f;
+    float* o = dst + gi * ds + (2 * r) * dp + 2 * c;   // even offset: one 8-B store per output row
+    *reinterpret_cast<float2*>(o) = make_float2((s + t) * 0.5f, (s - t) * 0.5f);
+    *reinterpret_cast<float2*>(o + dp) = make_float2((s2 + t2) * 0.5f, (s2 - t2) * 0.5f);
   }
 }
 
