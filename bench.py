@@ -254,7 +254,15 @@ def measure(name, cfg, args, ws, rank, local, pg):
     kern = "analysis" if ana_ms >= syn_ms else "synthesis"
     kern_ms = max(ana_ms, syn_ms)
     achieved = 8.0 * samples_rank / (kern_ms * 1e-3) / 1e9
+    steps_ms = [e[0].elapsed_time(e[3]) for e in evs]
+
+    def mmm(xs):   # median with min / max (this rank's per-step CUDA-event times, ms)
+        return {"median": statistics.median(xs), "min": min(xs), "max": max(xs)}
+
     res = {
+        "per_step_ms": {"analysis": mmm(ana), "synthesis": mmm(syn), "pack_gather": mmm(mid), "step": mmm(steps_ms)},
+        "gsamples_per_s_analysis": samples_rank / (ana_ms * 1e-3) / 1e9,
+        "gsamples_per_s_synthesis": samples_rank / (syn_ms * 1e-3) / 1e9,
         "value": bytes_step / (ms_step * 1e-3) / 1e9,
         "gsamples_per_s": samples_all / (ms_step * 1e-3) / 1e9,
         "ms_per_step": ms_step,
@@ -714,12 +722,13 @@ def main():
             if other == args.workload:
                 continue
             sub_args = argparse.Namespace(**vars(args))
-            sub_args.steps = max(5, min(args.steps, 10))
+            sub_args.steps = max(20, args.steps)   # >= 20 timed iterations
             r2, (p2, h2) = measure(other, WORKLOADS[other], sub_args, ws, rank, local, pg)
             del p2, h2
             breakdown[other] = {k: r2[k] for k in ("value", "gsamples_per_s", "ms_per_step", "analysis_ms",
                                                     "synthesis_ms", "gather_ms", "analysis_gbs", "synthesis_gbs",
-                                                    "roofline", "parity", "gpu_launches", "clocks")}
+                                                    "gsamples_per_s_analysis", "gsamples_per_s_synthesis",
+                                                    "per_step_ms", "roofline", "parity", "gpu_launches", "clocks")}
             breakdown[other]["workload"] = WORKLOADS[other]["desc"]
             breakdown[other]["scaling"] = WORKLOADS[other]["scaling"]
     cpu = None
@@ -737,7 +746,8 @@ def main():
                        "l2": "no flush: every step streams >= 4 GiB in and out, >> 126 MB L2",
                        "dtype_note": "fp32 I/O and levels 1-3; fp64 butterflies from level 4 (analysis)"},
             "gsamples_per_s": res["gsamples_per_s"],
-            "kernels": {k: res[k] for k in ("analysis_ms", "synthesis_ms", "gather_ms", "analysis_gbs", "synthesis_gbs")},
+            "kernels": {k: res[k] for k in ("analysis_ms", "synthesis_ms", "gather_ms", "analysis_gbs", "synthesis_gbs",
+                                            "gsamples_per_s_analysis", "gsamples_per_s_synthesis", "per_step_ms")},
             "roofline": res["roofline"],
             "sustained": res["sustained"],
             "cpu_baseline": cpu,
