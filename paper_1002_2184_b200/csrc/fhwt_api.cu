@@ -575,70 +575,69 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       nparts = 2;
     }
     for (int part = 0; part < nparts; ++part) {
-    const bool full = parts[part].full;
-    p.ct0 = parts[part].ct0;
-    p.tiles_c = parts[part].tiles_c;
-    p.ntiles = B * p.tiles_r * p.tiles_c;
-    const bool fast = full || (geom && env_int("FHWT_SYN_RAGGED_FAST", 1) != 0);
-    p.mask_mode = full ? 0 : 1;   // ragged or shifted boxes: masked variant, TMA boxes (mode 0)
-    // load path of the fast variant: 0 TMA boxes, 2 cp.async (LDGSTS) for all boxes.  Measured on
-    // B200 (tools/sweep_syn.py): cp.async 6.10 TB/s, TMA boxes 5.86 (register LDG of level 1: 5.19).
-    int mode = full ? env_int("FHWT_SYN_MODE", 3) : 0;
-    if (mode != 0 && mode != 3) mode = 2;
-    if (mode == 3 && !(p.TR == 32 && p.TC == 256)) mode = 2;   // warp-decoupled variant: 32 x 256 tiles only
-    p.l1_ldg = 0;
-    // stage layout: LL box, then per level j three boxes (128-B aligned: TMA destinations need it;
-    // with cp.async a 16-B packing would admit a 3rd CTA/SM, which measured slower: 5.54 vs 6.10 TB/s)
-    const size_t balign = 128;
-    size_t off = 0, tx = 0;
-    {
-      const size_t bytes = size_t(p.TR >> ps.Lp) * bw[ps.Lp] * 4;
-      p.box_off[0][0] = uint32_t(off);
-      off = align_up(off + bytes, balign);
-      tx += bytes;
-    }
-    for (int j = p.l1_ldg ? 2 : 1; j <= ps.Lp; ++j) {
-      const size_t bytes = size_t(p.TR >> j) * bw[j] * 4;
-      for (int q = 0; q < 3; ++q) {
-        p.box_off[j][q] = uint32_t(off);
+      const bool full = parts[part].full;
+      p.ct0 = parts[part].ct0;
+      p.tiles_c = parts[part].tiles_c;
+      p.ntiles = B * p.tiles_r * p.tiles_c;
+      const bool fast = full || (geom && env_int("FHWT_SYN_RAGGED_FAST", 1) != 0);
+      p.mask_mode = full ? 0 : 1;   // ragged or shifted boxes: masked variant, TMA boxes (mode 0)
+      // load path of the fast variant: 0 TMA boxes, 2 cp.async (LDGSTS) for all boxes.  Measured on
+      // B200 (tools/sweep_syn.py): cp.async 6.10 TB/s, TMA boxes 5.86 (register LDG of level 1: 5.19).
+      int mode = full ? env_int("FHWT_SYN_MODE", 3) : 0;
+      if (mode != 0 && mode != 3) mode = 2;
+      if (mode == 3 && !(p.TR == 32 && p.TC == 256)) mode = 2;   // warp-decoupled variant: 32 x 256 tiles only
+      // stage layout: LL box, then per level j three boxes (128-B aligned: TMA destinations need it;
+      // with cp.async a 16-B packing would admit a 3rd CTA/SM, which measured slower: 5.54 vs 6.10 TB/s)
+      const size_t balign = 128;
+      size_t off = 0, tx = 0;
+      {
+        const size_t bytes = size_t(p.TR >> ps.Lp) * bw[ps.Lp] * 4;
+        p.box_off[0][0] = uint32_t(off);
         off = align_up(off + bytes, balign);
         tx += bytes;
       }
+      for (int j = 1; j <= ps.Lp; ++j) {
+        const size_t bytes = size_t(p.TR >> j) * bw[j] * 4;
+        for (int q = 0; q < 3; ++q) {
+          p.box_off[j][q] = uint32_t(off);
+          off = align_up(off + bytes, balign);
+          tx += bytes;
+        }
+      }
+      p.tx_bytes = uint32_t(tx);
+      p.stage_bytes = uint32_t(align_up(off, 1024));
+      p.stages = env_int("FHWT_SYN_STAGES", syn_ring_stages(p.stage_bytes));   // 2 for 32 x 256 tiles
+      size_t pb[2] = {0, 0};
+      for (int j = 2; j <= ps.Lp; ++j) {
+        const int jj = j - 1;
+        pb[jj & 1] = std::max(pb[jj & 1], size_t(p.TR >> jj) * size_t(p.TC >> jj) * 4);
+      }
+      off = size_t(p.stages) * p.stage_bytes;
+      p.p_off[0] = uint32_t(off);
+      if (mode == 3) {
+        off = align_up(off + size_t(kThreads2d / 32) * kSynScratchBytes, 128);
+        p.p_off[1] = p.p_off[0];
+      } else {
+        off = align_up(off + pb[0], 128);
+        p.p_off[1] = uint32_t(off);
+        off = align_up(off + pb[1], 128);
+      }
+      p.bar_off = uint32_t(off);
+      const size_t smem = off + 12 * size_t(p.stages);   // mbarriers + stage-release counters
+      const int fast_lp = fast ? (mode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
+      int bps = 0;
+      FHWT_TRY(occupancy(2, fast_lp, smem, &bps));
+      // At most 2 resident CTAs/SM: the lighter LP < 5 variants fit 3-4, which measured 2.5-6.5 %
+      // slower (tools/sweep_ctas.py, profiles/r01_sweep_ctas.jsonl); LP = 5 is indifferent.
+      bps = std::min(bps, env_int("FHWT_CTAS_PER_SM", 2 * kThreads2d / syn2d_threads(fast_lp)));
+      const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
+      if (coop) {
+        if (mode != 3) return fail(FHWT_ERR_CUDA, "internal: cooperative synthesis needs the warp-decoupled kernel");
+        p.head = pl->passes[1].Lp;
+        p.ll_ws_out = reinterpret_cast<float*>(ws + pl->ws_off[0]);
+      }
+      FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
     }
-    p.tx_bytes = uint32_t(tx);
-    p.stage_bytes = uint32_t(align_up(off, 1024));
-    p.stages = env_int("FHWT_SYN_STAGES", syn_ring_stages(p.stage_bytes));   // 2 for 32 x 256 tiles
-    size_t pb[2] = {0, 0};
-    for (int j = 2; j <= ps.Lp; ++j) {
-      const int jj = j - 1;
-      pb[jj & 1] = std::max(pb[jj & 1], size_t(p.TR >> jj) * size_t(p.TC >> jj) * 4);
-    }
-    off = size_t(p.stages) * p.stage_bytes;
-    p.p_off[0] = uint32_t(off);
-    if (mode == 3) {
-      off = align_up(off + size_t(kThreads2d / 32) * kSynScratchBytes, 128);
-      p.p_off[1] = p.p_off[0];
-    } else {
-      off = align_up(off + pb[0], 128);
-      p.p_off[1] = uint32_t(off);
-      off = align_up(off + pb[1], 128);
-    }
-    p.bar_off = uint32_t(off);
-    const size_t smem = off + 12 * size_t(p.stages);   // mbarriers + stage-release counters
-    const int fast_lp = fast ? (mode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
-    int bps = 0;
-    FHWT_TRY(occupancy(2, fast_lp, smem, &bps));
-    // At most 2 resident CTAs/SM: the lighter LP < 5 variants fit 3-4, which measured 2.5-6.5 %
-    // slower (tools/sweep_ctas.py, profiles/r01_sweep_ctas.jsonl); LP = 5 is indifferent.
-    bps = std::min(bps, env_int("FHWT_CTAS_PER_SM", 2 * kThreads2d / syn2d_threads(fast_lp)));
-    const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
-    if (coop) {
-      if (mode != 3) return fail(FHWT_ERR_CUDA, "internal: cooperative synthesis needs the warp-decoupled kernel");
-      p.head = pl->passes[1].Lp;
-      p.ll_ws_out = reinterpret_cast<float*>(ws + pl->ws_off[0]);
-    }
-    FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
-    }   // parts
   }
   return FHWT_OK;
 }

@@ -54,7 +54,6 @@ struct Ana2dParams {
 
 struct Syn2dParams {
   const float* coeffs;   // Mallat coefficients (pitch W), read by the cp.async variant
-  int l1_ldg;            // reserved (0): level 1 is always staged with the other boxes
   const float* ll_ws;    // LL_{g0+Lp} source in the workspace (cp.async variant; pitch pitch4(Win >> Lp))
   float* out;            // d_R (final pass, pitch W) or the LL_{g0} hand-off (pitch Win)
   int64_t out_pitch;

@@ -833,8 +833,8 @@ __device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned
   cp_async_commit();
 }
 
-// Issues the TMA loads of tile t into one stage (LL box + 3 band boxes per level; level 1 is
-// skipped when it is read by LDG).  Called by all of warp 0; lane 0 issues.
+// Issues the TMA loads of tile t into one stage (LL box + 3 band boxes per level).  Called by all
+// of warp 0; lane 0 issues.
 __device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* base,
                                                uint64_t* bar, int64_t t, uint64_t pol) {
   const int lane = threadIdx.x & 31;
@@ -849,7 +849,7 @@ __device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMa
   const int llrows = p.row_boxes[L] ? (p.TR >> L) : 1;
   for (int r = 0; r < llrows; ++r)
     tma_load_2d(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int(col0 >> L), int(llrow + r), bar, pol);
-  for (int j = L; j >= (p.l1_ldg ? 2 : 1); --j) {
+  for (int j = L; j >= 1; --j) {
     const int g = p.g0 + j;
     const int64_t hg = p.H >> g, wg = p.W >> g;
     const int64_t br = b * p.H + (row0 >> j), bc = col0 >> j;
