@@ -173,10 +173,14 @@ def measure(name, cfg, args, ws, rank, local, pg):
         plan = fhwt.Plan1d(d.shape[-1], d.numel() // d.shape[-1], L)
     wsb = torch.empty(max(plan.workspace_bytes, 1), dtype=torch.uint8, device=dev)
     gather = cfg["shard"] == "rowband" and ws > 1
+    p2p = None
     if cfg["shard"] == "rowband":
         ll_rows, ll_cols = d.shape[0] >> L, d.shape[1] >> L
         ll_local = torch.empty((ll_rows, ll_cols), dtype=torch.float32, device=dev)
         ll_all = torch.empty((ll_rows * ws, ll_cols), dtype=torch.float32, device=dev)
+        if getattr(args, "ll_gather", "nccl") == "p2p" and dist.is_initialized():
+            # pack fused with the all-gather over NVLink peer memory (one kernel + a device barrier)
+            p2p = fdist.PeerLLGather(ll_rows, ll_cols, group=pg, device=dev)
     stream = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)     # c5: LL pack + all-gather, overlapped with the synthesis pass
     ana_done = torch.cuda.Event()
@@ -195,9 +199,12 @@ def measure(name, cfg, args, ws, rank, local, pg):
             with torch.cuda.stream(side):
                 if evs:
                     evs[4].record(side)
-                fhwt.pack_ll_2d(coeffs, L, out=ll_local, stream=side)
-                if gather:
-                    fdist.gather_coarse_ll(ll_local, group=pg, out=ll_all)
+                if p2p is not None:
+                    p2p(coeffs, L, stream=side)
+                else:
+                    fhwt.pack_ll_2d(coeffs, L, out=ll_local, stream=side)
+                    if gather:
+                        fdist.gather_coarse_ll(ll_local, group=pg, out=ll_all)
                 if evs:
                     evs[2].record(side)
         elif evs:
@@ -214,7 +221,12 @@ def measure(name, cfg, args, ws, rank, local, pg):
     torch.cuda.synchronize(dev)
     # properties of this run's own output (not timed)
     parity = sampled_parity(name, cfg, host, coeffs, rec, rank, ws) if rank == 0 else None
-    if gather and rank == 0:
+    if p2p is not None:   # the fused path's result against the plain pack of this rank's band
+        fhwt.pack_ll_2d(coeffs, L, out=ll_local)
+        torch.cuda.synchronize(dev)
+        if rank == 0:
+            parity["gathered_ll"] = dict(check_gathered_ll(p2p.buf, ll_local, rank, ws), path="p2p")
+    elif gather and rank == 0:
         parity["gathered_ll"] = check_gathered_ll(ll_all, ll_local, rank, ws)
 
     K = args.steps
@@ -657,7 +669,7 @@ def run_reference(args):
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the reference arm is the fp64 CPU oracle (no reference implementation exists); each step is a bounded sample",
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
     return 0
 
 
@@ -676,6 +688,8 @@ def main():
                     help="gloo only for plumbing checks (FHWT_BENCH_ONE_DEVICE=1 on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ll-gather", default="nccl", choices=["nccl", "p2p"],
+                    help="c5 coarse-LL exchange: NCCL all-gather, or pack + stores into peer symmetric memory")
     ap.add_argument("--sustained", type=float, default=1.5,
                     help="seconds of warm + timed back-to-back steps per analysis variant (0 = skip)")
     args = ap.parse_args()
@@ -697,6 +711,11 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(args.dist_backend)
+        pg = dist.group.WORLD
+    elif args.ll_gather == "p2p":   # one GPU: a one-rank group exercises the peer-store path on itself
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
         pg = dist.group.WORLD
     cfg = WORKLOADS[args.workload]
     res, (plan, host) = measure(args.workload, cfg, args, ws, rank, local, pg)
@@ -760,12 +779,32 @@ def main():
             "lowpass_u8": lowpass,
             "latency": latency,
         }
-        print(json.dumps(out), flush=True)
-    if ws > 1:
+        emit(out)
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
+def _json_stdout():
+    """Keep stdout to the one JSON line: library banners written to fd 1 (NCCL's version line,
+    symmetric-memory notices) are sent to stderr, and the JSON line goes to a saved copy of fd 1."""
+    global _OUT
+    try:
+        sys.stdout.flush()
+        _OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+    except OSError:
+        _OUT = sys.stdout
+
+
+_OUT = sys.stdout
+
+
+def emit(obj):
+    print(json.dumps(obj), file=_OUT, flush=True)
+
+
 if __name__ == "__main__":
+    _json_stdout()
     sys.exit(main())

@@ -138,6 +138,16 @@ int64_t fhwt_band_offset_2d(int64_t h, int64_t w, int level, int band, int64_t *
  * row-band sharded images. */
 fhwt_status fhwt_pack_ll_2d(const float *coeffs, float *ll_packed, int64_t h, int64_t w, int64_t batch,
                             int levels, fhwt_stream_t s);
+/* The pack fused with the row-band all-gather over peer memory (NVLink P2P
+ * stores instead of pack + collective): this rank's LL_levels block (as fhwt_pack_ll_2d) is stored
+ * into EVERY peer's gather buffer at element offset rank * batch*(h>>levels)*(w>>levels).
+ * peer_ll: DEVICE array of npeers device pointers, peer access enabled (e.g. the buffer_ptrs_dev of a
+ * torch symmetric-memory rendezvous), each buffer >= npeers * batch*(h>>levels)*(w>>levels) floats;
+ * rank in [0, npeers).  Asynchronous on s; the stores are visible to a peer only after a cross-rank
+ * barrier that follows this call on every rank (the caller's).  Errors: INVALID_ARG, as
+ * fhwt_plan_2d, CUDA. */
+fhwt_status fhwt_pack_ll_2d_peers(const float *coeffs, float *const *peer_ll, int rank, int npeers, int64_t h,
+                                  int64_t w, int64_t batch, int levels, fhwt_stream_t s);
 /* The same pack with (h, w, batch, levels) taken from a 2-D plan (SURVEY §8(b) form).
  * Errors: INVALID_ARG (NULL plan, 1-D plan, NULL buffers). */
 fhwt_status fhwt_plan_pack_ll_2d(fhwt_plan p, const float *coeffs, float *ll_packed, fhwt_stream_t s);

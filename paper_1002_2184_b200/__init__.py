@@ -18,7 +18,7 @@ __all__ = [
     "ShapeMismatch", "UnsupportedFilter", "Misaligned", "CudaError", "NoDevice", "InvalidArgument",
     "lib", "lib_path", "haar_filter_bank", "launch_count", "version",
     "analyze_1d", "synthesize_1d", "analyze_2d", "synthesize_2d", "Plan1d", "Plan2d",
-    "pack_ll_2d", "roundtrip_2d_host", "roundtrip_1d_host", "band_offset_1d", "band_offset_2d",
+    "pack_ll_2d", "pack_ll_2d_peers", "roundtrip_2d_host", "roundtrip_1d_host", "band_offset_1d", "band_offset_2d",
     "direct_workspace_bytes", "direct_analyze_1d", "direct_synthesize_1d", "direct_analyze_2d",
     "direct_synthesize_2d", "op_counts", "lowpass_2d_u8", "lowpass_2d_bf16",
 ]
@@ -127,6 +127,7 @@ def lib():
         "fhwt_band_offset_2d": (i64, [i64, i64, c_int, c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "fhwt_pack_ll_2d": (st, [vp, vp, i64, i64, i64, c_int, vp]),
         "fhwt_plan_pack_ll_2d": (st, [vp, vp, vp, vp]),
+        "fhwt_pack_ll_2d_peers": (st, [vp, vp, c_int, c_int, i64, i64, i64, c_int, vp]),
         "fhwt_workspace_bytes": (ctypes.c_size_t, [vp]),
         "fhwt_analyze": (st, [vp, vp, vp, vp, vp]),
         "fhwt_synthesize": (st, [vp, vp, vp, vp, vp]),
@@ -381,6 +382,15 @@ class Plan2d(_Plan):
             _check(lib().fhwt_plan_pack_ll_2d(self._h, _dev_f32(coeffs, "coeffs"), _dev_f32(out, "ll"),
                                               _stream(stream, coeffs)))
         return out
+
+
+def pack_ll_2d_peers(coeffs, levels: int, peer_ptrs_dev: int, rank: int, npeers: int, stream=None):
+    """fhwt_pack_ll_2d_peers: store this rank's packed LL_levels into every peer's gather buffer
+    (peer_ptrs_dev: device address of an array of npeers peer device pointers)."""
+    h, w, batch = _shape_2d(coeffs)
+    with _guard_device(coeffs):
+        _check(lib().fhwt_pack_ll_2d_peers(_dev_f32(coeffs, "coeffs"), ctypes.c_void_p(int(peer_ptrs_dev)), int(rank),
+                                           int(npeers), h, w, batch, int(levels), _stream(stream, coeffs)))
 
 
 def pack_ll_2d(coeffs, levels: int, out=None, stream=None):

@@ -911,6 +911,16 @@ fhwt_status fhwt_pack_ll_2d(const float* coeffs, float* ll_packed, int64_t h, in
   return FHWT_OK;
 }
 
+fhwt_status fhwt_pack_ll_2d_peers(const float* coeffs, float* const* peer_ll, int rank, int npeers, int64_t h,
+                                  int64_t w, int64_t batch, int levels, fhwt_stream_t s) {
+  FHWT_TRY(check_2d(h, w, batch, levels));
+  if (!coeffs || !peer_ll) return fail(FHWT_ERR_INVALID_ARG, "null pointer");
+  if (npeers < 1 || rank < 0 || rank >= npeers) return fail(FHWT_ERR_INVALID_ARG, "rank %d of %d peers", rank, npeers);
+  FHWT_CUDA(launch_pack_ll_peers(coeffs, peer_ll, rank, npeers, h, w, batch, levels, reinterpret_cast<cudaStream_t>(s)),
+            "pack_ll_peers launch");
+  return FHWT_OK;
+}
+
 fhwt_status fhwt_plan_pack_ll_2d(fhwt_plan p, const float* coeffs, float* ll_packed, fhwt_stream_t s) {
   if (!p) return fail(FHWT_ERR_INVALID_ARG, "null plan");
   if (p->kind != 2) return fail(FHWT_ERR_INVALID_ARG, "fhwt_plan_pack_ll_2d needs a 2-D plan");

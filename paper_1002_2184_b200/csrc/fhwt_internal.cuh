@@ -129,6 +129,8 @@ cudaError_t launch_ana2d_l1_scalar(const float* d, float* c, int64_t h, int64_t 
 cudaError_t launch_syn2d_l1_scalar(const float* c, float* d, int64_t h, int64_t w, int64_t batch, cudaStream_t s);
 cudaError_t launch_ana1d_l1_scalar(const float* d, float* c, int64_t n, int64_t batch, cudaStream_t s);
 cudaError_t launch_syn1d_l1_scalar(const float* c, float* d, int64_t n, int64_t batch, cudaStream_t s);
+cudaError_t launch_pack_ll_peers(const float* c, float* const* peers, int rank, int npeers, int64_t h, int64_t w,
+                                 int64_t batch, int levels, cudaStream_t s);
 cudaError_t launch_pack_ll(const float* c, float* ll, int64_t h, int64_t w, int64_t batch, int levels,
                            cudaStream_t s);
 

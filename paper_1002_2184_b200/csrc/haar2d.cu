@@ -1130,6 +1130,22 @@ __global__ void syn2d_l1_scalar_kernel(const float* __restrict__ c, float* __res
   }
 }
 
+// Pack fused with the row-band all-gather over peer memory: every LL element of this rank's band
+// is stored straight into each peer's gather buffer (NVLink P2P stores through UVA pointers), at
+// element offset rank * n.  One launch replaces pack + collective; a cross-rank barrier after it
+// (the caller's) makes the stores visible.
+__global__ void pack_ll_peers_kernel(const float* __restrict__ c, float* const* __restrict__ peers, int rank,
+                                     int npeers, int64_t h, int64_t w, int64_t batch, int levels) {
+  const int64_t hl = h >> levels, wl = w >> levels;
+  const int64_t total = batch * hl * wl;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / (hl * wl), rem = i - b * hl * wl;
+    const int64_t r = rem / wl, q = rem - r * wl;
+    const float v = c[b * h * w + r * w + q];
+    for (int k = 0; k < npeers; ++k) peers[k][int64_t(rank) * total + i] = v;
+  }
+}
+
 __global__ void pack_ll_kernel(const float* __restrict__ c, float* __restrict__ ll, int64_t h, int64_t w,
                                int64_t batch, int levels) {
   const int64_t hl = h >> levels, wl = w >> levels;
@@ -1295,6 +1311,14 @@ cudaError_t launch_ana2d_l1_scalar(const float* d, float* c, int64_t h, int64_t 
 cudaError_t launch_syn2d_l1_scalar(const float* c, float* d, int64_t h, int64_t w, int64_t batch, cudaStream_t s) {
   count_launch();
   syn2d_l1_scalar_kernel<<<grid_for(batch * (h / 2) * (w / 2), 256), 256, 0, s>>>(c, d, h, w, batch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_ll_peers(const float* c, float* const* peers, int rank, int npeers, int64_t h, int64_t w,
+                                 int64_t batch, int levels, cudaStream_t s) {
+  count_launch();
+  pack_ll_peers_kernel<<<grid_for(batch * (h >> levels) * (w >> levels), 256), 256, 0, s>>>(c, peers, rank, npeers, h,
+                                                                                             w, batch, levels);
   return cudaGetLastError();
 }
 

@@ -85,3 +85,30 @@ def max_over_ranks(values, device=None, group=None):
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     res = [float(v) for v in t.tolist()]
     return res[0] if scalar else res
+
+
+class PeerLLGather:
+    """The coarsest-LL all-gather of row-band sharding, fused with the pack over peer memory
+    (NVLink P2P): every rank stores its band's LL straight into each peer's symmetric buffer
+    (fhwt_pack_ll_2d_peers, one kernel), then one device-side cross-rank barrier (torch symmetric
+    memory) makes the stores visible.  The result is laid out as gather_coarse_ll's (rank order
+    = row order).  Needs CUDA devices with peer access (one node, NVLink / NVSwitch)."""
+
+    def __init__(self, rows_per_rank: int, cols: int, group=None, device=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        group = group or dist.group.WORLD
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.rows, self.cols = rows_per_rank, cols
+        self.buf = symm_mem.empty((self.world * rows_per_rank, cols), dtype=torch.float32,
+                                  device=device or torch.device("cuda", torch.cuda.current_device()))
+        self.handle = symm_mem.rendezvous(self.buf, group.group_name)
+
+    def __call__(self, coeffs: torch.Tensor, levels: int, stream=None) -> torch.Tensor:
+        from . import pack_ll_2d_peers
+        if coeffs.shape[-2] >> levels != self.rows or coeffs.shape[-1] >> levels != self.cols:
+            raise ValueError("coefficient band does not match the gather buffer")
+        pack_ll_2d_peers(coeffs, levels, self.handle.buffer_ptrs_dev, self.handle.rank, self.handle.world_size,
+                         stream=stream)
+        self.handle.barrier(channel=0)
+        return self.buf

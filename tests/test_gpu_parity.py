@@ -532,3 +532,34 @@ def test_short_signals_chunk_kernels(monkeypatch, n, batch, levels):
     rg = fhwt.synthesize_1d(c, levels)
     torch.cuda.synchronize()
     assert torch.equal(c, cg) and torch.equal(r, rg)
+
+
+def test_peer_memory_ll_gather_one_rank():
+    """The fused pack + all-gather over peer memory (fhwt_pack_ll_2d_peers + a symmetric-memory
+    barrier) on a one-rank NCCL group: the gathered LL equals the plain pack of the band.  (Multi-rank
+    layout: rank r's block lands at rows [r*rows, (r+1)*rows) of every peer's buffer, the same
+    kernel with npeers > 1; the row-band arithmetic is covered by tests/test_dist_gloo.py.)"""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1002_2184_b200 import dist as fdist
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        x = dev(np.stack([datagen.c4_image(0, 512)[:256]]))[0]
+        c = fhwt.analyze_2d(x, 8)
+        g = fdist.PeerLLGather(256 >> 8, 512 >> 8)
+        out = g(c, 8)
+        torch.cuda.synchronize()
+        assert torch.equal(out, fhwt.pack_ll_2d(c, 8))
+        with pytest.raises(fhwt.InvalidArgument):   # rank outside [0, npeers)
+            fhwt.pack_ll_2d_peers(c, 8, g.handle.buffer_ptrs_dev, 1, 1)
+    finally:
+        dist.destroy_process_group()
