@@ -156,7 +156,8 @@ fhwt_status fhwt_plan_pack_ll_2d(fhwt_plan p, const float *coeffs, float *ll_pac
  * End-to-end DWT + IDWT on HOST buffers (pinned memory recommended): the batch is streamed in
  * chunks of `chunk` images (or signals) through device staging buffers owned by the call, with
  * H2D copy, analysis, synthesis and D2H copies of coeffs (if h_coeffs != NULL) and d_R
- * overlapped across two CUDA streams.  Blocks until the results are in host memory.
+ * overlapped across CUDA streams (3 by default; env FHWT_RT_STREAMS, 2..4).  Blocks until the
+ * results are in host memory.
  * chunk <= 0 picks a default.  Errors as the device entry points, plus CUDA for copy failures. */
 fhwt_status fhwt_roundtrip_2d_host(const float *h_d, float *h_coeffs, float *h_dR, int64_t h, int64_t w,
                                    int64_t batch, int levels, int64_t chunk);
