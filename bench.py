@@ -591,7 +591,7 @@ def measure_e2e(cfg, host, steps):
             "ms_per_step": t * 1e3, "steps": steps,
             "h2d_bytes_per_step": 4 * s, "d2h_bytes_per_step": 4 * s,
             "pcie_duplex_ms_same_bytes": t_duplex * 1e3,
-            "api": "fhwt_roundtrip_%s_host (pinned host buffers; chunked H2D, DWT, IDWT, D2H of d_R on two streams)"
+            "api": "fhwt_roundtrip_%s_host (pinned host buffers; chunked H2D, DWT, IDWT, D2H of d_R on 3 CUDA streams)"
                    % ("2d" if cfg["kind"] == "2d" else "1d")}
 
 
