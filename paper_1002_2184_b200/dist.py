@@ -11,7 +11,9 @@ block independent), so sharding needs no halo exchange:
   of all bands is all-gathered (the only exchange; 64 KiB for c5).
 
 Only host arithmetic and the collective live here; the packing is the library's
-fhwt_pack_ll_2d kernel on GPU (callers pass the packed tensor).
+fhwt_pack_ll_2d kernel on GPU (callers pass the packed tensor).  PeerLLGather is the opt-in
+alternative that fuses the pack with the gather (fhwt_pack_ll_2d_peers stores into every peer's
+symmetric-memory buffer over NVLink).
 """
 from __future__ import annotations
 
@@ -91,8 +93,14 @@ class PeerLLGather:
     """The coarsest-LL all-gather of row-band sharding, fused with the pack over peer memory
     (NVLink P2P): every rank stores its band's LL straight into each peer's symmetric buffer
     (fhwt_pack_ll_2d_peers, one kernel), then one device-side cross-rank barrier (torch symmetric
-    memory) makes the stores visible.  The result is laid out as gather_coarse_ll's (rank order
-    = row order).  Needs CUDA devices with peer access (one node, NVLink / NVSwitch)."""
+    memory) on the same stream makes the stores visible.  The result is laid out as
+    gather_coarse_ll's (rank order = row order).  Needs CUDA devices with peer access (one node,
+    NVLink / NVSwitch).
+
+    Two buffer slots alternate between calls: call k writes slot k % 2 on every rank, so a rank
+    may still read call k-1's result (stream-ordered before its call k+1) while faster peers
+    already store call k.  Call k+1 reuses the slot of call k-1, which every rank finished reading
+    before it entered call k's barrier (reads are consumed before the next call on the stream)."""
 
     def __init__(self, rows_per_rank: int, cols: int, group=None, device=None):
         import torch.distributed._symmetric_memory as symm_mem
@@ -100,15 +108,29 @@ class PeerLLGather:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.rows, self.cols = rows_per_rank, cols
-        self.buf = symm_mem.empty((self.world * rows_per_rank, cols), dtype=torch.float32,
-                                  device=device or torch.device("cuda", torch.cuda.current_device()))
-        self.handle = symm_mem.rendezvous(self.buf, group.group_name)
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        self._mem = symm_mem.empty((2, self.world * rows_per_rank, cols), dtype=torch.float32, device=device)
+        self.handle = symm_mem.rendezvous(self._mem, group.group_name)
+        slot = self.world * rows_per_rank * cols * 4
+        # per slot: a device array of every peer's slot base address (the kernel's peer table)
+        self._peers = [torch.tensor([int(p) + k * slot for p in self.handle.buffer_ptrs], dtype=torch.int64,
+                                    device=device) for k in range(2)]
+        self._calls = 0
+
+    @property
+    def buf(self) -> torch.Tensor:
+        """The slot of the latest call's result."""
+        return self._mem[(self._calls - 1) % 2]
 
     def __call__(self, coeffs: torch.Tensor, levels: int, stream=None) -> torch.Tensor:
         from . import pack_ll_2d_peers
         if coeffs.shape[-2] >> levels != self.rows or coeffs.shape[-1] >> levels != self.cols:
             raise ValueError("coefficient band does not match the gather buffer")
-        pack_ll_2d_peers(coeffs, levels, self.handle.buffer_ptrs_dev, self.handle.rank, self.handle.world_size,
-                         stream=stream)
-        self.handle.barrier(channel=0)
-        return self.buf
+        k = self._calls % 2
+        stream = stream or torch.cuda.current_stream(self._mem.device)
+        with torch.cuda.stream(stream):   # the barrier kernel runs on torch's current stream
+            pack_ll_2d_peers(coeffs, levels, self._peers[k].data_ptr(), self.handle.rank, self.handle.world_size,
+                             stream=stream)
+            self.handle.barrier(channel=0)
+        self._calls += 1
+        return self._mem[k]

@@ -534,12 +534,32 @@ def test_short_signals_chunk_kernels(monkeypatch, n, batch, levels):
     assert torch.equal(c, cg) and torch.equal(r, rg)
 
 
+def test_pack_ll_peers_table_layout():
+    """fhwt_pack_ll_2d_peers with npeers = 3 local buffers standing in for the peers' symmetric
+    buffers (a plain device pointer table, no cross-rank waiting): rank r's packed LL lands at
+    rows [r*rows, (r+1)*rows) of every buffer and nothing else is written."""
+    x = dev(datagen.uniform((2, 256, 512), seed=41))
+    c = fhwt.analyze_2d(x, 5)
+    ll = fhwt.pack_ll_2d(c, 5)                              # [2, 8, 16]
+    rows = ll.numel() // ll.shape[-1]                       # every image's LL rows, stacked
+    bufs = [torch.full((3 * rows, 16), -7.0, device="cuda") for _ in range(3)]
+    table = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    fhwt.pack_ll_2d_peers(c, 5, table.data_ptr(), 1, 3)
+    torch.cuda.synchronize()
+    for b in bufs:
+        assert torch.equal(b[rows:2 * rows], ll.reshape(rows, 16))
+        assert bool((b[:rows] == -7).all()) and bool((b[2 * rows:] == -7).all())
+    with pytest.raises(fhwt.InvalidArgument):   # rank outside [0, npeers)
+        fhwt.pack_ll_2d_peers(c, 5, table.data_ptr(), 3, 3)
+    with pytest.raises(fhwt.InvalidArgument):
+        fhwt.pack_ll_2d_peers(c, 5, table.data_ptr(), -1, 3)
+
+
 def test_peer_memory_ll_gather_one_rank():
     """The fused pack + all-gather over peer memory (fhwt_pack_ll_2d_peers + a symmetric-memory
-    barrier) on a one-rank NCCL group: the gathered LL equals the plain pack of the band.  (Multi-rank
-    layout: rank r's block lands at rows [r*rows, (r+1)*rows) of every peer's buffer, the same
-    kernel with npeers > 1; the row-band arithmetic is covered by tests/test_dist_gloo.py.)"""
-    import os
+    barrier) on a one-rank NCCL group: the gathered LL equals the plain pack of the band, and the
+    two result slots alternate (call k's result survives call k+1).  Multi-rank placement is
+    test_pack_ll_peers_table_layout; the row-band arithmetic is tests/test_dist_gloo.py."""
     import socket
 
     import torch.distributed as dist
@@ -553,13 +573,18 @@ def test_peer_memory_ll_gather_one_rank():
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
                             device_id=torch.device("cuda", torch.cuda.current_device()))
     try:
-        x = dev(np.stack([datagen.c4_image(0, 512)[:256]]))[0]
-        c = fhwt.analyze_2d(x, 8)
-        g = fdist.PeerLLGather(256 >> 8, 512 >> 8)
-        out = g(c, 8)
-        torch.cuda.synchronize()
-        assert torch.equal(out, fhwt.pack_ll_2d(c, 8))
-        with pytest.raises(fhwt.InvalidArgument):   # rank outside [0, npeers)
-            fhwt.pack_ll_2d_peers(c, 8, g.handle.buffer_ptrs_dev, 1, 1)
+        xs = [dev(datagen.c4_image(i, 2048)[:1024]) for i in range(2)]
+        cs = [fhwt.analyze_2d(x, 5) for x in xs]
+        g = fdist.PeerLLGather(1024 >> 5, 2048 >> 5)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        out0 = g(cs[0], 5, stream=side)
+        out1 = g(cs[1], 5, stream=side)
+        side.synchronize()
+        assert out0.data_ptr() != out1.data_ptr() and g.buf.data_ptr() == out1.data_ptr()
+        assert torch.equal(out0, fhwt.pack_ll_2d(cs[0], 5))
+        assert torch.equal(out1, fhwt.pack_ll_2d(cs[1], 5))
+        with pytest.raises(ValueError):
+            g(fhwt.analyze_2d(xs[0][:512], 5), 5)
     finally:
         dist.destroy_process_group()
