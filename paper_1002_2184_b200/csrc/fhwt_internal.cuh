@@ -44,6 +44,7 @@ struct Ana2dParams {
   int mask_mode;         // fast variants: 0 all tiles full, 1 last column tile ragged (masked stores)
   int aligned_levels;    // levels j with even band offsets (unchecked 8-B stores): 1..aligned_levels
   int clamp_last;        // ragged width: the last column tile starts at Win - TC (see tile_col0)
+  int clamp_rows;        // Hin % TR != 0: the last row tile starts at Hin - TR (see tile_row0)
   int fused;             // 32 x 256 fast tiles, LP >= 3: levels 2+3 and 4+5 fused (FHWT_ANA_FUSED, default 1)
   int tail;              // > 0: after the tiles, a grid barrier and levels 6..5+tail of the fp64 LL5
                          // hand-off in the same (cooperative) launch (ana_coarse); 0: none
@@ -65,6 +66,7 @@ struct Syn2dParams {
   int64_t tiles_r, tiles_c, ntiles;
   int64_t ct0;             // first column tile of this launch (a ragged width runs as two launches)
   int clamp_last;          // ragged width: the last column tile starts at Win - TC (see tile_col0)
+  int clamp_rows;          // Hin % TR != 0: the last row tile starts at Hin - TR (see tile_row0)
   int stages;
   uint32_t stage_bytes, bar_off;
   uint32_t box_off[6][3];  // per pass-level j (1..Lp): offsets of HL, LH, HH boxes; [0][0] = LL box

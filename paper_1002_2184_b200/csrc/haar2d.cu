@@ -40,6 +40,15 @@ __device__ __forceinline__ int64_t tile_col0(const P& p, int64_t ct) {
   return (p.clamp_last && c + p.TC > p.Win) ? p.Win - p.TC : c;
 }
 
+// First row of row tile rt (within an image): rt * TR, except that with clamp_rows the last tile of
+// a height that is not a multiple of TR starts at Hin - TR (full, overlapping its neighbour; Hin - TR
+// is a multiple of 2^Lp, so the overlapped rows are recomputed from the same inputs: same values).
+template <typename P>
+__device__ __forceinline__ int64_t tile_row0(const P& p, int64_t rt) {
+  const int64_t r = rt * p.TR;
+  return (p.clamp_rows && r + p.TR > p.Hin) ? p.Hin - p.TR : r;
+}
+
 // Threads per CTA of a compile-time fast variant: one 2 x 2V unit per thread on level 1 of the
 // smallest tiles (8 x 128: 64 threads), so small-tile shapes (e.g. 1080-row frames) run many
 // independent CTAs per SM instead of a few latency-bound 256-thread ones; 256 from 32 x 128 up.
@@ -209,19 +218,24 @@ __device__ __forceinline__ void ana_issue_tile(const Ana2dParams& p, const CUten
                                                uint64_t pol) {
   const int lane = threadIdx.x & 31;
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+  int64_t grow = rt * p.TR;   // first row in the (batch * Hin)-row tensor
+  if (p.clamp_rows) {
+    const int64_t b = rt / p.tiles_r;
+    grow = b * p.Hin + tile_row0(p, rt - b * p.tiles_r);
+  }
   if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
   __syncwarp();
   if (p.row_boxes) {
     if (lane == 0) {
       if (p.l2hint)
         for (int r = 0; r < p.TR; ++r)
-          tma_load_2d(dst + r * row_bytes, map, int(tile_col0(p, ct)), int(rt * p.TR + r), bar, pol);
+          tma_load_2d(dst + r * row_bytes, map, int(tile_col0(p, ct)), int(grow + r), bar, pol);
       else
         for (int r = 0; r < p.TR; ++r)
-          tma_load_2d_nohint(dst + r * row_bytes, map, int(tile_col0(p, ct)), int(rt * p.TR + r), bar);
+          tma_load_2d_nohint(dst + r * row_bytes, map, int(tile_col0(p, ct)), int(grow + r), bar);
     }
   } else if (lane == 0) {
-    tma_load_2d(dst, map, int(tile_col0(p, ct)), int(rt * p.TR), bar, pol);
+    tma_load_2d(dst, map, int(tile_col0(p, ct)), int(grow), bar, pol);
   }
 }
 
@@ -564,7 +578,7 @@ __global__ void __launch_bounds__(288, 2) ana2d_fused3_kernel(const __grid_const
     const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
                         tile_bytes, row_bytes, pol};
     ana_fused3_tile(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b,
-                          (rt - b * p.tiles_r) * 32, ct * 256, it, refill);
+                          tile_row0(p, rt - b * p.tiles_r), ct * 256, it, refill);
   }
   if (p.tail > 0) {
     cooperative_groups::this_grid().sync();
@@ -604,7 +618,7 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
     mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
-    const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
+    const int64_t row0 = tile_row0(p, rt - b * p.tiles_r);
     const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
                         tile_bytes, row_bytes, pol};
     // mask_mode 1: the last column tile is ragged (masked stores); aligned_levels < LP: the coarse
@@ -665,7 +679,8 @@ struct TileXY {
   int64_t b, row0, col0;
 };
 // tile -> (image, first row, first column); 32-bit division when the tile count allows it
-__device__ __forceinline__ TileXY tile_xy(int64_t tile, int64_t tiles_c, int64_t tiles_r, int TR, int TC) {
+__device__ __forceinline__ TileXY tile_xy(int64_t tile, int64_t tiles_c, int64_t tiles_r, int TR, int TC,
+                                          int64_t clamp_row0) {   // clamp_row0: Hin - TR, or -1 (no clamp)
   TileXY t;
   if (tiles_c * tiles_r < (int64_t(1) << 31) && tile < (int64_t(1) << 31)) {
     const uint32_t rt = uint32_t(tile) / uint32_t(tiles_c), ct = uint32_t(tile) - rt * uint32_t(tiles_c);
@@ -679,6 +694,7 @@ __device__ __forceinline__ TileXY tile_xy(int64_t tile, int64_t tiles_c, int64_t
     t.row0 = (rt - t.b * tiles_r) * TR;
     t.col0 = ct * TC;
   }
+  if (clamp_row0 >= 0 && t.row0 > clamp_row0) t.row0 = clamp_row0;
   return t;
 }
 
@@ -797,7 +813,7 @@ template <int LP, int TRF, int TCF>
 __device__ __forceinline__ void syn_cp_async_tile(const Syn2dParams& p, unsigned char* base, int64_t t) {
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
-  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = tile_col0(p, ct + p.ct0);
+  const int64_t row0 = tile_row0(p, rt - b * p.tiles_r), col0 = tile_col0(p, ct + p.ct0);
   int q0 = 0;
 #pragma unroll
   for (int j = 1; j <= LP; ++j) {
@@ -840,7 +856,7 @@ __device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMa
   const int lane = threadIdx.x & 31;
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
-  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = tile_col0(p, ct + p.ct0);
+  const int64_t row0 = tile_row0(p, rt - b * p.tiles_r), col0 = tile_col0(p, ct + p.ct0);
   if (lane == 0) mbar_arrive_expect_tx(bar, p.tx_bytes);
   __syncwarp();
   if (lane != 0) return;
@@ -871,7 +887,7 @@ __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const 
                                                     uint64_t* bar, int64_t t, uint64_t pol) {
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
-  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = tile_col0(p, ct + p.ct0);
+  const int64_t row0 = tile_row0(p, rt - b * p.tiles_r), col0 = tile_col0(p, ct + p.ct0);
   mbar_arrive_expect_tx(bar, p.tx_bytes);
   const int L = p.Lp;
   const int64_t llrow = p.ll_from_ws ? b * (p.Hin >> L) + (row0 >> L) : b * p.H + (row0 >> L);
@@ -991,7 +1007,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(c
   for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
     const int s = it % p.stages;
     mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
-    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256);
+    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256, p.clamp_rows ? p.Hin - 32 : -1);
     const unsigned char* stage = smem + s * p.stage_bytes;
     const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> LP);
     warp_syn_steps<LP, LP>(p, ll, 256 >> LP, stage, warp, sc, xy.b, xy.row0,
@@ -1065,7 +1081,7 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
     }
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
-    const int64_t row0 = (rt - b * p.tiles_r) * p.TR;
+    const int64_t row0 = tile_row0(p, rt - b * p.tiles_r);
     unsigned char* stage = smem + s * p.stage_bytes;
     if constexpr (LPFAST > 0) {
       const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]);

@@ -16,6 +16,8 @@ def main():
                   (1024, 256, 256, 8), (65536, 16, 64, 4))
     if os.environ.get("RAGGED"):
         shapes = ((256, 1000, 1000, 3), (128, 720, 1280, 4), (512, 600, 800, 3), (64, 1200, 1600, 4), (32, 3000, 4000, 3))
+    if os.environ.get("SHAPES"):   # "b,h,w,L;b,h,w,L;..."
+        shapes = tuple(tuple(int(v) for v in t.split(",")) for t in os.environ["SHAPES"].split(";"))
     for (b, h, w, L) in shapes:
         x = torch.rand(b, h, w, device="cuda")
         plan = fhwt.Plan2d(h, w, b, L)
