@@ -276,7 +276,10 @@ int choose_tc(int64_t w, int pref) {
   if (pref < 256) return int(std::min<int64_t>(pref, w));
   if (w < 128) return env_int("FHWT_NARROW_FAST", 1) && w >= 16 && w % 16 == 0 ? 128 : int(w);   // one masked tile
   if (w % 256 == 0) return 256;
-  if (w % 128 == 0) return 128;
+  // w % 256 == 128: 256-column tiles with the last one overlapping (clamp_last) when that repeats at
+  // most 10 % of the columns; measured 1080 x 1920: synthesis 5.17 -> 6.23 TB/s (the 32 x 256
+  // warp-decoupled kernel instead of 32 x 128 cp.async tiles), analysis 5.28 -> 5.43; 1280 neutral
+  if (w % 128 == 0) return (128 * 10 <= w && env_int("FHWT_TC256_CLAMP", 1) != 0) ? 256 : 128;
   // ragged: 256-column tiles unless they would pad a row by more than 20 % (e.g. 800 -> 1024);
   // measured: 1600-wide rows 5.4 TB/s with 256-column tiles vs 4.6 with 128
   return ((w + 255) / 256 * 256 - w) * 5 > w ? 128 : 256;

@@ -494,22 +494,25 @@ def test_ragged_widths_fast_geometry(monkeypatch, b, h, w, levels):
 
 
 @pytest.mark.parametrize("b,h,w,levels", [(2, 1000, 1000, 3), (1, 1080, 1920, 3), (2, 720, 1280, 4), (1, 600, 800, 3),
-                                          (3, 1000, 512, 1), (1, 1040, 512, 4), (2, 232, 256, 3), (2, 1000, 3000, 2)])
+                                          (3, 1000, 512, 1), (1, 1040, 512, 4), (2, 232, 256, 3), (2, 1000, 3000, 2),
+                                          (1, 256, 3968, 5), (2, 64, 1408, 3)])
 def test_row_clamped_tiles(monkeypatch, b, h, w, levels):
     """Heights that are not a multiple of 32 keep 32-row tiles with the last row tile clamped to
-    h - 32 (overlapping rows recomputed and stored twice): oracle parity, and bitwise equality
-    with the 8/16-row tiling (FHWT_CLAMP_ROWS=0)."""
+    h - 32 (overlapping rows recomputed and stored twice), widths with w % 256 == 128 take
+    256-column tiles with the last one clamped: oracle parity, and bitwise equality with the
+    8/16-row (FHWT_CLAMP_ROWS=0) and 128-column (FHWT_TC256_CLAMP=0) tilings."""
     x = datagen.uniform((b, h, w), seed=3 * h + w + levels, lo=-1.0, hi=1.0)
     xd = dev(x)
     c = fhwt.analyze_2d(xd, levels)
     r = fhwt.synthesize_2d(c, levels)
     assert_close(host(c), o.analyze_2d(x, levels), x, 2, what=f"row clamp {h}x{w} L={levels}")
     assert_close(host(r), x, x, 2, what="row clamp round trip")
-    monkeypatch.setenv("FHWT_CLAMP_ROWS", "0")
-    c0 = fhwt.analyze_2d(xd, levels)
-    r0 = fhwt.synthesize_2d(c, levels)
-    torch.cuda.synchronize()
-    assert torch.equal(c, c0) and torch.equal(r, r0)
+    for knob in ("FHWT_CLAMP_ROWS", "FHWT_TC256_CLAMP"):   # then also 128-column tiles for w % 256 == 128
+        monkeypatch.setenv(knob, "0")
+        c0 = fhwt.analyze_2d(xd, levels)
+        r0 = fhwt.synthesize_2d(c, levels)
+        torch.cuda.synchronize()
+        assert torch.equal(c, c0) and torch.equal(r, r0), knob
 
 
 @pytest.mark.parametrize("b,h,w,levels", [(7, 32, 32, 5), (300, 16, 64, 4), (5, 64, 64, 6), (9, 8, 8, 3), (3, 4, 4, 2),
