@@ -550,11 +550,22 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     TmaMaps2d maps;
     std::memset(&maps, 0, sizeof maps);
     int bw[6] = {0, 0, 0, 0, 0, 0};
+    // Shifted warp-decoupled variant (mode 6, haar2d.cu syn_issue_tile_lane<true>): 32 x 256 tiles
+    // whose band blocks do not all start 16-B aligned (W >> j odd or 2 mod 4, or the clamped last
+    // tile's Win - 256 >> j): every box starts at the aligned column below and is 4 columns wider.
+    bool shifted = false;
+    if (ps.g0 == 0 && !coop && p.TR == 32 && p.TC == 256 && p.Win > p.TC && W % 4 == 0 &&
+        env_int("FHWT_SYN_SHIFT", 1) != 0 && env_int("FHWT_SYN_MODE", 3) == 3) {
+      bool al = (W >> 1) % 2 == 0;
+      for (int j = 1; j <= ps.Lp; ++j)
+        al = al && (W >> j) % 4 == 0 && (p.Win % p.TC == 0 || ((p.Win - p.TC) >> j) % 4 == 0);
+      shifted = !al;
+    }
     for (int j = 1; j <= ps.Lp; ++j) {
       // TMA box starts must be 16-byte aligned: LH boxes start at col0 >> j (a multiple of 4),
       // HL/HH boxes at (W >> g) + (col0 >> j), so they start hoff = (W >> g) & 3 columns early.
-      p.hoff[j] = int((W >> (ps.g0 + j)) & 3);
-      bw[j] = int(pitch4((p.TC >> j) + p.hoff[j]));
+      p.hoff[j] = shifted ? 0 : int((W >> (ps.g0 + j)) & 3);
+      bw[j] = shifted ? (p.TC >> j) + 4 : int(pitch4((p.TC >> j) + p.hoff[j]));
       p.box_pitch[j] = bw[j];
       p.row_boxes[j] = bw[j] * 4 >= 1024 && (bw[j] * 4) % 128 == 0;   // see the analysis note
       FHWT_TRY(encode_2d(&maps.level[j], coeffs, false, W, B * H, W, bw[j], p.row_boxes[j] ? 1 : p.TR >> j));
@@ -578,9 +589,13 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     // (cp.async / warp-decoupled) and the last column of tiles on the masked TMA variant.
     const bool ragged = p.Win % p.TC != 0;
     // clamp_last: the last tile starts at Win - TC, full and on the fast path (needs those tile
-    // starts 16-B aligned at every level too); otherwise the split below
+    // starts 16-B aligned at every level too, or the shifted variant); otherwise the split below
     p.clamp_last = aligned && ragged && p.Win > p.TC && env_int("FHWT_CLAMP_LAST", 1) != 0;
     for (int j = 1; j <= ps.Lp && p.clamp_last; ++j) p.clamp_last = ((p.Win - p.TC) >> j) % 4 == 0;
+    if (shifted) {
+      aligned = true;   // every tile full, boxes widened and shifted
+      p.clamp_last = ragged;
+    }
     const bool split = aligned && ragged && !p.clamp_last && !coop && p.Win >= p.TC &&
                        env_int("FHWT_SYN_SPLIT", 1) != 0;
     struct Part {
@@ -606,6 +621,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       int mode = full ? env_int("FHWT_SYN_MODE", 3) : 0;
       if (mode != 0 && mode != 3) mode = 2;
       if (mode == 3 && !(p.TR == 32 && p.TC == 256)) mode = 2;   // warp-decoupled variant: 32 x 256 tiles only
+      if (shifted) mode = 6;
       // stage layout: LL box, then per level j three boxes (128-B aligned: TMA destinations need it;
       // with cp.async a 16-B packing would admit a 3rd CTA/SM, which measured slower: 5.54 vs 6.10 TB/s)
       const size_t balign = 128;
@@ -634,7 +650,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       }
       off = size_t(p.stages) * p.stage_bytes;
       p.p_off[0] = uint32_t(off);
-      if (mode == 3) {
+      if (mode == 3 || mode == 6) {
         off = align_up(off + size_t(kThreads2d / 32) * kSynScratchBytes, 128);
         p.p_off[1] = p.p_off[0];
       } else {

@@ -883,17 +883,23 @@ __device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMa
 // --------------------------------------------------- warp-decoupled synthesis (32 x 256 tiles)
 // Mirror of ana2d_warp_kernel: warp w rebuilds output columns [32w, 32w + 32) of a tile from the
 // level-j coefficient blocks at columns [(32w) >> j, (32w + 32) >> j) of the staged boxes.
+// SHIFT: band blocks that do not start 16-B aligned (W >> g or the clamped last tile's column
+// offset not a multiple of 4): every box starts at the aligned column at or below the block and is 4
+// columns wider (box_pitch = (TC >> j) + 4); the compute phase adds the shift (column & 3).
+template <bool SHIFT = false>
 __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* base,
                                                     uint64_t* bar, int64_t t, uint64_t pol) {
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
   const int64_t row0 = tile_row0(p, rt - b * p.tiles_r), col0 = tile_col0(p, ct + p.ct0);
+  constexpr int64_t AL = SHIFT ? ~int64_t(3) : ~int64_t(0);
   mbar_arrive_expect_tx(bar, p.tx_bytes);
   const int L = p.Lp;
   const int64_t llrow = p.ll_from_ws ? b * (p.Hin >> L) + (row0 >> L) : b * p.H + (row0 >> L);
   const int llrows = p.row_boxes[L] ? (p.TR >> L) : 1;
   for (int r = 0; r < llrows; ++r)
-    tma_load_2d(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int(col0 >> L), int(llrow + r), bar, pol);
+    tma_load_2d(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int((col0 >> L) & AL), int(llrow + r), bar,
+                pol);
   for (int j = L; j >= 1; --j) {
     const int g = p.g0 + j;
     const int64_t hg = p.H >> g, wg = p.W >> g;
@@ -901,23 +907,27 @@ __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const 
     const int rb = p.box_pitch[j] * 4;
     const int nrows = p.row_boxes[j] ? (p.TR >> j) : 1;
     for (int r = 0; r < nrows; ++r) {
-      tma_load_2d(base + p.box_off[j][0] + r * rb, &maps.level[j], int(wg + bc), int(br + r), bar, pol);
-      tma_load_2d(base + p.box_off[j][1] + r * rb, &maps.level[j], int(bc), int(br + hg + r), bar, pol);
-      tma_load_2d(base + p.box_off[j][2] + r * rb, &maps.level[j], int(wg + bc), int(br + hg + r), bar, pol);
+      tma_load_2d(base + p.box_off[j][0] + r * rb, &maps.level[j], int((wg + bc) & AL), int(br + r), bar, pol);
+      tma_load_2d(base + p.box_off[j][1] + r * rb, &maps.level[j], int(bc & AL), int(br + hg + r), bar, pol);
+      tma_load_2d(base + p.box_off[j][2] + r * rb, &maps.level[j], int((wg + bc) & AL), int(br + hg + r), bar, pol);
     }
   }
 }
 
-template <int J>
+template <int J, bool SHIFT, bool LLSHIFT>
 __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float* __restrict__ ll, int llp,
                                                const unsigned char* stage, int warp, float* __restrict__ dst,
-                                               int64_t b, int64_t row0, int64_t colw) {
-  constexpr int R = 32 >> J, C = 32 >> J, BP = 256 >> J;
+                                               int64_t b, int64_t row0, int64_t colw, int64_t col0) {
+  constexpr int R = 32 >> J, C = 32 >> J, BP = (256 >> J) + (SHIFT ? 4 : 0);
   constexpr int V = C >= 2 ? 2 : 1, UPR = C / V, NU = R * UPR, OC = 2 * C;
-  const int co = (32 * warp) >> J;
-  const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]) + co;
+  int co = (32 * warp) >> J, coh = co;
+  if constexpr (SHIFT) {   // see syn_issue_tile_lane<true>
+    co += int((col0 >> J) & 3);
+    coh += int(((p.W >> (p.g0 + J)) + (col0 >> J)) & 3);
+  }
+  const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]) + coh;
   const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]) + co;
-  const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]) + co;
+  const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]) + coh;
   const int lane = threadIdx.x & 31;
   float* const obase = p.out + (b * p.Hin + row0) * p.out_pitch + colw;
 #pragma unroll
@@ -926,10 +936,10 @@ __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float
     if (NU % 32 != 0 && u >= NU) break;
     const int r = u / UPR, c = (u - r * UPR) * V;
     float vll[V], vhl[V], vlh[V], vhh[V];
-    load_row<float, V, true>(ll + r * llp + c, vll);
-    load_row<float, V, true>(hl + r * BP + c, vhl);
-    load_row<float, V, true>(lh + r * BP + c, vlh);
-    load_row<float, V, true>(hh + r * BP + c, vhh);
+    load_row<float, V, !LLSHIFT>(ll + r * llp + c, vll);
+    load_row<float, V, !SHIFT>(hl + r * BP + c, vhl);
+    load_row<float, V, !SHIFT>(lh + r * BP + c, vlh);
+    load_row<float, V, !SHIFT>(hh + r * BP + c, vhh);
     float top[2 * V], bot[2 * V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -957,19 +967,19 @@ __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float
   }
 }
 
-template <int J, int LP>
+template <int J, int LP, bool SHIFT>
 __device__ __forceinline__ void warp_syn_steps(const Syn2dParams& p, const float* ll, int llp,
                                                const unsigned char* stage, int warp, WarpScratch* sc, int64_t b,
-                                               int64_t row0, int64_t colw) {
+                                               int64_t row0, int64_t colw, int64_t col0) {
   float* dst = J == 5 ? reinterpret_cast<float*>(sc->ll4) : J == 4 ? sc->ll3 : J == 3 ? sc->ll2 : sc->ll1;
-  warp_syn_level<J>(p, ll, llp, stage, warp, dst, b, row0, colw);
+  warp_syn_level<J, SHIFT, SHIFT && J == LP>(p, ll, llp, stage, warp, dst, b, row0, colw, col0);
   if constexpr (J > 1) {
     __syncwarp();
-    warp_syn_steps<J - 1, LP>(p, dst, 2 * (32 >> J), stage, warp, sc, b, row0, colw);
+    warp_syn_steps<J - 1, LP, SHIFT>(p, dst, 2 * (32 >> J), stage, warp, sc, b, row0, colw, col0);
   }
 }
 
-template <int LP>
+template <int LP, bool SHIFT = false>
 __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(const __grid_constant__ Syn2dParams p,
                                                                 const __grid_constant__ TmaMaps2d maps) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -987,7 +997,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(c
     fence_mbar_init();
   }
   __syncthreads();
-  if constexpr (LP == 5) {
+  if constexpr (LP == 5 && !SHIFT) {
     if (p.head > 0) {   // cooperative launch: coarse levels -> fp32 LL5 hand-off, then a grid barrier
       if (p.head == 1) syn_coarse<1>(p);
       else if (p.head == 2) syn_coarse<2>(p);
@@ -1001,7 +1011,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(c
   if (tid == 0)
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
-      if (t < p.ntiles) syn_issue_tile_lane(p, maps, smem + s * p.stage_bytes, &bars[s], t, pol);
+      if (t < p.ntiles) syn_issue_tile_lane<SHIFT>(p, maps, smem + s * p.stage_bytes, &bars[s], t, pol);
     }
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
@@ -1009,15 +1019,17 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(c
     mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
     const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256, p.clamp_rows ? p.Hin - 32 : -1);
     const unsigned char* stage = smem + s * p.stage_bytes;
-    const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> LP);
-    warp_syn_steps<LP, LP>(p, ll, 256 >> LP, stage, warp, sc, xy.b, xy.row0,
-                           tile_col0(p, xy.col0 / 256 + p.ct0) + 32 * warp);
+    const int64_t col0 = tile_col0(p, xy.col0 / 256 + p.ct0);
+    const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> LP) +
+                      (SHIFT ? int((col0 >> LP) & 3) : 0);
+    warp_syn_steps<LP, LP, SHIFT>(p, ll, (256 >> LP) + (SHIFT ? 4 : 0), stage, warp, sc, xy.b, xy.row0,
+                                  col0 + 32 * warp, col0);
     __syncwarp();
     if (lane == 0) {   // stage release: the 8th warp through level 1 refills it
       __threadfence_block();
       if ((atomicAdd(&cnt[s], 1u) & 7u) == 7u) {
         const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
-        if (nt < p.ntiles) syn_issue_tile_lane(p, maps, smem + s * p.stage_bytes, &bars[s], nt, pol);
+        if (nt < p.ntiles) syn_issue_tile_lane<SHIFT>(p, maps, smem + s * p.stage_bytes, &bars[s], nt, pol);
       }
     }
   }
@@ -1259,6 +1271,10 @@ template <int LP>
 struct SynW {
   static const void* get() { return (const void*)syn2d_warp_kernel<LP>; }
 };
+template <int LP>
+struct SynWS {
+  static const void* get() { return (const void*)syn2d_warp_kernel<LP, true>; }
+};
 
 static const void* ana2d_fn(bool in_f64, int fast) {
   if (in_f64) return (const void*)ana2d_kernel<double, 0, 0, 0>;
@@ -1271,6 +1287,7 @@ static const void* syn2d_fn(int fast) {
   if (fast == 0) return (const void*)syn2d_kernel<0, 0, 0, 0>;
   const int mode = (fast >> 24) & 0xff;
   if (mode == 3) return warp_fn<SynW>(fast & 15);
+  if (mode == 6) return warp_fn<SynWS>(fast & 15);
   return mode == 2 ? by_geometry<SynF2>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15)
                    : by_geometry<SynF0>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15);
 }
@@ -1282,7 +1299,10 @@ int ana2d_threads(int fast) {
   const int mode = (fast >> 24) & 0xff;
   return mode == 5 ? 288 : fast_threads_rt(fast);
 }
-int syn2d_threads(int fast) { return ((fast >> 24) & 0xff) == 3 ? kThreads2d : fast_threads_rt(fast); }
+int syn2d_threads(int fast) {
+  const int mode = (fast >> 24) & 0xff;
+  return (mode == 3 || mode == 6) ? kThreads2d : fast_threads_rt(fast);
+}
 
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm) {
   const void* fn = ana2d_fn(in_f64, fast_lp);

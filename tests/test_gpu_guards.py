@@ -32,7 +32,7 @@ def assert_guards(buf):
 @pytest.mark.parametrize("b,h,w,levels", [(2, 40, 1000, 3), (3, 32, 800, 3), (1, 48, 1600, 4), (2, 64, 1160, 3),
                                           (1, 256, 1280, 7), (33, 32, 32, 5), (301, 16, 64, 4), (5, 64, 64, 6),
                                           (2, 128, 512, 7), (3, 8, 24, 3), (2, 1000, 1000, 3), (1, 1080, 512, 3),
-                                          (1, 360, 256, 3)])
+                                          (1, 360, 256, 3), (2, 64, 1064, 3), (1, 64, 1088, 6)])
 def test_2d_outputs_stay_in_bounds(b, h, w, levels):
     x = torch.rand(b, h, w, device="cuda")
     cbuf, c = guarded((b, h, w))

@@ -493,6 +493,26 @@ def test_ragged_widths_fast_geometry(monkeypatch, b, h, w, levels):
     assert torch.equal(c, cg) and torch.equal(r, rg)
 
 
+@pytest.mark.parametrize("b,h,w,levels", [(2, 64, 1000, 3), (1, 96, 1160, 3), (1, 64, 1088, 6), (2, 32, 1064, 3),
+                                          (1, 1000, 1000, 3), (1, 64, 1184, 5), (1, 256, 1800, 3), (2, 64, 520, 3),
+                                          (1, 64, 2024, 2)])
+def test_shifted_synthesis_boxes(monkeypatch, b, h, w, levels):
+    """Widths whose band blocks do not start 16-B aligned run the shifted warp-decoupled synthesis
+    (boxes start at the aligned column below, 4 columns wider; last tile clamped): oracle parity
+    and bitwise equality with the masked TMA variant (FHWT_SYN_SHIFT=0)."""
+    x = datagen.uniform((b, h, w), seed=5 * h + w + levels, lo=-1.0, hi=1.0)
+    c = fhwt.analyze_2d(dev(x), levels)
+    r = fhwt.synthesize_2d(c, levels)
+    assert_close(host(r), x, x, 2, what=f"shifted {h}x{w} L={levels}")
+    c32 = o.analyze_2d(x, levels).astype(np.float32)
+    rs = fhwt.synthesize_2d(dev(c32), levels)
+    assert_close(host(rs), o.synthesize_2d(c32, levels), x, 2, what="shifted synthesis vs oracle")
+    monkeypatch.setenv("FHWT_SYN_SHIFT", "0")
+    r0 = fhwt.synthesize_2d(c, levels)
+    torch.cuda.synchronize()
+    assert torch.equal(r, r0)
+
+
 @pytest.mark.parametrize("b,h,w,levels", [(2, 1000, 1000, 3), (1, 1080, 1920, 3), (2, 720, 1280, 4), (1, 600, 800, 3),
                                           (3, 1000, 512, 1), (1, 1040, 512, 4), (2, 232, 256, 3), (2, 1000, 3000, 2),
                                           (1, 256, 3968, 5), (2, 64, 1408, 3)])
