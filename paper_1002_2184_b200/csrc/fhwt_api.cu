@@ -295,6 +295,40 @@ int choose_tc(int64_t w, int pref) {
 int ring_stages(uint32_t stage_bytes) {
   return int(std::min<uint32_t>(8, std::max<uint32_t>(2, (65536 + stage_bytes - 1) / stage_bytes)));
 }
+// Analysis ring depth / CTAs-per-SM cap for the narrower first-pass tiles (tools/sweep128.sh,
+// profiles/r01_generic_shapes.md; GB/s analysis, default occupancy -> table):
+//   32 x 128: 2 CTAs/SM, 2 stages (3 when tiles overlap): 480 x 640 5.5 -> 6.3 TB/s, 1152^2 5.5 -> 6.3,
+//             600 x 800 (overlapping last tile) 5.0 -> 6.0
+//   16 x 256: 3 CTAs/SM: 2160 x 3840 5.4 -> 6.3, 720 x 1280 5.3 -> 6.2 (at 2 stages; 4 stages as good)
+//   16 x 128: 4 CTAs/SM, 4 stages: 400 x 544 4.8 -> 6.2
+// 32 x 256 (c4) keeps the occupancy limit (2 CTAs/SM) and 2 stages; 8-row tiles keep the defaults.
+void ana_tile_cfg(int tr, int tc, bool overlap, int* stages, int* cap_ctas) {
+  if (tr == 32 && tc == 128) {
+    *cap_ctas = 2;
+    *stages = overlap ? 3 : 2;
+  } else if (tr == 16 && tc == 256) {
+    *cap_ctas = 3;
+    *stages = 4;
+  } else if (tr == 16 && tc == 128) {
+    *cap_ctas = 4;
+    *stages = 4;
+  }
+}
+
+// Synthesis (cp.async variant) ring depth / CTAs-per-SM cap for the narrower tiles
+// (tools/sweep_syn128.sh; GB/s synthesis, default -> table): 32 x 128 at 2 stages, 3 CTAs/SM:
+// 480 x 640 5.3 -> 5.8, 600 x 800 5.0 -> 6.1, 1152^2 5.4 -> 5.8; 16 x 128 at 4 stages, 4 CTAs/SM:
+// 400 x 544 5.2 -> 5.7.
+void syn_tile_cfg(int tr, int tc, int* stages, int* cap_ctas) {
+  if (tr == 32 && tc == 128) {
+    *stages = 2;
+    *cap_ctas = 3;
+  } else if (tr == 16 && tc == 128) {
+    *stages = 4;
+    *cap_ctas = 4;
+  }
+}
+
 int syn_ring_stages(uint32_t stage_bytes) {
   return int(std::min<uint32_t>(4, std::max<uint32_t>(2, (49152 + stage_bytes - 1) / stage_bytes)));
 }
@@ -454,7 +488,12 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     // Ring depth: at least 64 KB of staged input per CTA (2 stages of 32 x 256 fp32 tiles; up to 8
     // stages of smaller tiles, e.g. 8 x 128 for 1080-row frames, where 2 stages kept too few bytes
     // in flight).
-    p.stages = in64 ? 2 : env_int("FHWT_ANA_STAGES", ring_stages(p.stage_bytes));
+    // Narrower fast tiles: ring depth and resident CTAs per SM from a measured table (tile_cfg);
+    // too many small CTAs per SM (occupancy allows 4-10) streamed 10-25 % slower.
+    int cap_ctas = 0, stages = ring_stages(p.stage_bytes);
+    if (!in64 && ps.g0 == 0 && env_int("FHWT_ANA_TILE_TABLE", 1) != 0)
+      ana_tile_cfg(p.TR, p.TC, p.Win % p.TC != 0 || p.clamp_rows, &stages, &cap_ctas);
+    p.stages = in64 ? 2 : env_int("FHWT_ANA_STAGES", stages);
     size_t pb[2] = {0, 0};
     for (int j = 1; j < ps.Lp; ++j) {
       const size_t sz = (in64 || ps.g0 + j >= kFirstF64Level) ? 8 : 4;
@@ -486,7 +525,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     const int fast = fast_ok ? (vmode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
     FHWT_TRY(occupancy(in64 ? 1 : 0, fast, smem, &bps));
-    if (const int cap = env_int("FHWT_CTAS_PER_SM", 0)) bps = std::min(bps, cap);   // sweep knob
+    if (const int cap = env_int("FHWT_ANA_CTAS_PER_SM", env_int("FHWT_CTAS_PER_SM", cap_ctas))) bps = std::min(bps, cap);
     const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
     // 5 < L <= 8 on the 32-row fast path: the coarse levels run after a grid barrier in the same,
     // cooperative, launch (haar2d.cu ana_coarse) instead of a second small-grid pass.
@@ -642,7 +681,10 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       }
       p.tx_bytes = uint32_t(tx);
       p.stage_bytes = uint32_t(align_up(off, 1024));
-      p.stages = env_int("FHWT_SYN_STAGES", syn_ring_stages(p.stage_bytes));   // 2 for 32 x 256 tiles
+      // 2 stages for 32 x 256 tiles; the cp.async variant's narrower tiles from a measured table
+      int syn_stages = syn_ring_stages(p.stage_bytes), syn_cap = 0;
+      if (mode == 2 && env_int("FHWT_SYN_TILE_TABLE", 1) != 0) syn_tile_cfg(p.TR, p.TC, &syn_stages, &syn_cap);
+      p.stages = env_int("FHWT_SYN_STAGES", syn_stages);
       size_t pb[2] = {0, 0};
       for (int j = 2; j <= ps.Lp; ++j) {
         const int jj = j - 1;
@@ -665,7 +707,8 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       FHWT_TRY(occupancy(2, fast_lp, smem, &bps));
       // At most 2 resident CTAs/SM: the lighter LP < 5 variants fit 3-4, which measured 2.5-6.5 %
       // slower (tools/sweep_ctas.py, profiles/r01_sweep_ctas.jsonl); LP = 5 is indifferent.
-      bps = std::min(bps, env_int("FHWT_CTAS_PER_SM", 2 * kThreads2d / syn2d_threads(fast_lp)));
+      const int cap = env_int("FHWT_CTAS_PER_SM", syn_cap);   // sweep knob; 0 = the measured default
+      bps = std::min(bps, cap > 0 ? cap : 2 * kThreads2d / syn2d_threads(fast_lp));
       const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
       if (coop) {
         if (mode != 3) return fail(FHWT_ERR_CUDA, "internal: cooperative synthesis needs the warp-decoupled kernel");
