@@ -722,6 +722,19 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
 }
 
 // ------------------------------------------------------------------ 1-D execution
+// Levels > 10 of signals of 1024, 2048, 4096 or 8192 samples (a full decomposition: J up to 13):
+// the 8 warps of a CTA hold whole signals, so levels 11..J run inside the first-pass CTA from
+// the chunks' LL10 in shared memory (haar1d.cu ana1d_tail / syn1d_tail) instead of a second pass
+// whose grid has one warp per 1-8 values.  Measured 65536 x 4096, J = 12: analysis 0.371 ->
+// 0.314 ms, synthesis 0.353 -> 0.311.  Returns the number of such levels, or 0.
+int tail1d(const fhwt_plan_s* pl) {
+  if (pl->passes.size() != 2 || pl->passes[0].Lp != 10 || env_int("FHWT_1D_TAIL", 1) == 0) return 0;
+  const int64_t chunks = pl->n / kChunk1d;
+  if (pl->n % kChunk1d != 0 || (chunks != 1 && chunks != 2 && chunks != 4 && chunks != 8)) return 0;
+  if ((pl->batch * chunks) % 8 != 0) return 0;   // whole CTAs (8 warps) only
+  return pl->passes[1].Lp;
+}
+
 fhwt_status run_ana1d(const fhwt_plan_s* pl, const float* d, float* coeffs, char* ws, cudaStream_t s) {
   const int64_t n = pl->n, B = pl->batch;
   if (n % 4 != 0 || !aligned16(d) || !aligned16(coeffs)) {
@@ -732,9 +745,14 @@ fhwt_status run_ana1d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
   }
   if (small1d_ok(pl, d, coeffs)) return run_small1d(pl, d, coeffs, s, true);
   const size_t np = pl->passes.size();
+  const int tail = tail1d(pl);
   for (size_t k = 0; k < np; ++k) {
     const Pass ps = pl->passes[k];
     Haar1dParams p{};
+    if (tail) {   // levels 11.. inside the first pass (haar1d.cu ana1d_tail)
+      p.tail = tail;
+      p.final_pass = 1;
+    }
     p.n = n;
     p.nin = n >> ps.g0;
     p.batch = B;
@@ -743,12 +761,13 @@ fhwt_status run_ana1d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     p.chunks = (p.nin + kChunk1d - 1) / kChunk1d;
     p.nwarps = B * p.chunks;
     p.coeffs_out = coeffs;
-    p.final_pass = k + 1 == np;
+    p.final_pass = tail || k + 1 == np;
     p.in = k == 0 ? static_cast<const void*>(d) : static_cast<const void*>(ws + pl->ws_off[k - 1]);
     p.in_pitch = k == 0 ? n : pitch4(p.nin);
     p.out = p.final_pass ? nullptr : static_cast<void*>(ws + pl->ws_off[k]);
     p.out_pitch = p.final_pass ? 0 : pitch4(p.nin >> ps.Lp);
     FHWT_CUDA(launch_ana1d(p, k > 0, s), "ana1d launch");
+    if (tail) break;
   }
   return FHWT_OK;
 }
@@ -763,9 +782,12 @@ fhwt_status run_syn1d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
   }
   if (small1d_ok(pl, coeffs, dR)) return run_small1d(pl, coeffs, dR, s, false);
   const size_t np = pl->passes.size();
+  const int tail = tail1d(pl);
   for (size_t kk = np; kk-- > 0;) {
+    if (tail && kk > 0) continue;   // the coarse levels run inside the fine pass (syn1d_tail)
     const Pass ps = pl->passes[kk];
     Haar1dParams p{};
+    p.tail = tail;
     p.n = n;
     p.nin = n >> ps.g0;
     p.batch = B;

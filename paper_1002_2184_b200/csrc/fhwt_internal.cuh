@@ -114,6 +114,8 @@ struct Haar1dParams {
   int64_t nwarps;
   int Lp, g0;
   int final_pass;        // analysis: approx goes to coeffs; synthesis: output is d_R
+  int tail;              // > 0 (first pass, Lp = 10, chunks | 8): levels 11..10+tail run inside the
+                         // CTA (its 8 warps hold whole signals) instead of a second pass
 };
 
 // launchers (return cudaError_t of the launch)

@@ -105,12 +105,43 @@ struct Ana1dCtx {
   }
 };
 
+// Coarse levels 11..10+T of the signals a CTA holds whole (p.tail = T; chunks = 1024-sample chunks
+// per signal divides the CTA's 8 warps): thread s < 8 / chunks takes signal s of the CTA from the
+// chunks' fp64 LL10 values in shared memory.  Same operations, in the same order, as the fp64
+// second pass (ana1d_kernel<double>): bitwise equal results.
+__device__ __forceinline__ void ana1d_tail(const Haar1dParams& p, const double* ll10, int64_t cta_w0) {
+  const int per = int(p.chunks), nsig = (kThreads1d / 32) / per;
+  const int s = threadIdx.x;
+  if (s >= nsig) return;
+  const int64_t b = cta_w0 / per + s;
+  float* crow = p.coeffs_out + b * p.n;
+  double v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = k < per ? ll10[s * per + k] : 0.0;
+  int m = per;
+#pragma unroll
+  for (int t = 1; t <= 3; ++t) {
+    if (t > p.tail) break;
+    const int j = 10 + t;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (2 * k + 1 >= m) break;
+      const double e = v[2 * k], o = v[2 * k + 1];
+      stg_stream1(crow + (p.n >> j) + k, float((e - o) * kS64));
+      v[k] = (e + o) * kS64;
+    }
+    m >>= 1;
+  }
+  for (int k = 0; k < m; ++k) stg_stream1(crow + k, float(v[k]));
+}
+
 template <typename TIn>
 __global__ void __launch_bounds__(kThreads1d) ana1d_kernel(const __grid_constant__ Haar1dParams p) {
   using T1 = TIn;  // levels 1..3; levels >= 4 are fp64
+  __shared__ double tail_ll[kThreads1d / 32];
   const int lane = threadIdx.x & 31;
   const int64_t w = int64_t(blockIdx.x) * (kThreads1d / 32) + (threadIdx.x >> 5);
-  if (w >= p.nwarps) return;  // warp-uniform
+  if (w >= p.nwarps) return;  // warp-uniform (with p.tail, nwarps is a multiple of the CTA's warps)
   Ana1dCtx ctx;
   ctx.p = &p;
   ctx.b = w / p.chunks;
@@ -227,6 +258,14 @@ __global__ void __launch_bounds__(kThreads1d) ana1d_kernel(const __grid_constant
     if (act) ctx.put_detail(j, i, (v - pv) * kS64);
     v = a;
     if (j == Lp) {
+      if constexpr (sizeof(TIn) == 4) {
+        if (p.tail > 0) {   // Lp = 10: lane 0 holds the chunk's LL10
+          if (lane == 0) tail_ll[threadIdx.x >> 5] = a;
+          __syncthreads();
+          ana1d_tail(p, tail_ll, int64_t(blockIdx.x) * (kThreads1d / 32));
+          return;
+        }
+      }
       if (act) ctx.put_approx(i, a);
       return;
     }
@@ -247,10 +286,38 @@ struct Syn1dCtx {
   }
 };
 
+// Inverse of ana1d_tail: thread s rebuilds the fp32 LL10 values of signal s of the CTA from a_J and
+// the details of levels J..11 (same operations as the fp32 coarse pass of syn1d_kernel).
+__device__ __forceinline__ void syn1d_tail(const Haar1dParams& p, float* ll10, int64_t cta_w0) {
+  const int per = int(p.chunks), nsig = (kThreads1d / 32) / per;
+  const int s = threadIdx.x;
+  if (s >= nsig) return;
+  const int64_t b = cta_w0 / per + s;
+  const float* crow = p.coeffs_in + b * p.n;
+  float v[8];
+  int m = per >> p.tail;
+  for (int k = 0; k < m; ++k) v[k] = crow[k];
+#pragma unroll
+  for (int t = 3; t >= 1; --t) {
+    if (t > p.tail) continue;
+    const int j = 10 + t;
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+      if (k >= m) continue;
+      const float a = v[k], d = crow[(p.n >> j) + k];
+      v[2 * k] = (a + d) * kS32;
+      v[2 * k + 1] = (a - d) * kS32;
+    }
+    m <<= 1;
+  }
+  for (int k = 0; k < per; ++k) ll10[s * per + k] = v[k];
+}
+
 __global__ void __launch_bounds__(kThreads1d) syn1d_kernel(const __grid_constant__ Haar1dParams p) {
+  __shared__ float tail_ll[kThreads1d / 32];
   const int lane = threadIdx.x & 31;
   const int64_t w = int64_t(blockIdx.x) * (kThreads1d / 32) + (threadIdx.x >> 5);
-  if (w >= p.nwarps) return;
+  if (w >= p.nwarps) return;   // with p.tail, nwarps is a multiple of the CTA's warps
   Syn1dCtx ctx;
   ctx.p = &p;
   ctx.b = w / p.chunks;
@@ -297,7 +364,14 @@ __global__ void __launch_bounds__(kThreads1d) syn1d_kernel(const __grid_constant
 #pragma unroll
   for (int t = 0; t < 5; ++t) dh[t] = (Lp >= 6 + t) ? ctx.ld(ctx.detail(6 + t), lane >> (t + 1), 6 + t) : 0.f;
 
-  auto lda = [&](int i) -> float { return i < (ctx.m >> Lp) ? ldg_stream1(ap + i) : 0.f; };
+  if (p.tail > 0) {   // Lp = 10: this chunk's LL10 comes from the CTA's coarse levels
+    syn1d_tail(p, tail_ll, int64_t(blockIdx.x) * (kThreads1d / 32));
+    __syncthreads();
+  }
+  auto lda = [&](int i) -> float {
+    if (p.tail > 0) return tail_ll[threadIdx.x >> 5];
+    return i < (ctx.m >> Lp) ? ldg_stream1(ap + i) : 0.f;
+  };
 
   // ---- coarse levels
   float a2[8];

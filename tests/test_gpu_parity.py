@@ -446,6 +446,24 @@ def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
     assert_close(host(outs[0][1]), x, x, 2, what=f"variants round trip L={levels}")
 
 
+@pytest.mark.parametrize("batch,n,levels", [(16, 2048, 11), (8, 4096, 12), (8, 4096, 11), (4, 8192, 13),
+                                             (4, 8192, 12), (6, 4096, 12), (3, 4096, 12), (1, 8192, 13)])
+def test_1d_coarse_levels_inside_the_cta(monkeypatch, batch, n, levels):
+    """Levels > 10 of 2048-8192-sample signals run inside the first-pass CTA (its warps hold whole
+    signals) when the batch fills whole CTAs, else as a second pass (3 x 4096): oracle parity and
+    bitwise equality with the two-pass path (FHWT_1D_TAIL=0)."""
+    x = datagen.uniform((batch, n), seed=n + levels + batch, lo=-1.0, hi=1.0)
+    check_1d(x, levels)
+    xd = dev(x)
+    c = fhwt.analyze_1d(xd, levels)
+    r = fhwt.synthesize_1d(c, levels)
+    monkeypatch.setenv("FHWT_1D_TAIL", "0")
+    c0 = fhwt.analyze_1d(xd, levels)
+    r0 = fhwt.synthesize_1d(c, levels)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c0) and torch.equal(r, r0)
+
+
 def test_cuda_graph_capture_of_cooperative_launches():
     """L = 7 runs each direction as one cooperative launch (grid barrier before/after the coarse
     levels); captured in a CUDA graph, replay reproduces the eager results bitwise."""
