@@ -467,6 +467,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     if (!in64 && p.TR == 8 && p.TC == 256 && env_int("FHWT_TR8_TC128", 1) != 0) p.TC = 128;   // see tr8_tc
     p.clamp_rows = p.Hin % p.TR != 0;
     p.tiles_r = (p.Hin + p.TR - 1) / p.TR;
+    p.row_pad = int(p.tiles_r * p.TR - p.Hin);
     p.tiles_c = (p.Win + p.TC - 1) / p.TC;
     p.ntiles = B * p.tiles_r * p.tiles_c;
     p.final_pass = final_pass;
@@ -520,7 +521,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     const size_t smem = off + 12 * size_t(p.stages);   // mbarriers + stage-release counters
     // FHWT_ANA_FUSED=3: the fused2 path with a dedicated 9th tail warp (ana2d_fused3_kernel)
     const bool fused3 = fast_ok && p.fused == 3 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 && p.mask_mode == 0 &&
-                        p.aligned_levels >= ps.Lp && !p.clamp_last;
+                        p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows;
     const int vmode = fused3 ? 5 : 0;
     const int fast = fast_ok ? (vmode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;

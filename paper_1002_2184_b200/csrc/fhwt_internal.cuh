@@ -45,6 +45,7 @@ struct Ana2dParams {
   int aligned_levels;    // levels j with even band offsets (unchecked 8-B stores): 1..aligned_levels
   int clamp_last;        // ragged width: the last column tile starts at Win - TC (see tile_col0)
   int clamp_rows;        // Hin % TR != 0: the last row tile starts at Hin - TR (see tile_row0)
+  int row_pad;           // clamp_rows: tiles_r * TR - Hin (rows the last tile moves up)
   int fused;             // 32 x 256 fast tiles, LP >= 3: levels 2+3 and 4+5 fused (FHWT_ANA_FUSED, default 1)
   int tail;              // > 0: after the tiles, a grid barrier and levels 6..5+tail of the fp64 LL5
                          // hand-off in the same (cooperative) launch (ana_coarse); 0: none

@@ -213,33 +213,36 @@ __device__ __forceinline__ void ana_tile(const Ana2dParams& p, const TIn* stage,
 // Loads input tile `t` into a stage: TR one-row TMA boxes issued by the 32 lanes of warp 0.
 // (Measured on B200, tools/membench: 32 one-row boxes stream at 6.9 TB/s where one 32-row box
 // of the same bytes stops at 6.1 TB/s.)  Must be called by all of warp 0.
+template <bool CLAMPR>
 __device__ __forceinline__ void ana_issue_tile(const Ana2dParams& p, const CUtensorMap* map, unsigned char* dst,
                                                uint64_t* bar, int64_t t, uint32_t bytes, uint32_t row_bytes,
                                                uint64_t pol) {
   const int lane = threadIdx.x & 31;
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
-  int64_t grow = rt * p.TR;   // first row in the (batch * Hin)-row tensor
-  if (p.clamp_rows) {
-    const int64_t b = rt / p.tiles_r;
-    grow = b * p.Hin + tile_row0(p, rt - b * p.tiles_r);
-  }
+  // first row in the (batch * Hin)-row tensor (< 2^31: the host splits larger batches).  With
+  // clamp_rows every image's last row tile moves up by row_pad = tiles_r * TR - Hin, so the row is
+  // rt * TR - row_pad * (b + last) = rt * TR - row_pad * ((rt + 1) / tiles_r).  Compile-time
+  // (CLAMPR): any clamp arithmetic in this issue path cost the unclamped analysis 2-4 %.
+  int grow = int(rt) * p.TR;
+  if constexpr (CLAMPR) grow -= p.row_pad * int((uint32_t(rt) + 1u) / uint32_t(p.tiles_r));
   if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
   __syncwarp();
   if (p.row_boxes) {
     if (lane == 0) {
       if (p.l2hint)
         for (int r = 0; r < p.TR; ++r)
-          tma_load_2d(dst + r * row_bytes, map, int(tile_col0(p, ct)), int(grow + r), bar, pol);
+          tma_load_2d(dst + r * row_bytes, map, int(tile_col0(p, ct)), grow + r, bar, pol);
       else
         for (int r = 0; r < p.TR; ++r)
-          tma_load_2d_nohint(dst + r * row_bytes, map, int(tile_col0(p, ct)), int(grow + r), bar);
+          tma_load_2d_nohint(dst + r * row_bytes, map, int(tile_col0(p, ct)), grow + r, bar);
     }
   } else if (lane == 0) {
-    tma_load_2d(dst, map, int(tile_col0(p, ct)), int(grow), bar, pol);
+    tma_load_2d(dst, map, int(tile_col0(p, ct)), grow, bar, pol);
   }
 }
 
 // Re-arms stage s of the TMA ring with the CTA's tile `next` (warp 0; no-op past the end).
+template <bool CLAMPR>
 struct Refill {
   const Ana2dParams* p;
   const CUtensorMap* map;
@@ -250,7 +253,7 @@ struct Refill {
   uint64_t pol;   // must be warp-uniform (computed by every thread): a divergent cache-hint operand
                   // makes each TMA issue a waterfall loop (analysis 6.57 -> 6.15 TB/s)
   __device__ __forceinline__ void operator()() const {
-    if (threadIdx.x < 32 && next < p->ntiles) ana_issue_tile(*p, map, dst, bar, next, bytes, row_bytes, pol);
+    if (threadIdx.x < 32 && next < p->ntiles) ana_issue_tile<CLAMPR>(*p, map, dst, bar, next, bytes, row_bytes, pol);
   }
 };
 
@@ -258,9 +261,9 @@ struct Refill {
 // time, so every index is a shift/constant and levels g >= 4 are fp64 by construction.
 // FULL: a full tile with 8-B aligned band rows (no masks); else stores are masked at the image's
 // right edge (TMA zero-fills the columns past it) and checked for alignment (odd band offsets).
-template <int J, int LP, int TRF, int TCF, bool FULL = true>
+template <int J, int LP, int TRF, int TCF, bool FULL = true, typename RF>
 __device__ __forceinline__ void ana_fast_step(const Ana2dParams& p, const void* src, unsigned char* smem, int64_t b,
-                                              int64_t row0, int64_t col0, const Refill& refill) {
+                                              int64_t row0, int64_t col0, const RF& refill) {
   constexpr int R = TRF >> (J - 1), C = TCF >> (J - 1);
   constexpr bool src64 = J - 1 >= kFirstF64Level;
   constexpr bool cmp64 = J >= kFirstF64Level;
@@ -333,9 +336,9 @@ __device__ __forceinline__ TB ana_pair(const Ana2dParams& p, const float (&x)[4]
 // each).  Two CTA barriers per tile instead of five, and the levels 4-5 threads overlap the next
 // tile's level 1 (LL1 and LL3 live in different buffers; the next tile's first barrier orders the
 // reuse).  Same arithmetic, same order, as ana_fast_step: outputs are bitwise identical.
-template <int LP>
+template <int LP, typename RF>
 __device__ __forceinline__ void ana_fused_tile(const Ana2dParams& p, const float* stage, unsigned char* smem, int64_t b,
-                                               int64_t row0, int64_t col0, const Refill& refill) {
+                                               int64_t row0, int64_t col0, const RF& refill) {
   static_assert(LP >= 3 && LP <= 5, "fused path covers 3..5 levels");
   float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]);   // 16 x 128
   float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);   // 4 x 32
@@ -515,8 +518,9 @@ __device__ __forceinline__ void ana_level5_pair(const Ana2dParams& p, const doub
   }
 }
 
+template <typename RF>
 __device__ __forceinline__ void ana_fused3_tile(const Ana2dParams& p, const float* stage, unsigned char* smem, int64_t b,
-                                                int64_t row0, int64_t col0, int it, const Refill& refill) {
+                                                int64_t row0, int64_t col0, int it, const RF& refill) {
   float* ll2 = reinterpret_cast<float*>(smem + p.p_off[1]) + (it & 1) * 512;                  // 8 x 64
   double* ll4 = reinterpret_cast<double*>(smem + p.p_off[1] + 4096) + (it & 1) * 32;          // 2 x 16
   const int tid = threadIdx.x;
@@ -566,7 +570,8 @@ __global__ void __launch_bounds__(288, 2) ana2d_fused3_kernel(const __grid_const
   if (tid < 32) {
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
-      if (t < p.ntiles) ana_issue_tile(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, tile_bytes, row_bytes, pol);
+      if (t < p.ntiles)
+        ana_issue_tile<false>(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, tile_bytes, row_bytes, pol);
     }
   }
   int it = 0;
@@ -575,10 +580,10 @@ __global__ void __launch_bounds__(288, 2) ana2d_fused3_kernel(const __grid_const
     mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
-    const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
-                        tile_bytes, row_bytes, pol};
-    ana_fused3_tile(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b,
-                          tile_row0(p, rt - b * p.tiles_r), ct * 256, it, refill);
+    const Refill<false> refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
+                               tile_bytes, row_bytes, pol};
+    ana_fused3_tile(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, (rt - b * p.tiles_r) * 32,
+                    ct * 256, it, refill);
   }
   if (p.tail > 0) {
     cooperative_groups::this_grid().sync();
@@ -588,20 +593,12 @@ __global__ void __launch_bounds__(288, 2) ana2d_fused3_kernel(const __grid_const
   }
 }
 
-template <typename TIn, int LPFAST, int TRF, int TCF>
-__global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads2d,
-                                  LPFAST > 0 ? FHWT_MINB_ANA * kThreads2d / fast_threads(TRF, TCF) : FHWT_MINB_ANA)
-    ana2d_kernel(const __grid_constant__ Ana2dParams p,
-                                                           const __grid_constant__ CUtensorMap in_map) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+// The persistent tile loop of ana2d_kernel; CLAMPR: the last row tile of every image is clamped
+// (p.clamp_rows), a compile-time choice so the unclamped issue path carries no clamp arithmetic.
+template <typename TIn, int LPFAST, int TRF, int TCF, bool CLAMPR>
+__device__ __forceinline__ void ana2d_tiles(const Ana2dParams& p, const CUtensorMap& in_map, unsigned char* smem,
+                                            uint64_t* bars) {
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    prefetch_tmap(&in_map);
-    for (int s = 0; s < p.stages; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
   const uint32_t row_bytes = uint32_t(p.TC) * uint32_t(sizeof(TIn));
   const uint32_t tile_bytes = uint32_t(p.TR) * row_bytes;
   const uint64_t pol = policy_evict_first();   // warp-uniform (see Refill)
@@ -609,7 +606,7 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
       if (t < p.ntiles)
-        ana_issue_tile(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, tile_bytes, row_bytes, pol);
+        ana_issue_tile<CLAMPR>(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, tile_bytes, row_bytes, pol);
     }
   }
   int it = 0;
@@ -618,9 +615,9 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
     mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
-    const int64_t row0 = tile_row0(p, rt - b * p.tiles_r);
-    const Refill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
-                        tile_bytes, row_bytes, pol};
+    const int64_t row0 = CLAMPR ? tile_row0(p, rt - b * p.tiles_r) : (rt - b * p.tiles_r) * p.TR;
+    const Refill<CLAMPR> refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
+                                tile_bytes, row_bytes, pol};
     // mask_mode 1: the last column tile is ragged (masked stores); aligned_levels < LP: the coarse
     // levels' band offsets are odd (alignment-checked stores there).  With clamp_last the last tile
     // instead starts at Win - TC (full, overlapping its neighbour: identical values stored twice).
@@ -655,6 +652,26 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
       refill();
     }
   }
+}
+
+template <typename TIn, int LPFAST, int TRF, int TCF>
+__global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads2d,
+                                  LPFAST > 0 ? FHWT_MINB_ANA * kThreads2d / fast_threads(TRF, TCF) : FHWT_MINB_ANA)
+    ana2d_kernel(const __grid_constant__ Ana2dParams p,
+                                                           const __grid_constant__ CUtensorMap in_map) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    prefetch_tmap(&in_map);
+    for (int s = 0; s < p.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (p.clamp_rows)
+    ana2d_tiles<TIn, LPFAST, TRF, TCF, true>(p, in_map, smem, bars);
+  else
+    ana2d_tiles<TIn, LPFAST, TRF, TCF, false>(p, in_map, smem, bars);
   if constexpr (LPFAST == 5) {
     if (p.tail > 0) {   // cooperative launch: every CTA is resident, so the grid barrier is safe
       cooperative_groups::this_grid().sync();
