@@ -297,8 +297,9 @@ int ring_stages(uint32_t stage_bytes) {
 }
 // Analysis ring depth / CTAs-per-SM cap for the narrower first-pass tiles (tools/sweep128.sh,
 // profiles/r01_generic_shapes.md; GB/s analysis, default occupancy -> table):
-//   32 x 128: 2 CTAs/SM, 2 stages (3 when tiles overlap): 480 x 640 5.5 -> 6.3 TB/s, 1152^2 5.5 -> 6.3,
-//             600 x 800 (overlapping last tile) 5.0 -> 6.0
+//   32 x 128: 2 CTAs/SM, 2 stages (3 when the last column tile overlaps): 480 x 640 5.5 -> 6.3 TB/s,
+//             1152^2 5.5 -> 6.3, 1000 x 1152 (clamped rows) 5.3 -> 6.1, 600 x 800 (clamped
+//             columns: 5.8 at 2 stages, 6.4 at 3) 4.6 -> 6.4
 //   16 x 256: 3 CTAs/SM: 2160 x 3840 5.4 -> 6.3, 720 x 1280 5.3 -> 6.2 (at 2 stages; 4 stages as good)
 //   16 x 128: 4 CTAs/SM, 4 stages: 400 x 544 4.8 -> 6.2
 // 32 x 256 (c4) keeps the occupancy limit (2 CTAs/SM) and 2 stages; 8-row tiles keep the defaults.
@@ -493,7 +494,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     // too many small CTAs per SM (occupancy allows 4-10) streamed 10-25 % slower.
     int cap_ctas = 0, stages = ring_stages(p.stage_bytes);
     if (!in64 && ps.g0 == 0 && env_int("FHWT_ANA_TILE_TABLE", 1) != 0)
-      ana_tile_cfg(p.TR, p.TC, p.Win % p.TC != 0 || p.clamp_rows, &stages, &cap_ctas);
+      ana_tile_cfg(p.TR, p.TC, p.Win % p.TC != 0, &stages, &cap_ctas);
     p.stages = in64 ? 2 : env_int("FHWT_ANA_STAGES", stages);
     size_t pb[2] = {0, 0};
     for (int j = 1; j < ps.Lp; ++j) {
