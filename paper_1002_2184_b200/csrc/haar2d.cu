@@ -346,7 +346,48 @@ __device__ __forceinline__ void ana_fused_tile(const Ana2dParams& p, const float
   __syncthreads();
   refill();
   const int tid = threadIdx.x;
-  if (tid < 128) {   // levels 2 + 3: block (br, bc) of LL1, 4 x 32 blocks
+  if (p.fused == 6) {   // levels 2 + 3 over all 256 threads: two lanes per 4 x 4 LL1 block, level 3
+                        // after a lane-pair shuffle of the LL2 columns
+    const int blk = tid >> 1, h = tid & 1, br = blk >> 5, bc = blk & 31;
+    float x[4][2];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float2 v = *reinterpret_cast<const float2*>(ll1 + (4 * br + r) * 128 + 4 * bc + 2 * h);
+      x[r][0] = v.x; x[r][1] = v.y;
+    }
+    const int64_t W = p.W;
+    float ll[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {   // level 2: rows 2br + i, column 2bc + h of the level-2 bands
+      const float a = x[2 * i][0], bb = x[2 * i][1], c = x[2 * i + 1][0], d = x[2 * i + 1][1];
+      const float s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+      ll[i] = (s1 + s2) * 0.5f;
+      float* pr = p.out + (b * p.H + (row0 >> 2) + 2 * br + i) * W + (col0 >> 2) + 2 * bc + h;
+      const int64_t wg = W >> 2, hgW = (p.H >> 2) * W;
+      stg_stream1(pr + wg, (d1 + d2) * 0.5f);
+      stg_stream1(pr + hgW, (s1 - s2) * 0.5f);
+      stg_stream1(pr + hgW + wg, (d1 - d2) * 0.5f);
+    }
+    const float o0 = __shfl_xor_sync(0xffffffffu, ll[0], 1), o1 = __shfl_xor_sync(0xffffffffu, ll[1], 1);
+    if (h == 0) {   // level 3 on the 2 x 2 LL2 block (same operands and order as ana_pair)
+      const float a = ll[0], bb = o0, c = ll[1], d = o1;
+      const float s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+      float* pr = p.out + (b * p.H + (row0 >> 3) + br) * W + (col0 >> 3) + bc;
+      const int64_t wg = W >> 3, hgW = (p.H >> 3) * W;
+      stg_stream1(pr + wg, (d1 + d2) * 0.5f);
+      stg_stream1(pr + hgW, (s1 - s2) * 0.5f);
+      stg_stream1(pr + hgW + wg, (d1 - d2) * 0.5f);
+      const float l3 = (s1 + s2) * 0.5f;
+      if constexpr (LP > 3) {
+        ll3[br * 32 + bc] = l3;
+      } else if (p.final_pass) {
+        stg_stream1(pr, l3);
+      } else {
+        const int64_t wpitch = ((p.Win >> 3) + 3) & ~int64_t(3);
+        p.ws_out[(b * (p.Hin >> 3) + (row0 >> 3) + br) * wpitch + (col0 >> 3) + bc] = double(l3);
+      }
+    }
+  } else if (tid < 128) {   // levels 2 + 3: block (br, bc) of LL1, 4 x 32 blocks
     const int br = tid >> 5, bc = tid & 31;
     float x[4][4];
 #pragma unroll

@@ -12,7 +12,8 @@ import paper_1002_2184_b200 as fhwt  # noqa: E402
 
 
 def main():
-    x = torch.rand(256, 2048, 2048, device="cuda")
+    B, H, W = (int(v) for v in os.environ.get("SHAPE", "256,2048,2048").split(","))
+    x = torch.rand(B, H, W, device="cuda")
     c = torch.empty_like(x)
     r = torch.empty_like(x)
     base = dict(os.environ)
@@ -21,7 +22,7 @@ def main():
         kv = dict(t.split("=") for t in spec.split(","))
         L = int(kv.pop("L", "5"))
         syn = kv.pop("SYN", "0") == "1"
-        plan = fhwt.Plan2d(2048, 2048, 256, L)
+        plan = fhwt.Plan2d(H, W, B, L)
         ws = torch.empty(max(plan.workspace_bytes, 1), dtype=torch.uint8, device="cuda")
         cases.append((spec, plan, ws, kv, syn))
     times = {c[0]: [] for c in cases}
