@@ -408,9 +408,13 @@ fhwt_status run_small1d(const fhwt_plan_s* pl, const float* in, float* out, cuda
   p.W = int(pl->n);
   p.L = pl->levels;
   const int n = p.W;
-  p.G = std::max(1, std::min<int>(int(std::min<int64_t>(pl->batch, 1 << 20)), env_int("FHWT_SMALL1D_CHUNK", 8192) / n));
+  // Chunk size and ring depth per direction (tools/sweep_small1d.sh, GB/s for n = 256 / 512 / 128):
+  // analysis 16 KB chunks x 3 stages (5544 / 5435 / 6332; 32 KB x 2: 5542 / 5505 / 5616), synthesis
+  // 64 KB chunks x 2 stages (6649 / 6430 / 6517; 32 KB x 2: 5851 / 5629 / 6054).
+  const int chunk = env_int("FHWT_SMALL1D_CHUNK", analysis ? 4096 : 16384);
+  p.G = std::max(1, std::min<int>(int(std::min<int64_t>(pl->batch, 1 << 20)), chunk / n));
   p.nchunks = (pl->batch + p.G - 1) / p.G;
-  p.stages = env_int("FHWT_SMALL_STAGES", 2);
+  p.stages = env_int("FHWT_SMALL_STAGES", analysis ? 3 : 2);
   p.stage_bytes = uint32_t(align_up(size_t(p.G) * n * 4, 1024));
   size_t off = size_t(p.stages) * p.stage_bytes;
   p.off_out = uint32_t(off);
@@ -431,6 +435,7 @@ fhwt_status run_small1d(const fhwt_plan_s* pl, const float* in, float* out, cuda
   int bps = 0;
   FHWT_CUDA(small2d_occupancy(analysis, smem, &bps, true), "small1d occupancy");
   if (bps < 1) return fail(FHWT_ERR_CUDA, "short-signal kernel does not fit (%zu B shared memory)", smem);
+  if (const int cap = env_int("FHWT_SMALL_CTAS", 0)) bps = std::min(bps, cap);   // sweep knob
   const int64_t grid = std::min<int64_t>(p.nchunks, int64_t(bps) * di.sms);
   FHWT_CUDA(launch_small2d(p, analysis, int(grid), smem, s, true), "small1d launch");
   return FHWT_OK;
