@@ -13,7 +13,9 @@ import oracle as o  # noqa: E402
 import paper_1002_2184_b200 as fhwt  # noqa: E402
 
 KNOBS = [{}, {"FHWT_ANA_FUSED": "0"}, {"FHWT_ANA_FUSED": "3"}, {"FHWT_SYN_MODE": "2"}, {"FHWT_SYN_MODE": "0"},
-         {"FHWT_COOP": "0"}, {"FHWT_CLAMP_LAST": "0"}, {"FHWT_SMALL_IMAGES": "0"}, {"FHWT_SMALL_SIGNALS": "0"}]
+         {"FHWT_COOP": "0"}, {"FHWT_CLAMP_LAST": "0"}, {"FHWT_SMALL_IMAGES": "0"}, {"FHWT_SMALL_SIGNALS": "0"},
+         {"FHWT_CLAMP_ROWS": "0"}, {"FHWT_TC256_CLAMP": "0"}, {"FHWT_SYN_SHIFT": "0"}, {"FHWT_1D_TAIL": "0"},
+         {"FHWT_ANA_TILE_TABLE": "0", "FHWT_SYN_TILE_TABLE": "0"}, {"FHWT_ANA_FUSED": "6"}, {"FHWT_ANA_FUSED": "1"}]
 
 
 def main():
@@ -51,6 +53,10 @@ def main():
             blk = 1 << J
             nn = blk * int(rng.integers(1, max(2, (1 << 16) // blk)))
             b = int(rng.integers(1, 40))
+            if rng.random() < 0.2:   # full decompositions of 2048-8192 samples (levels inside the CTA)
+                nn = int(rng.choice([2048, 4096, 8192]))
+                J = int(rng.integers(11, nn.bit_length()))
+                b = 8 * int(rng.integers(1, 5)) if rng.random() < 0.7 else int(rng.integers(1, 12))
             while nn * b > 1 << 21:
                 b = max(1, b // 2)
                 if b == 1:
