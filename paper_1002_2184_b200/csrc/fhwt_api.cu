@@ -320,8 +320,13 @@ void ana_tile_cfg(int tr, int tc, bool overlap, int* stages, int* cap_ctas) {
 // (tools/sweep_syn128.sh; GB/s synthesis, default -> table): 32 x 128 at 2 stages, 3 CTAs/SM:
 // 480 x 640 5.3 -> 5.8, 600 x 800 5.0 -> 6.1, 1152^2 5.4 -> 5.8; 16 x 128 at 4 stages, 4 CTAs/SM:
 // 400 x 544 5.2 -> 5.7.
-void syn_tile_cfg(int tr, int tc, int* stages, int* cap_ctas) {
-  if (tr == 32 && tc == 128) {
+void syn_tile_cfg(int mode, int tr, int tc, int* stages, int* cap_ctas) {
+  if ((mode == 3 || mode == 6) && tr == 32 && tc == 128) {   // warp-decoupled kernel, 4 warps per CTA
+    *stages = 2;
+    *cap_ctas = 3;
+  } else if (mode != 2) {
+    return;
+  } else if (tr == 32 && tc == 128) {
     *stages = 2;
     *cap_ctas = 3;
   } else if (tr == 16 && tc == 128) {
@@ -604,7 +609,13 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     // whose band blocks do not all start 16-B aligned (W >> j odd or 2 mod 4, or the clamped last
     // tile's Win - 256 >> j): every box starts at the aligned column below and is 4 columns wider.
     bool shifted = false;
-    if (ps.g0 == 0 && !coop && p.TR == 32 && p.TC == 256 && p.Win > p.TC && W % 4 == 0 &&
+    // 32 x 128 tiles on the warp kernel too, for LP <= 3 and widths without an overlapping last tile
+    // (tools/sweep_syn_warp128.sh, 2 stages x 3 CTAs/SM vs cp.async: 480 x 640 L=3 5866 -> 6314,
+    // 1152^2 5844 -> 6305, 768 x 896 5886 -> 6305, 1000 x 1152 5938 -> 6167; but 600 x 800
+    // (clamped) 6097 -> 5588, 480 x 640 L=4 6363 -> 5478, L=5 6074 -> 4878)
+    const bool warp128 = env_int("FHWT_SYN_WARP128", ps.Lp <= 3 && p.Win % 128 == 0 ? 1 : 0) != 0;
+    if (ps.g0 == 0 && !coop && p.TR == 32 && (p.TC == 256 || (p.TC == 128 && warp128)) && p.Win > p.TC &&
+        W % 4 == 0 &&
         env_int("FHWT_SYN_SHIFT", 1) != 0 && env_int("FHWT_SYN_MODE", 3) == 3) {
       bool al = (W >> 1) % 2 == 0;
       for (int j = 1; j <= ps.Lp; ++j)
@@ -670,7 +681,8 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       // B200 (tools/sweep_syn.py): cp.async 6.10 TB/s, TMA boxes 5.86 (register LDG of level 1: 5.19).
       int mode = full ? env_int("FHWT_SYN_MODE", 3) : 0;
       if (mode != 0 && mode != 3) mode = 2;
-      if (mode == 3 && !(p.TR == 32 && p.TC == 256)) mode = 2;   // warp-decoupled variant: 32 x 256 tiles only
+      // warp-decoupled variant: 32 x 256 and 32 x 128 tiles (one warp per 32 columns)
+      if (mode == 3 && !(p.TR == 32 && (p.TC == 256 || (p.TC == 128 && warp128)))) mode = 2;
       if (shifted) mode = 6;
       // stage layout: LL box, then per level j three boxes (128-B aligned: TMA destinations need it;
       // with cp.async a 16-B packing would admit a 3rd CTA/SM, which measured slower: 5.54 vs 6.10 TB/s)
@@ -694,7 +706,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       p.stage_bytes = uint32_t(align_up(off, 1024));
       // 2 stages for 32 x 256 tiles; the cp.async variant's narrower tiles from a measured table
       int syn_stages = syn_ring_stages(p.stage_bytes), syn_cap = 0;
-      if (mode == 2 && env_int("FHWT_SYN_TILE_TABLE", 1) != 0) syn_tile_cfg(p.TR, p.TC, &syn_stages, &syn_cap);
+      if (env_int("FHWT_SYN_TILE_TABLE", 1) != 0) syn_tile_cfg(mode, p.TR, p.TC, &syn_stages, &syn_cap);
       p.stages = env_int("FHWT_SYN_STAGES", syn_stages);
       size_t pb[2] = {0, 0};
       for (int j = 2; j <= ps.Lp; ++j) {
@@ -704,7 +716,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       off = size_t(p.stages) * p.stage_bytes;
       p.p_off[0] = uint32_t(off);
       if (mode == 3 || mode == 6) {
-        off = align_up(off + size_t(kThreads2d / 32) * kSynScratchBytes, 128);
+        off = align_up(off + size_t(p.TC / 32) * kSynScratchBytes, 128);
         p.p_off[1] = p.p_off[0];
       } else {
         off = align_up(off + pb[0], 128);

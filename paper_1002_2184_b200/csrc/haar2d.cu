@@ -972,11 +972,11 @@ __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const 
   }
 }
 
-template <int J, bool SHIFT, bool LLSHIFT>
+template <int J, bool SHIFT, bool LLSHIFT, int TCF>
 __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float* __restrict__ ll, int llp,
                                                const unsigned char* stage, int warp, float* __restrict__ dst,
                                                int64_t b, int64_t row0, int64_t colw, int64_t col0) {
-  constexpr int R = 32 >> J, C = 32 >> J, BP = (256 >> J) + (SHIFT ? 4 : 0);
+  constexpr int R = 32 >> J, C = 32 >> J, BP = (TCF >> J) + (SHIFT ? 4 : 0);
   constexpr int V = C >= 2 ? 2 : 1, UPR = C / V, NU = R * UPR, OC = 2 * C;
   int co = (32 * warp) >> J, coh = co;
   if constexpr (SHIFT) {   // see syn_issue_tile_lane<true>
@@ -1025,21 +1025,23 @@ __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float
   }
 }
 
-template <int J, int LP, bool SHIFT>
+template <int J, int LP, bool SHIFT, int TCF>
 __device__ __forceinline__ void warp_syn_steps(const Syn2dParams& p, const float* ll, int llp,
                                                const unsigned char* stage, int warp, WarpScratch* sc, int64_t b,
                                                int64_t row0, int64_t colw, int64_t col0) {
   float* dst = J == 5 ? reinterpret_cast<float*>(sc->ll4) : J == 4 ? sc->ll3 : J == 3 ? sc->ll2 : sc->ll1;
-  warp_syn_level<J, SHIFT, SHIFT && J == LP>(p, ll, llp, stage, warp, dst, b, row0, colw, col0);
+  warp_syn_level<J, SHIFT, SHIFT && J == LP, TCF>(p, ll, llp, stage, warp, dst, b, row0, colw, col0);
   if constexpr (J > 1) {
     __syncwarp();
-    warp_syn_steps<J - 1, LP, SHIFT>(p, dst, 2 * (32 >> J), stage, warp, sc, b, row0, colw, col0);
+    warp_syn_steps<J - 1, LP, SHIFT, TCF>(p, dst, 2 * (32 >> J), stage, warp, sc, b, row0, colw, col0);
   }
 }
 
-template <int LP, bool SHIFT = false>
-__global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(const __grid_constant__ Syn2dParams p,
+// TCF: tile columns, 256 (8 warps) or 128 (4 warps); each warp owns a 32-column slice.
+template <int LP, bool SHIFT = false, int TCF = 256>
+__global__ void __launch_bounds__(TCF, FHWT_MINB_SYN * 256 / TCF) syn2d_warp_kernel(const __grid_constant__ Syn2dParams p,
                                                                 const __grid_constant__ TmaMaps2d maps) {
+  constexpr unsigned NW = TCF / 32;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
   unsigned* cnt = reinterpret_cast<unsigned*>(smem + p.bar_off + 8 * p.stages);
@@ -1055,7 +1057,7 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(c
     fence_mbar_init();
   }
   __syncthreads();
-  if constexpr (LP == 5 && !SHIFT) {
+  if constexpr (LP == 5 && !SHIFT && TCF == 256) {
     if (p.head > 0) {   // cooperative launch: coarse levels -> fp32 LL5 hand-off, then a grid barrier
       if (p.head == 1) syn_coarse<1>(p);
       else if (p.head == 2) syn_coarse<2>(p);
@@ -1075,17 +1077,17 @@ __global__ void __launch_bounds__(kThreads2d, FHWT_MINB_SYN) syn2d_warp_kernel(c
   for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
     const int s = it % p.stages;
     mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
-    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256, p.clamp_rows ? p.Hin - 32 : -1);
+    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, TCF, p.clamp_rows ? p.Hin - 32 : -1);
     const unsigned char* stage = smem + s * p.stage_bytes;
-    const int64_t col0 = tile_col0(p, xy.col0 / 256 + p.ct0);
+    const int64_t col0 = tile_col0(p, xy.col0 / TCF + p.ct0);
     const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> LP) +
                       (SHIFT ? int((col0 >> LP) & 3) : 0);
-    warp_syn_steps<LP, LP, SHIFT>(p, ll, (256 >> LP) + (SHIFT ? 4 : 0), stage, warp, sc, xy.b, xy.row0,
-                                  col0 + 32 * warp, col0);
+    warp_syn_steps<LP, LP, SHIFT, TCF>(p, ll, (TCF >> LP) + (SHIFT ? 4 : 0), stage, warp, sc, xy.b, xy.row0,
+                                       col0 + 32 * warp, col0);
     __syncwarp();
-    if (lane == 0) {   // stage release: the 8th warp through level 1 refills it
+    if (lane == 0) {   // stage release: the last warp through level 1 refills it
       __threadfence_block();
-      if ((atomicAdd(&cnt[s], 1u) & 7u) == 7u) {
+      if ((atomicAdd(&cnt[s], 1u) & (NW - 1)) == NW - 1) {
         const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
         if (nt < p.ntiles) syn_issue_tile_lane<SHIFT>(p, maps, smem + s * p.stage_bytes, &bars[s], nt, pol);
       }
@@ -1333,6 +1335,14 @@ template <int LP>
 struct SynWS {
   static const void* get() { return (const void*)syn2d_warp_kernel<LP, true>; }
 };
+template <int LP>
+struct SynW128 {
+  static const void* get() { return (const void*)syn2d_warp_kernel<LP, false, 128>; }
+};
+template <int LP>
+struct SynWS128 {
+  static const void* get() { return (const void*)syn2d_warp_kernel<LP, true, 128>; }
+};
 
 static const void* ana2d_fn(bool in_f64, int fast) {
   if (in_f64) return (const void*)ana2d_kernel<double, 0, 0, 0>;
@@ -1344,8 +1354,9 @@ static const void* ana2d_fn(bool in_f64, int fast) {
 static const void* syn2d_fn(int fast) {
   if (fast == 0) return (const void*)syn2d_kernel<0, 0, 0, 0>;
   const int mode = (fast >> 24) & 0xff;
-  if (mode == 3) return warp_fn<SynW>(fast & 15);
-  if (mode == 6) return warp_fn<SynWS>(fast & 15);
+  const bool narrow = ((fast >> 4) & 0xfff) == 128;
+  if (mode == 3) return narrow ? warp_fn<SynW128>(fast & 15) : warp_fn<SynW>(fast & 15);
+  if (mode == 6) return narrow ? warp_fn<SynWS128>(fast & 15) : warp_fn<SynWS>(fast & 15);
   return mode == 2 ? by_geometry<SynF2>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15)
                    : by_geometry<SynF0>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15);
 }
@@ -1359,7 +1370,7 @@ int ana2d_threads(int fast) {
 }
 int syn2d_threads(int fast) {
   const int mode = (fast >> 24) & 0xff;
-  return (mode == 3 || mode == 6) ? kThreads2d : fast_threads_rt(fast);
+  return (mode == 3 || mode == 6) ? ((fast >> 4) & 0xfff) : fast_threads_rt(fast);   // one warp per 32 columns
 }
 
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm) {

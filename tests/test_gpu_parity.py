@@ -531,6 +531,27 @@ def test_shifted_synthesis_boxes(monkeypatch, b, h, w, levels):
     assert torch.equal(r, r0)
 
 
+@pytest.mark.parametrize("b,h,w,levels,env", [
+    (2, 64, 640, 3, {}), (1, 96, 1152, 2, {}), (3, 32, 384, 1, {}), (1, 1000, 1152, 3, {}),
+    (1, 64, 800, 3, {"FHWT_SYN_WARP128": "1"}), (2, 64, 640, 5, {"FHWT_SYN_WARP128": "1"}),
+    (2, 64, 640, 4, {"FHWT_SYN_WARP128": "1"}), (1, 64, 1000, 3, {"FHWT_SYN_WARP128": "1", "FHWT_SYN_TC": "128"})])
+def test_warp_synthesis_128_column_tiles(monkeypatch, b, h, w, levels, env):
+    """The warp-decoupled synthesis on 32 x 128 tiles (4 warps per CTA; default for L <= 3 and
+    w % 128 == 0, forced elsewhere, incl. clamped and shifted boxes): oracle parity and bitwise
+    equality with the cp.async variant (FHWT_SYN_WARP128=0)."""
+    x = datagen.uniform((b, h, w), seed=7 * h + w + levels, lo=-1.0, hi=1.0)
+    c32 = o.analyze_2d(x, levels).astype(np.float32)
+    cd = dev(c32)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    r = fhwt.synthesize_2d(cd, levels)
+    assert_close(host(r), o.synthesize_2d(c32, levels), x, 2, what=f"warp128 {h}x{w} L={levels}")
+    monkeypatch.setenv("FHWT_SYN_WARP128", "0")
+    r0 = fhwt.synthesize_2d(cd, levels)
+    torch.cuda.synchronize()
+    assert torch.equal(r, r0)
+
+
 @pytest.mark.parametrize("b,h,w,levels", [(2, 1000, 1000, 3), (1, 1080, 1920, 3), (2, 720, 1280, 4), (1, 600, 800, 3),
                                           (3, 1000, 512, 1), (1, 1040, 512, 4), (2, 232, 256, 3), (2, 1000, 3000, 2),
                                           (1, 256, 3968, 5), (2, 64, 1408, 3)])
