@@ -944,12 +944,13 @@ __device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMa
 // SHIFT: band blocks that do not start 16-B aligned (W >> g or the clamped last tile's column
 // offset not a multiple of 4): every box starts at the aligned column at or below the block and is 4
 // columns wider (box_pitch = (TC >> j) + 4); the compute phase adds the shift (column & 3).
-template <bool SHIFT = false>
+template <bool SHIFT = false, bool CLAMPR = true>
 __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* base,
                                                     uint64_t* bar, int64_t t, uint64_t pol) {
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
   const int64_t b = rt / p.tiles_r;
-  const int64_t row0 = tile_row0(p, rt - b * p.tiles_r), col0 = tile_col0(p, ct + p.ct0);
+  const int64_t row0 = CLAMPR ? tile_row0(p, rt - b * p.tiles_r) : (rt - b * p.tiles_r) * p.TR;
+  const int64_t col0 = tile_col0(p, ct + p.ct0);
   constexpr int64_t AL = SHIFT ? ~int64_t(3) : ~int64_t(0);
   mbar_arrive_expect_tx(bar, p.tx_bytes);
   const int L = p.Lp;
@@ -1037,15 +1038,49 @@ __device__ __forceinline__ void warp_syn_steps(const Syn2dParams& p, const float
   }
 }
 
+// The persistent tile loop of syn2d_warp_kernel; CLAMPR (p.clamp_rows) is compile-time so the
+// unclamped issue path carries no clamp arithmetic (as in ana2d_tiles).
+template <int LP, bool SHIFT, int TCF, bool CLAMPR>
+__device__ __forceinline__ void syn2d_warp_tiles(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* smem,
+                                                 uint64_t* bars, unsigned* cnt, WarpScratch* sc) {
+  constexpr unsigned NW = TCF / 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t pol = policy_evict_first();
+  if (tid == 0)
+    for (int s = 0; s < p.stages; ++s) {
+      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
+      if (t < p.ntiles) syn_issue_tile_lane<SHIFT, CLAMPR>(p, maps, smem + s * p.stage_bytes, &bars[s], t, pol);
+    }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+    const int s = it % p.stages;
+    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, TCF, CLAMPR ? p.Hin - 32 : -1);
+    const unsigned char* stage = smem + s * p.stage_bytes;
+    const int64_t col0 = tile_col0(p, xy.col0 / TCF + p.ct0);
+    const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> LP) +
+                      (SHIFT ? int((col0 >> LP) & 3) : 0);
+    warp_syn_steps<LP, LP, SHIFT, TCF>(p, ll, (TCF >> LP) + (SHIFT ? 4 : 0), stage, warp, sc, xy.b, xy.row0,
+                                       col0 + 32 * warp, col0);
+    __syncwarp();
+    if (lane == 0) {   // stage release: the last warp through level 1 refills it
+      __threadfence_block();
+      if ((atomicAdd(&cnt[s], 1u) & (NW - 1)) == NW - 1) {
+        const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
+        if (nt < p.ntiles) syn_issue_tile_lane<SHIFT, CLAMPR>(p, maps, smem + s * p.stage_bytes, &bars[s], nt, pol);
+      }
+    }
+  }
+}
+
 // TCF: tile columns, 256 (8 warps) or 128 (4 warps); each warp owns a 32-column slice.
 template <int LP, bool SHIFT = false, int TCF = 256>
 __global__ void __launch_bounds__(TCF, FHWT_MINB_SYN * 256 / TCF) syn2d_warp_kernel(const __grid_constant__ Syn2dParams p,
                                                                 const __grid_constant__ TmaMaps2d maps) {
-  constexpr unsigned NW = TCF / 32;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
   unsigned* cnt = reinterpret_cast<unsigned*>(smem + p.bar_off + 8 * p.stages);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
   WarpScratch* sc = reinterpret_cast<WarpScratch*>(smem + p.p_off[0] + warp * kSynScratchBytes);
   if (tid == 0) {
     for (int j = 1; j <= LP; ++j) prefetch_tmap(&maps.level[j]);
@@ -1067,32 +1102,10 @@ __global__ void __launch_bounds__(TCF, FHWT_MINB_SYN * 256 / TCF) syn2d_warp_ker
       fence_proxy_async_global();
     }
   }
-  const uint64_t pol = policy_evict_first();
-  if (tid == 0)
-    for (int s = 0; s < p.stages; ++s) {
-      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
-      if (t < p.ntiles) syn_issue_tile_lane<SHIFT>(p, maps, smem + s * p.stage_bytes, &bars[s], t, pol);
-    }
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
-    const int s = it % p.stages;
-    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
-    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, TCF, p.clamp_rows ? p.Hin - 32 : -1);
-    const unsigned char* stage = smem + s * p.stage_bytes;
-    const int64_t col0 = tile_col0(p, xy.col0 / TCF + p.ct0);
-    const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> LP) +
-                      (SHIFT ? int((col0 >> LP) & 3) : 0);
-    warp_syn_steps<LP, LP, SHIFT, TCF>(p, ll, (TCF >> LP) + (SHIFT ? 4 : 0), stage, warp, sc, xy.b, xy.row0,
-                                       col0 + 32 * warp, col0);
-    __syncwarp();
-    if (lane == 0) {   // stage release: the last warp through level 1 refills it
-      __threadfence_block();
-      if ((atomicAdd(&cnt[s], 1u) & (NW - 1)) == NW - 1) {
-        const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
-        if (nt < p.ntiles) syn_issue_tile_lane<SHIFT>(p, maps, smem + s * p.stage_bytes, &bars[s], nt, pol);
-      }
-    }
-  }
+  if (p.clamp_rows)
+    syn2d_warp_tiles<LP, SHIFT, TCF, true>(p, maps, smem, bars, cnt, sc);
+  else
+    syn2d_warp_tiles<LP, SHIFT, TCF, false>(p, maps, smem, bars, cnt, sc);
 }
 
 template <int N>
