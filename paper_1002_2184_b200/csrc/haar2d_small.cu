@@ -52,14 +52,33 @@ __device__ __forceinline__ void issue_chunk(const Small2dParams& p, const float*
 // One analysis level j of g images: source LL_{j-1} (per image h x w, pitch sp, image stride ss),
 // bands to the output chunk O (Mallat layout, pitch W), LL_j to dst (compact per image) or, at the
 // last level, to O.
-template <typename TS, typename TD>
-__device__ __forceinline__ void small_ana_level(const Small2dParams& p, const TS* src, int sp, int ss, float* O,
-                                                TD* dst, int g, int h, int w, bool last) {
+// (image, row, column) of unit u = (gi * h2 + r) * w2 + c.  POW2: h2 and w2 are powers of two
+// (shifts instead of integer divisions, which dominated these kernels' issue slots).
+template <bool POW2>
+__device__ __forceinline__ void unit_rc(uint32_t u, uint32_t per, uint32_t w2, uint32_t& gi, uint32_t& rem,
+                                        uint32_t& r, uint32_t& c) {
+  if constexpr (POW2) {
+    gi = u >> (__ffs(per) - 1);
+    rem = u & (per - 1);
+    r = rem >> (__ffs(w2) - 1);
+    c = rem & (w2 - 1);
+  } else {
+    gi = u / per;
+    rem = u - gi * per;
+    r = rem / w2;
+    c = rem - r * w2;
+  }
+}
+
+template <typename TS, typename TD, bool POW2>
+__device__ __forceinline__ void small_ana_level_t(const Small2dParams& p, const TS* src, int sp, int ss, float* O,
+                                                  TD* dst, int g, int h, int w, bool last) {
   const int h2 = h >> 1, w2 = w >> 1;
   const uint32_t per = uint32_t(h2 * w2), total = per * uint32_t(g);
   const int imgO = p.H * p.W;
   for (uint32_t u = threadIdx.x; u < total; u += blockDim.x) {
-    const uint32_t gi = u / per, rem = u - gi * per, r = rem / uint32_t(w2), c = rem - r * uint32_t(w2);
+    uint32_t gi, rem, r, c;
+    unit_rc<POW2>(u, per, uint32_t(w2), gi, rem, r, c);
     const TS* s = src + gi * ss + (2 * r) * sp + 2 * c;   // even offset: pairs load as one 8/16-B word
     TD a, bb, cc, d;
     if constexpr (sizeof(TS) == 4) {
@@ -80,6 +99,17 @@ __device__ __forceinline__ void small_ana_level(const Small2dParams& p, const TS
     else
       dst[gi * per + rem] = ll;
   }
+}
+
+template <typename TS, typename TD>
+__device__ __forceinline__ void small_ana_level(const Small2dParams& p, const TS* src, int sp, int ss, float* O,
+                                                TD* dst, int g, int h, int w, bool last) {
+  // measured (tools/generic_shapes.py SMALL=1): shifts win for L >= 4 (32x32 L=5 4.77 -> 5.74 TB/s,
+  // 64x64 L=6 4.48 -> 6.14, 16x64 L=4 5.20 -> 5.43) and lose at L = 3 (64x64 5.71 -> 5.48)
+  if (p.L >= 4 && ((h & (h - 1)) | (w & (w - 1))) == 0)
+    small_ana_level_t<TS, TD, true>(p, src, sp, ss, O, dst, g, h, w, last);
+  else
+    small_ana_level_t<TS, TD, false>(p, src, sp, ss, O, dst, g, h, w, last);
 }
 
 __global__ void __launch_bounds__(256, 2) ana2d_small_kernel(const __grid_constant__ Small2dParams p) {
@@ -143,13 +173,15 @@ __global__ void __launch_bounds__(256, 2) ana2d_small_kernel(const __grid_consta
 // One synthesis level j of g images: LL_j (per image h2 x w2 at pitch lp, image stride ls) and the
 // level-j bands of the coefficient chunk S (pitch W) -> LL_{j-1} (h x w) into dst (pitch dp,
 // image stride ds).
-__device__ __forceinline__ void small_syn_level(const Small2dParams& p, const float* ll, int lp, int ls,
-                                                const float* S, float* dst, int dp, int ds, int g, int h, int w) {
+template <bool POW2>
+__device__ __forceinline__ void small_syn_level_t(const Small2dParams& p, const float* ll, int lp, int ls,
+                                                  const float* S, float* dst, int dp, int ds, int g, int h, int w) {
   const int h2 = h >> 1, w2 = w >> 1;
   const uint32_t per = uint32_t(h2 * w2), total = per * uint32_t(g);
   const int imgS = p.H * p.W;
   for (uint32_t u = threadIdx.x; u < total; u += blockDim.x) {
-    const uint32_t gi = u / per, rem = u - gi * per, r = rem / uint32_t(w2), c = rem - r * uint32_t(w2);
+    uint32_t gi, rem, r, c;
+    unit_rc<POW2>(u, per, uint32_t(w2), gi, rem, r, c);
     const float* b = S + gi * imgS + r * p.W + c;
     const float vll = ll[gi * ls + r * lp + c], vhl = b[w2], vlh = b[h2 * p.W], vhh = b[h2 * p.W + w2];
     const float s = vll + vlh, t = vhl + vhh, s2 = vll - vlh, t2 = vhl - vhh;
@@ -157,6 +189,16 @@ __device__ __forceinline__ void small_syn_level(const Small2dParams& p, const fl
     *reinterpret_cast<float2*>(o) = make_float2((s + t) * 0.5f, (s - t) * 0.5f);
     *reinterpret_cast<float2*>(o + dp) = make_float2((s2 + t2) * 0.5f, (s2 - t2) * 0.5f);
   }
+}
+
+__device__ __forceinline__ void small_syn_level(const Small2dParams& p, const float* ll, int lp, int ls,
+                                                const float* S, float* dst, int dp, int ds, int g, int h, int w) {
+  // measured: shifts win for L >= 5 (32x32 L=5 5.23 -> 5.79 TB/s, 64x64 L=6 5.01 -> 5.83) and lose
+  // at L = 3, 4 (64x64 L=3 6.20 -> 5.66, 16x64 L=4 5.76 -> 5.60)
+  if (p.L >= 5 && ((h & (h - 1)) | (w & (w - 1))) == 0)
+    small_syn_level_t<true>(p, ll, lp, ls, S, dst, dp, ds, g, h, w);
+  else
+    small_syn_level_t<false>(p, ll, lp, ls, S, dst, dp, ds, g, h, w);
 }
 
 __global__ void __launch_bounds__(256, 2) syn2d_small_kernel(const __grid_constant__ Small2dParams p) {
