@@ -492,10 +492,9 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     // are request-bound and slower than multi-row boxes.
     p.l2hint = env_int("FHWT_ANA_L2HINT", 1);
     // Level-pair fusion (32 x 256 tiles), measured: LP = 5 levels 2+3 by 128 threads and 4+5 by 8 (+3 %);
-    // LP = 3 levels 2+3 by all 256 threads, two lanes per 4 x 4 LL1 block (mode 6: 6.19-6.24 ->
-    // 6.41-6.45 TB/s; at LP = 5 mode 6 loses, 6.13 -> 5.89, since the levels 4+5 warp then also
-    // carries levels 2+3); LP = 4 level by level.
-    p.fused = env_int("FHWT_ANA_FUSED", ps.Lp == 5 ? 1 : ps.Lp == 3 ? 6 : 0);
+    // LP = 3, 4 level by level.  Mode 6 (LP = 3: levels 2+3 by all 256 threads, two lanes per 4 x 4
+    // LL1 block) won on two boxes (+1-3.5 %) and lost on two (-7 %, 2048^2 images): kept as an option.
+    p.fused = env_int("FHWT_ANA_FUSED", ps.Lp == 5 ? 1 : 0);
     p.row_boxes = size_t(p.TC) * (in64 ? 8 : 4) >= 1024 && (size_t(p.TC) * (in64 ? 8 : 4)) % 128 == 0;
     FHWT_TRY(encode_2d(&map, in, in64, p.Win, B * p.Hin, in_pitch, p.TC, p.row_boxes ? 1 : p.TR));
     // shared memory layout: stages | P[0] | P[1] | barriers

@@ -213,12 +213,23 @@ __device__ __forceinline__ void ana_tile(const Ana2dParams& p, const TIn* stage,
 // Loads input tile `t` into a stage: TR one-row TMA boxes issued by the 32 lanes of warp 0.
 // (Measured on B200, tools/membench: 32 one-row boxes stream at 6.9 TB/s where one 32-row box
 // of the same bytes stops at 6.1 TB/s.)  Must be called by all of warp 0.
-template <bool CLAMPR>
+// U32: 32-bit tile decode (tile counts are < 2^31: a tile holds >= 1024 pixels and a buffer < 2^36).
+// Measured on two boxes (interleaved processes): +1.0-1.6 % for LP = 4, 5 (c4, c5) and -1.5 % for
+// LP = 3, so the fast variants choose it by LP (the issue path is sensitive to every instruction).
+template <bool CLAMPR, bool U32 = false>
 __device__ __forceinline__ void ana_issue_tile(const Ana2dParams& p, const CUtensorMap* map, unsigned char* dst,
                                                uint64_t* bar, int64_t t, uint32_t bytes, uint32_t row_bytes,
                                                uint64_t pol) {
   const int lane = threadIdx.x & 31;
-  const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+  int64_t rt, ct;
+  if constexpr (U32) {
+    const uint32_t r32 = uint32_t(t) / uint32_t(p.tiles_c);
+    rt = r32;
+    ct = uint32_t(t) - r32 * uint32_t(p.tiles_c);
+  } else {
+    rt = t / p.tiles_c;
+    ct = t - rt * p.tiles_c;
+  }
   // first row in the (batch * Hin)-row tensor (< 2^31: the host splits larger batches).  With
   // clamp_rows every image's last row tile moves up by row_pad = tiles_r * TR - Hin, so the row is
   // rt * TR - row_pad * (b + last) = rt * TR - row_pad * ((rt + 1) / tiles_r).  Compile-time
@@ -242,7 +253,7 @@ __device__ __forceinline__ void ana_issue_tile(const Ana2dParams& p, const CUten
 }
 
 // Re-arms stage s of the TMA ring with the CTA's tile `next` (warp 0; no-op past the end).
-template <bool CLAMPR>
+template <bool CLAMPR, bool U32 = false>
 struct Refill {
   const Ana2dParams* p;
   const CUtensorMap* map;
@@ -253,7 +264,8 @@ struct Refill {
   uint64_t pol;   // must be warp-uniform (computed by every thread): a divergent cache-hint operand
                   // makes each TMA issue a waterfall loop (analysis 6.57 -> 6.15 TB/s)
   __device__ __forceinline__ void operator()() const {
-    if (threadIdx.x < 32 && next < p->ntiles) ana_issue_tile<CLAMPR>(*p, map, dst, bar, next, bytes, row_bytes, pol);
+    if (threadIdx.x < 32 && next < p->ntiles)
+      ana_issue_tile<CLAMPR, U32>(*p, map, dst, bar, next, bytes, row_bytes, pol);
   }
 };
 
@@ -647,7 +659,8 @@ __device__ __forceinline__ void ana2d_tiles(const Ana2dParams& p, const CUtensor
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
       if (t < p.ntiles)
-        ana_issue_tile<CLAMPR>(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, tile_bytes, row_bytes, pol);
+        ana_issue_tile<CLAMPR, (LPFAST >= 4)>(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, tile_bytes,
+                                              row_bytes, pol);
     }
   }
   int it = 0;
@@ -657,8 +670,8 @@ __device__ __forceinline__ void ana2d_tiles(const Ana2dParams& p, const CUtensor
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
     const int64_t row0 = CLAMPR ? tile_row0(p, rt - b * p.tiles_r) : (rt - b * p.tiles_r) * p.TR;
-    const Refill<CLAMPR> refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x,
-                                tile_bytes, row_bytes, pol};
+    const Refill<CLAMPR, (LPFAST >= 4)> refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s],
+                                               tile + int64_t(p.stages) * gridDim.x, tile_bytes, row_bytes, pol};
     // mask_mode 1: the last column tile is ragged (masked stores); aligned_levels < LP: the coarse
     // levels' band offsets are odd (alignment-checked stores there).  With clamp_last the last tile
     // instead starts at Win - TC (full, overlapping its neighbour: identical values stored twice).
