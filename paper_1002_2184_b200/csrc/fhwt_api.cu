@@ -547,6 +547,9 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     const bool coop = k == 0 && np == 2 && pl->passes[1].Lp <= 3 && ps.Lp == 5 && fast_ok &&
                       env_int("FHWT_COOP", 1) != 0;
     p.tail = coop ? pl->passes[1].Lp : 0;
+    if (env_int("FHWT_DEBUG_LAUNCH", 0))
+      std::fprintf(stderr, "[fhwt] ana2d fused %d tile %dx%d LP %d stages %d smem %zu B ctas/SM %d grid %lld\n",
+                   p.fused, p.TR, p.TC, ps.Lp, p.stages, smem, bps, (long long)grid);
     FHWT_CUDA(launch_ana2d(p, map, in64, fast, int(grid), smem, s), "ana2d launch");
     if (coop) break;
   }
@@ -737,6 +740,9 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
         p.head = pl->passes[1].Lp;
         p.ll_ws_out = reinterpret_cast<float*>(ws + pl->ws_off[0]);
       }
+      if (env_int("FHWT_DEBUG_LAUNCH", 0))
+        std::fprintf(stderr, "[fhwt] syn2d mode %d tile %dx%d LP %d stages %d smem %zu B ctas/SM %d grid %lld\n", mode,
+                     p.TR, p.TC, ps.Lp, p.stages, smem, bps, (long long)grid);
       FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
     }
   }
