@@ -736,6 +736,12 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
   }
 }
 
+__device__ __forceinline__ unsigned atom_add_acq_rel_cta(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
+
 // ---------------------------------------------------------- shared helpers of the warp kernels
 // Per-warp LL scratch of the warp-decoupled synthesis kernel (syn2d_warp_kernel).
 struct WarpScratch {
@@ -1077,8 +1083,11 @@ __device__ __forceinline__ void syn2d_warp_tiles(const Syn2dParams& p, const Tma
                                        col0 + 32 * warp, col0);
     __syncwarp();
     if (lane == 0) {   // stage release: the last warp through level 1 refills it
-      __threadfence_block();
-      if ((atomicAdd(&cnt[s], 1u) & (NW - 1)) == NW - 1) {
+      // acq_rel RMW on the stage counter (after __syncwarp): releases this warp's reads of the
+      // stage, and the last warp acquires every other warp's before it re-arms the stage for TMA
+      // (the same release/acquire hand-off as an "empty" mbarrier; a full fence here, MEMBAR.SC,
+      // showed in 2.6 % of the stall samples)
+      if ((atom_add_acq_rel_cta(&cnt[s], 1u) & (NW - 1)) == NW - 1) {
         const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
         if (nt < p.ntiles) syn_issue_tile_lane<SHIFT, CLAMPR>(p, maps, smem + s * p.stage_bytes, &bars[s], nt, pol);
       }
