@@ -313,7 +313,10 @@ __device__ __forceinline__ void syn1d_tail(const Haar1dParams& p, float* ll10, i
   for (int k = 0; k < per; ++k) ll10[s * per + k] = v[k];
 }
 
-__global__ void __launch_bounds__(kThreads1d) syn1d_kernel(const __grid_constant__ Haar1dParams p) {
+// At least 3 resident CTAs (768 threads) per SM: the kernel waits on its chunk's loads (long
+// scoreboard, profiles/r01_sass_hotspots.md), so occupancy is what keeps loads in flight; measured
+// c2 synthesis 6711 -> 6916 GB/s, every 1-D shape +1.5-5 % (alternating processes).
+__global__ void __launch_bounds__(kThreads1d, 3) syn1d_kernel(const __grid_constant__ Haar1dParams p) {
   __shared__ float tail_ll[kThreads1d / 32];
   const int lane = threadIdx.x & 31;
   const int64_t w = int64_t(blockIdx.x) * (kThreads1d / 32) + (threadIdx.x >> 5);
