@@ -4,7 +4,10 @@
 
 One step = one multi-level analysis (fhwt_plan_analyze) + one synthesis (fhwt_plan_synthesize)
 of the whole workload, inputs resident in HBM.  Default workload: BASELINE configs[3] (c4,
-256 images 2048x2048 fp32, L=5) — the largest single-GPU 2-D config, sharded by image index.
+256 images 2048x2048 fp32, L=5) — the largest single-GPU 2-D config.  At N GPUs the fixed
+workload is split (strong scaling, as BASELINE configs[3]/[4] say): c4 256/N images per rank, c2
+4096/N signals, c5 32768/N-row bands + the coarsest-LL all-gather.  The per-rank step is replayed
+as CUDA graphs.
 Algorithmic bytes per step = 16 B/sample (fp32 read + write, twice).  A JSON line is printed by
 rank 0.  ``--impl reference`` times the fp64 CPU oracle on the same workload instead.
 
@@ -30,11 +33,11 @@ METRIC = "Fast Haar DWT+IDWT GB/s and Gsamples/s vs B200 HBM roofline at 1/2/4/8
 FALLBACK_HBM_GBS = 6650.0
 
 WORKLOADS = {
-    "c2": dict(kind="1d", n=65536, batch=4096, levels=10, shard="signal", scaling="weak",
+    "c2": dict(kind="1d", n=65536, batch=4096, levels=10, shard="signal",
                desc="c2: 1-D batched 4096 x 65536 fp32 (3 sinusoids + N(0,0.1)), J=10, DWT+IDWT"),
-    "c4": dict(kind="2d", h=2048, w=2048, batch=256, levels=5, shard="image", scaling="weak",
+    "c4": dict(kind="2d", h=2048, w=2048, batch=256, levels=5, shard="image",
                desc="c4: 2-D batched 256 x 2048x2048 fp32 (G()/255 images), L=5, DWT+IDWT"),
-    "c5": dict(kind="2d", h=32768, w=32768, batch=1, levels=8, shard="rowband", scaling="strong",
+    "c5": dict(kind="2d", h=32768, w=32768, batch=1, levels=8, shard="rowband",
                desc="c5: 2-D 32768x32768 fp32 (G()/255), L=8, row bands + NCCL LL all-gather, DWT+IDWT"),
 }
 
@@ -79,81 +82,112 @@ def ncu_traffic(workload, kernel):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock, board power and clock-event (throttle) reasons sampled through NVML every ~2 ms by
+    a background thread while the timed region runs (the c4 region is ~55 ms: nvidia-smi's 200 ms
+    polling saw 3 mostly idle samples in round 1).  Falls back to nvidia-smi if NVML is missing."""
+    PERIOD_S = 0.002
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
     def __init__(self, device_index):
         self.dev = device_index
-        self.proc = None
-        self.path = None
+        self.samples = []
+        self.max_mhz = None
+        self._stop = None
+        self._th = None
+        self.err = None
 
     def __enter__(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
-                 "-i", str(self.dev)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-            time.sleep(0.3)
-        except Exception:  # noqa: BLE001
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.dev]) if vis and vis.split(",")[0].isdigit() else self.dev
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001
+            self.err = f"NVML unavailable: {e}"
+            return self
+        self._stop = threading.Event()
+
+        def poll():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                         nv.nvmlDeviceGetPowerUsage(h) / 1e3,
+                                         nv.nvmlDeviceGetCurrentClocksEventReasons(h),
+                                         nv.nvmlDeviceGetUtilizationRates(h).gpu))
+                except Exception:  # noqa: BLE001
+                    pass
+                time.sleep(self.PERIOD_S)
+
+        self._th = threading.Thread(target=poll, daemon=True)
+        self._th.start()
+        time.sleep(0.01)
         return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            time.sleep(0.25)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:  # noqa: BLE001
-                self.proc.kill()
+        if self._th is not None:
+            self._stop.set()
+            self._th.join(timeout=5)
 
     def summary(self):
-        if self.proc is None or not self.path:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = []
-        with open(self.path) as f:
-            for line in f:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
-                    rows.append(parts)
-        os.unlink(self.path)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[1]) for r in rows]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
-                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit()),
-                "samples": len(rows)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [self.err or "no samples"]}
+        loaded = [s for s in self.samples if s[3] > 0] or self.samples
+        reasons = 0
+        for s in loaded:
+            reasons |= int(s[2])
+        return {"sm_mhz": statistics.median(s[0] for s in loaded), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(v for k, v in self.REASONS.items() if reasons & k),
+                "power_w_max": max(s[1] for s in loaded), "samples": len(self.samples),
+                "samples_under_load": sum(1 for s in self.samples if s[3] > 0),
+                "sampler": f"NVML every {self.PERIOD_S * 1e3:.0f} ms during the timed region"}
 
 
 # ---------------------------------------------------------------------------------- data
-def make_inputs(name, cfg, ws, rank):
+def shard_of(cfg, ws, rank, weak=False):
+    """This rank's share of the workload: c4 / c2 split their fixed global batch
+    of images / signals into contiguous blocks of batch/N units (strong scaling; --weak gives every
+    rank a full batch instead), c5 splits its rows into 2^L-aligned bands of h/N rows."""
+    from paper_1002_2184_b200 import dist as fdist
+    if cfg["shard"] in ("image", "signal"):
+        if weak:
+            first, count = fdist.unit_shard(cfg["batch"], rank)
+            global_batch = cfg["batch"] * ws
+        else:
+            first, count = fdist.unit_range(cfg["batch"], ws, rank)
+            global_batch = cfg["batch"]
+        return {"kind": "units", "first": first, "count": count, "global_batch": global_batch,
+                "scaling": "weak" if weak else "strong"}
+    r0, r1 = fdist.row_band(cfg["h"], ws, rank, cfg["levels"])
+    return {"kind": "rows", "r0": r0, "r1": r1, "global_batch": 1, "scaling": "strong"}
+
+
+def make_inputs(name, cfg, ws, rank, weak=False):
     """This rank's shard of the workload as a pinned host array (datagen, seeded per unit)."""
     import torch
 
     import datagen
-    from paper_1002_2184_b200 import dist as fdist
-    if cfg["shard"] in ("image", "signal"):   # weak scaling: rank r owns units [r*B, (r+1)*B)
-        first, count = fdist.unit_shard(cfg["batch"], rank)
+    sh = shard_of(cfg, ws, rank, weak)
+    if sh["kind"] == "units":
+        first, count = sh["first"], sh["count"]
         shape = (count, cfg["h"], cfg["w"]) if cfg["shard"] == "image" else (count, cfg["n"])
         host = torch.empty(shape, dtype=torch.float32).pin_memory()
         datagen.generate("c4" if cfg["shard"] == "image" else "c2", first=first, count=count, size=shape[-1],
                          out=host.numpy())
         units = f"{cfg['shard']}s [{first}, {first + count})"
-    else:                                    # strong scaling: rank r owns a 2^L-aligned row band
-        r0, r1 = fdist.row_band(cfg["h"], ws, rank, cfg["levels"])
+    else:
+        r0, r1 = sh["r0"], sh["r1"]
         host = torch.empty((r1 - r0, cfg["w"]), dtype=torch.float32).pin_memory()
         datagen.generate("c5", r0=r0, r1=r1, size=cfg["h"], out=host.numpy())
         units = f"rows [{r0}, {r1})"
-    return host, units
+    return host, units, sh
 
 
 # ---------------------------------------------------------------------------------- GPU arm
-def measure(name, cfg, args, ws, rank, local, pg):
+def measure(name, cfg, args, ws, rank, local, pg, timed=True):
     import torch
     import torch.distributed as dist
 
@@ -161,76 +195,114 @@ def measure(name, cfg, args, ws, rank, local, pg):
     from paper_1002_2184_b200 import dist as fdist
     dev = torch.device("cuda", local)
     t0 = time.time()
-    host, units = make_inputs(name, cfg, ws, rank)
+    host, units, shard = make_inputs(name, cfg, ws, rank, weak=getattr(args, "weak", False))
     log(f"[rank {rank}] {name}: generated {tuple(host.shape)} ({units}) in {time.time() - t0:.1f}s")
     d = host.to(dev)
     coeffs = torch.empty_like(d)
     rec = torch.empty_like(d)
     L = cfg["levels"]
     if cfg["kind"] == "2d":
-        plan = fhwt.Plan2d(d.shape[-2], d.shape[-1], d.numel() // (d.shape[-2] * d.shape[-1]), L)
+        plan = fhwt.Plan2d(d.shape[-2], d.shape[-1], d.numel() // (d.shape[-2] * d.shape[-1]), L, device=local)
     else:
-        plan = fhwt.Plan1d(d.shape[-1], d.numel() // d.shape[-1], L)
+        plan = fhwt.Plan1d(d.shape[-1], d.numel() // d.shape[-1], L, device=local)
     wsb = torch.empty(max(plan.workspace_bytes, 1), dtype=torch.uint8, device=dev)
-    gather = cfg["shard"] == "rowband" and ws > 1
+    rowband = cfg["shard"] == "rowband"
+    gather = rowband and ws > 1
     p2p = None
-    if cfg["shard"] == "rowband":
+    if rowband:
         ll_rows, ll_cols = d.shape[0] >> L, d.shape[1] >> L
         ll_local = torch.empty((ll_rows, ll_cols), dtype=torch.float32, device=dev)
         ll_all = torch.empty((ll_rows * ws, ll_cols), dtype=torch.float32, device=dev)
         if getattr(args, "ll_gather", "nccl") == "p2p" and dist.is_initialized():
             # pack fused with the all-gather over NVLink peer memory (one kernel + a device barrier)
             p2p = fdist.PeerLLGather(ll_rows, ll_cols, group=pg, device=dev)
-    stream = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)     # c5: LL pack + all-gather, overlapped with the synthesis pass
     ana_done = torch.cuda.Event()
 
-    def step(evs=None):
-        if evs:
-            evs[0].record(stream)
+    def ana():
         plan.analyze(d, out=coeffs, workspace=wsb)
-        if evs:
-            evs[1].record(stream)
-        if cfg["shard"] == "rowband":
-            # Synthesis needs only this band's own coefficients, so the pack (K6)
-            # and the one exchange (NCCL all-gather of the coarsest LL) run on a side stream.
+
+    def rest(stream, mid_evs=None):
+        """Everything after the analysis: (c5) pack + all-gather of the coarsest LL on the side
+        stream — synthesis needs only the band's own coefficients — and synthesis."""
+        if rowband:
             ana_done.record(stream)
             side.wait_event(ana_done)
             with torch.cuda.stream(side):
-                if evs:
-                    evs[4].record(side)
+                if mid_evs:
+                    mid_evs[0].record(side)
                 if p2p is not None:
                     p2p(coeffs, L, stream=side)
                 else:
                     fhwt.pack_ll_2d(coeffs, L, out=ll_local, stream=side)
                     if gather:
                         fdist.gather_coarse_ll(ll_local, group=pg, out=ll_all)
-                if evs:
-                    evs[2].record(side)
-        elif evs:
-            evs[4].record(stream)
-            evs[2].record(stream)
+                if mid_evs:
+                    mid_evs[1].record(side)
         plan.synthesize(coeffs, out=rec, workspace=wsb)
-        if cfg["shard"] == "rowband":
+        if rowband:
             stream.wait_stream(side)      # the step ends when the gathered LL is in place too
-        if evs:
-            evs[3].record(stream)
 
-    for _ in range(args.warmup):
-        step()
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):      # eager warm-up (allocations, TMA descriptors, NCCL setup)
+        ana()
+        rest(stream)
     torch.cuda.synchronize(dev)
-    # properties of this run's own output (not timed)
-    parity = sampled_parity(name, cfg, host, coeffs, rec, rank, ws) if rank == 0 else None
-    if p2p is not None:   # the fused path's result against the plain pack of this rank's band
-        fhwt.pack_ll_2d(coeffs, L, out=ll_local)
-        torch.cuda.synchronize(dev)
-        if rank == 0:
-            parity["gathered_ll"] = dict(check_gathered_ll(p2p.buf, ll_local, rank, ws), path="p2p")
-    elif gather and rank == 0:
-        parity["gathered_ll"] = check_gathered_ll(ll_all, ll_local, rank, ws)
+
+    # The per-rank step as CUDA graphs (one for the analysis, one for the rest), so the K timed
+    # steps replay them back to back; a CUDA event between the two replays times the analysis.
+    # Not capturable: the gloo plumbing backend (host-side gather) and the peer-memory gather.
+    graphs = None
+    graph_note = "eager"
+    n_per_step = None
+    if not getattr(args, "no_graph", False) and p2p is None and not (gather and dist.get_backend(pg) != "nccl"):
+        try:
+            cs = torch.cuda.Stream(dev)
+            cs.wait_stream(stream)
+            g_ana, g_rest = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            n0 = fhwt.launch_count()
+            with torch.cuda.stream(cs):
+                with torch.cuda.graph(g_ana, stream=cs):
+                    ana()
+                with torch.cuda.graph(g_rest, stream=cs):
+                    rest(cs)
+            n_per_step = fhwt.launch_count() - n0
+            stream.wait_stream(cs)
+            for _ in range(2):
+                g_ana.replay()
+                g_rest.replay()
+            torch.cuda.synchronize(dev)
+            graphs = (g_ana, g_rest)
+            graph_note = "CUDA graphs (analysis | pack + gather + synthesis), replayed"
+        except Exception as e:  # noqa: BLE001
+            log(f"[rank {rank}] graph capture failed ({e!r}); timing eager launches")
+            graph_note = f"eager (capture failed: {type(e).__name__})"
+            torch.cuda.synchronize(dev)
+
+    def step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        if graphs:
+            graphs[0].replay()
+        else:
+            ana()
+        if evs:
+            evs[1].record(stream)
+        if graphs:
+            graphs[1].replay()
+        else:
+            rest(stream)
+        if evs:
+            evs[2].record(stream)
+
+    step()
+    torch.cuda.synchronize(dev)
+    # properties of this run's own output (not timed), on every rank
+    checks = run_checks(name, cfg, host, d, coeffs, rec, plan, shard, L, rank, ws, pg, dev,
+                        ll_local if rowband else None, (p2p.buf if p2p is not None else ll_all) if gather else None)
 
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     if ws > 1:
         dist.barrier(group=pg)
     torch.cuda.synchronize(dev)
@@ -243,36 +315,49 @@ def measure(name, cfg, args, ws, rank, local, pg):
             step(evs[k])
         end.record(stream)
         torch.cuda.synchronize(dev)
-    launches = fhwt.launch_count() - n0
+    launches = fhwt.launch_count() - n0 if graphs is None else n_per_step * K
     if ws > 1:
         dist.barrier(group=pg)
     total_ms = start.elapsed_time(end)
+    # the side-stream pack + gather, timed in eager steps outside the timed region (graph replays
+    # cannot hold events on the side stream)
+    mid = []
+    if rowband:
+        for _ in range(min(K, 10)):
+            me = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ana()
+            rest(stream, me)
+            torch.cuda.synchronize(dev)
+            mid.append(me[0].elapsed_time(me[1]))
     sustained = None
-    if getattr(args, "sustained", 0) > 0 and name == args.workload:
-        sustained = measure_sustained(step, stream, local, total_ms / K, args.sustained,
+    if getattr(args, "sustained", 0) > 0 and name == args.workload and timed:
+        def eager_step():   # the variants are chosen per launch (env knobs), so no graph replays here
+            ana()
+            rest(stream)
+        sustained = measure_sustained(eager_step, stream, local, total_ms / K, args.sustained,
                                       16.0 * d.numel() * ws)
-    ana = [e[0].elapsed_time(e[1]) for e in evs]
-    mid = [e[4].elapsed_time(e[2]) for e in evs]      # pack + gather on the side stream
-    syn = [e[1].elapsed_time(e[3]) for e in evs]      # synthesis (+ the gather's tail, if any)
-    vals = [total_ms, statistics.mean(ana), statistics.mean(syn), statistics.mean(mid)]
+    ana_t = [e[0].elapsed_time(e[1]) for e in evs]
+    syn_t = [e[1].elapsed_time(e[2]) for e in evs]      # synthesis (+ the gather's tail, if any)
+    vals = [total_ms, statistics.mean(ana_t), statistics.mean(syn_t), statistics.mean(mid) if mid else 0.0]
     if ws > 1:
         vals = fdist.max_over_ranks(vals, device=dev, group=pg)
     total_ms, ana_ms, syn_ms, mid_ms = vals
     samples_rank = d.numel()
-    samples_all = samples_rank * ws
+    samples_all = samples_rank * ws if shard["scaling"] == "weak" or rowband else fdist_total(cfg, ws, pg, samples_rank, dev)
     ms_step = total_ms / K
     bytes_step = 16.0 * samples_all
     peak, peak_src = measured_peak()
     kern = "analysis" if ana_ms >= syn_ms else "synthesis"
     kern_ms = max(ana_ms, syn_ms)
     achieved = 8.0 * samples_rank / (kern_ms * 1e-3) / 1e9
-    steps_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    steps_ms = [e[0].elapsed_time(e[2]) for e in evs]
 
     def mmm(xs):   # median with min / max (this rank's per-step CUDA-event times, ms)
-        return {"median": statistics.median(xs), "min": min(xs), "max": max(xs)}
+        return {"median": statistics.median(xs), "min": min(xs), "max": max(xs)} if xs else None
 
     res = {
-        "per_step_ms": {"analysis": mmm(ana), "synthesis": mmm(syn), "pack_gather": mmm(mid), "step": mmm(steps_ms)},
+        "per_step_ms": {"analysis": mmm(ana_t), "synthesis": mmm(syn_t), "pack_gather_eager": mmm(mid),
+                        "step": mmm(steps_ms)},
         "gsamples_per_s_analysis": samples_rank / (ana_ms * 1e-3) / 1e9,
         "gsamples_per_s_synthesis": samples_rank / (syn_ms * 1e-3) / 1e9,
         "value": bytes_step / (ms_step * 1e-3) / 1e9,
@@ -282,6 +367,7 @@ def measure(name, cfg, args, ws, rank, local, pg):
         "analysis_gbs": 8.0 * samples_rank / (ana_ms * 1e-3) / 1e9,
         "synthesis_gbs": 8.0 * samples_rank / (syn_ms * 1e-3) / 1e9,
         "gpu_launches": launches,
+        "launch_mode": graph_note,
         "clocks": clk.summary(),
         "roofline": {
             "bound": "hbm", "kernel": KERNEL_NAMES[(cfg["kind"], kern)],
@@ -291,8 +377,10 @@ def measure(name, cfg, args, ws, rank, local, pg):
             "traffic": ncu_traffic(name, kern),
         },
         "samples_per_rank": samples_rank,
+        "samples_all": samples_all,
         "units": units,
-        "parity": parity,
+        "shard": shard,
+        "parity": checks,
         "sustained": sustained,
     }
     del d, coeffs, rec, wsb
@@ -300,10 +388,114 @@ def measure(name, cfg, args, ws, rank, local, pg):
     return res, (plan, host)
 
 
+def fdist_total(cfg, ws, pg, samples_rank, dev):
+    """Strong scaling: the samples all ranks processed (shares can differ by one unit)."""
+    if ws == 1:
+        return samples_rank
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(samples_rank)], dtype=torch.float64,
+                     device=dev if dist.get_backend(pg) == "nccl" else "cpu")
+    dist.all_reduce(t, group=pg)
+    return int(t.item())
+
+
+def run_checks(name, cfg, host, d, coeffs, rec, plan, shard, L, rank, ws, pg, dev, ll_local, ll_gathered):
+    """Properties of this run's own output that hold at any size, on the device, on EVERY rank,
+    reduced to rank 0 (max of errors, min of booleans).  The oracle comparisons live in
+    tests/test_gpu_fullsize.py and tests/test_gpu_parity.py; bench executes oracle/ only in its
+    cpu_baseline and --impl reference legs.
+    * per unit: round trip |d_R - d| / max|d| and the energy defect of the orthonormal transform
+      (fp64 on the device);
+    * P-invariance: the rank's first unit transformed alone (c2 / c4), or each
+      half of the rank's row band transformed on its own (c5), equals bitwise the corresponding
+      coefficients of the rank's batch / band output — so a split into 2N ranks gives the bits of a
+      split into N, and by induction of N = 1;
+    * (c5, N > 1) the all-gathered coarsest LL on this rank against a rank-local reference of every
+      band, 2^L * avg_pool(band, 2^L) in fp64 (each rank's reference all-gathered the same way), and
+      identical on all ranks (checksum min == max)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1002_2184_b200 as fhwt
+    from paper_1002_2184_b200 import dist as fdist
+    rowband = shard["kind"] == "rows"
+    dims = tuple(range(1, host.dim())) if not rowband else (0, 1)
+    rts, ens = [], []
+    n = host.shape[0] if not rowband else 1
+    stepn = max(1, n // 8)
+    for i0 in range(0, n, stepn):   # a few units at a time keeps the fp64 temporaries small
+        sl = slice(i0, min(n, i0 + stepn)) if not rowband else slice(None)
+        x = d[sl].double()
+        scale = x.abs().amax(dim=dims)
+        rts.append(float(((rec[sl].double() - x).abs().amax(dim=dims) / scale).max()))
+        e_in = (x * x).sum(dim=dims)
+        ens.append(float((((coeffs[sl].double() ** 2).sum(dim=dims) - e_in).abs() / e_in).max()))
+        del x
+    torch.cuda.empty_cache()
+    # P-invariance
+    if not rowband:
+        one = (fhwt.analyze_2d(d[:1].contiguous(), L) if cfg["kind"] == "2d" else fhwt.analyze_1d(d[:1].contiguous(), L))
+        p_inv = bool(torch.equal(one, coeffs[:1]))
+        del one
+    else:
+        H, W = d.shape
+        p_inv = True
+        if H % (2 << L) == 0:
+            for r0, r1 in ((0, H // 2), (H // 2, H)):
+                half = fhwt.analyze_2d(d[r0:r1], L)
+                hb = r1 - r0
+                for j in range(1, L + 1):
+                    g0, g1 = fdist.band_rows(r0, r1, j)
+                    hj, wj, bj = H >> j, W >> j, hb >> j
+                    p_inv &= bool(torch.equal(half[:bj, wj:2 * wj], coeffs[g0:g1, wj:2 * wj]))
+                    p_inv &= bool(torch.equal(half[bj:2 * bj, :wj], coeffs[hj + g0:hj + g1, :wj]))
+                    p_inv &= bool(torch.equal(half[bj:2 * bj, wj:2 * wj], coeffs[hj + g0:hj + g1, wj:2 * wj]))
+                p_inv &= bool(torch.equal(half[:hb >> L, :W >> L], coeffs[g0:g1, :W >> L]))
+                del half
+        torch.cuda.empty_cache()
+    out = {"check": "every unit: round trip and energy (fp64 on device); P-invariance; gathered LL (c5, N>1)",
+           "roundtrip_err_rel": max(rts), "energy_defect_rel": max(ens), "tol": 1e-5, "p_invariant": p_inv}
+    if rowband:
+        # the band's own packed LL against 2^L * avg_pool of its input (fp64, rank-local reference)
+        x = d.double()[None, None]
+        ref_local = (torch.nn.functional.avg_pool2d(x, 1 << L) * float(1 << L))[0, 0]
+        scale_local = float(d.abs().max())
+        out["packed_ll_err_rel"] = float((ll_local.double() - ref_local).abs().max()) / scale_local
+        if ll_gathered is not None:
+            nccl = dist.get_backend(pg) == "nccl"
+            dv = dev if nccl else "cpu"
+            ref_all = torch.empty((ws * ref_local.shape[0], ref_local.shape[1]), dtype=torch.float64, device=dv)
+            if nccl:
+                dist.all_gather_into_tensor(ref_all, ref_local.contiguous(), group=pg)
+            else:
+                parts = [torch.empty_like(ref_local.cpu()) for _ in range(ws)]
+                dist.all_gather(parts, ref_local.cpu().contiguous(), group=pg)
+                ref_all.copy_(torch.cat(parts, 0))
+            sc = fdist.max_over_ranks(scale_local, device=dev, group=pg)
+            g = ll_gathered.double().to(dv)
+            err = float((g - ref_all).abs().max()) / sc
+            ck = float(g.sum())
+            out["gathered_ll_err_rel"] = err
+            out["gathered_ll_identical_on_all_ranks"] = (fdist.max_over_ranks(ck, device=dev, group=pg) ==
+                                                         -fdist.max_over_ranks(-ck, device=dev, group=pg))
+        del x, ref_local
+    if ws > 1:   # reduce to rank 0: max of errors, min (AND) of booleans
+        keys = [k for k, v in out.items() if isinstance(v, float)]
+        vals = fdist.max_over_ranks([out[k] for k in keys], device=dev, group=pg)
+        out.update(zip(keys, vals))
+        bkeys = [k for k, v in out.items() if isinstance(v, bool)]
+        bvals = fdist.max_over_ranks([0.0 if out[k] else 1.0 for k in bkeys], device=dev, group=pg)
+        out.update({k: v == 0.0 for k, v in zip(bkeys, bvals)})
+        out["ranks_checked"] = ws
+    return out
+
+
 # Analysis-kernel variants compared under sustained load (DESIGN.md §7, profiles/r01_power_cap.md):
 # the default CTA-synchronous fused kernel is fastest at full clock, the dedicated-tail-warp kernel
 # (FHWT_ANA_FUSED=3, 3 stages) once the board sits at its power cap.
-SUSTAINED_VARIANTS = {"default": {}, "ana_fused3_st3": {"FHWT_ANA_FUSED": "3", "FHWT_ANA_STAGES": "3"}}
+SUSTAINED_VARIANTS = {"default": {},
+                      "ana_fused3_st3": {"FHWT_TUNING": "1", "FHWT_ANA_FUSED": "3", "FHWT_ANA_STAGES": "3"}}
 
 
 def measure_sustained(step, stream, local, ms_per_step, seconds, bytes_per_step):
@@ -362,29 +554,6 @@ def measure_sustained(step, stream, local, ms_per_step, seconds, bytes_per_step)
         if v is not None:
             os.environ[k] = v
     return out
-
-
-def sampled_parity(name, cfg, host, coeffs, rec, rank, ws):
-    """Properties of this run's own output that hold at any size, on the device (the oracle
-    comparisons live in tests/test_gpu_fullsize.py; bench executes oracle/ only in its cpu_baseline
-    and --impl reference legs): per-unit round trip |d_R - d| / max|d| and the relative energy
-    defect of the orthonormal transform, in fp64 over every unit."""
-    import torch
-    dims = tuple(range(1, host.dim())) if cfg["shard"] != "rowband" else (0, 1)
-    rts, ens = [], []
-    n = host.shape[0] if cfg["shard"] != "rowband" else 1
-    step = max(1, n // 8)
-    for i0 in range(0, n, step):   # a few units at a time keeps the fp64 temporaries small
-        sl = slice(i0, min(n, i0 + step)) if cfg["shard"] != "rowband" else slice(None)
-        x = host[sl].to(rec.device).double()
-        scale = x.abs().amax(dim=dims)
-        rts.append(float(((rec[sl].double() - x).abs().amax(dim=dims) / scale).max()))
-        e_in = (x * x).sum(dim=dims)
-        ens.append(float((((coeffs[sl].double() ** 2).sum(dim=dims) - e_in).abs() / e_in).max()))
-        del x
-    torch.cuda.empty_cache()
-    return {"check": "round trip and energy of every unit (fp64 on device)", "roundtrip_err_rel": max(rts),
-            "energy_defect_rel": max(ens), "tol": 1e-5}
 
 
 def measure_direct(name, cfg, d_host, steps=5):
@@ -548,14 +717,6 @@ def measure_lowpass(steps=10):
             "bf16_input": bf16}
 
 
-def check_gathered_ll(ll_all, ll_local, rank, ws):
-    """The all-gathered coarsest LL holds every rank's band in rank order: this rank's slice must
-    equal its own packed LL bitwise (other ranks' values are checked by their own runs and tests)."""
-    rows = ll_local.shape[0]
-    same = bool((ll_all[rank * rows:(rank + 1) * rows] == ll_local).all())
-    return {"rows_per_rank": rows, "ranks": ws, "own_slice_bitwise_equal": same}
-
-
 def measure_e2e(cfg, host, steps):
     """Same metric through the public host-buffer API: every step copies the pinned input H2D, runs
     DWT + IDWT and copies the step's result d_R back D2H (fhwt_roundtrip_*_host; the coefficients
@@ -663,7 +824,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(s["wall_s"] for s in steps),
         "higher_is_better": True,
-        "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "levels": cfg["levels"]},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -692,6 +853,11 @@ def main():
                     help="c5 coarse-LL exchange: NCCL all-gather, or pack + stores into peer symmetric memory")
     ap.add_argument("--sustained", type=float, default=1.5,
                     help="seconds of warm + timed back-to-back steps per analysis variant (0 = skip)")
+    ap.add_argument("--weak", action="store_true",
+                    help="c2 / c4: every rank transforms a full batch (weak scaling) instead of batch/N units")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA graph replays")
+    ap.add_argument("--no-t1", action="store_true",
+                    help="N > 1: skip rank 0's single-GPU run of the whole workload (the T(1) of the self-check)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules; using 3")
@@ -732,9 +898,28 @@ def main():
         e2e = measure_e2e(cfg, host, args.e2e_steps)
         if ws > 1:
             from paper_1002_2184_b200 import dist as fdist
-            e2e["ms_per_step"] = fdist.max_over_ranks(e2e["ms_per_step"], device=torch.device("cuda", local))
-            e2e["value"] = 16.0 * host.numel() * ws / (e2e["ms_per_step"] * 1e-3) / 1e9
+            e2e["ms_per_step"] = fdist.max_over_ranks(e2e["ms_per_step"], device=torch.device("cuda", local), group=pg)
+            e2e["value"] = 16.0 * res["samples_all"] / (e2e["ms_per_step"] * 1e-3) / 1e9
+            e2e["h2d_bytes_per_step"] = e2e["d2h_bytes_per_step"] = 4 * res["samples_all"]
+            e2e["note"] = "every rank round-trips its own shard; bytes are the whole job's"
     del host
+    multi = None
+    if ws > 1:
+        # Self-check of the scaling (the driver computes the official efficiency from its own per-N
+        # runs): rank 0 times the whole workload alone on its GPU, T(1), next to this run's T(N).
+        multi = {"t_n_ms": res["ms_per_step"], "shard_per_rank": res["shard"],
+                 "gather_ms": res["gather_ms"] if cfg["shard"] == "rowband" else None}
+        if not args.no_t1 and not args.weak:
+            if rank == 0:
+                sub = argparse.Namespace(**vars(args))
+                sub.sustained = 0
+                r1, (p1, h1) = measure(args.workload, cfg, sub, 1, 0, local, None, timed=False)
+                del p1, h1
+                multi.update(t1_ms=r1["ms_per_step"], t1_value=r1["value"],
+                             self_check_efficiency=r1["ms_per_step"] / (ws * res["ms_per_step"]),
+                             note="T(1)/(N*T(N)) with T(1) timed by rank 0 alone in this run; "
+                                  "the driver's own per-N runs are authoritative")
+            dist.barrier(group=pg)
     breakdown = {}
     if not args.no_breakdown:
         for other in ("c2", "c5", "c4"):
@@ -749,7 +934,8 @@ def main():
                                                     "gsamples_per_s_analysis", "gsamples_per_s_synthesis",
                                                     "per_step_ms", "roofline", "parity", "gpu_launches", "clocks")}
             breakdown[other]["workload"] = WORKLOADS[other]["desc"]
-            breakdown[other]["scaling"] = WORKLOADS[other]["scaling"]
+            breakdown[other]["scaling"] = r2["shard"]["scaling"]
+            breakdown[other]["launch_mode"] = r2["launch_mode"]
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = time_oracle(args.workload, cfg)
@@ -757,11 +943,13 @@ def main():
         out = {
             "metric": METRIC, "value": res["value"], "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
-            "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": res["shard"]["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["desc"], "levels": cfg["levels"],
-                       "global_batch": (cfg.get("batch", 1) * ws if cfg["shard"] != "rowband" else 1),
+                       "global_batch": res["shard"]["global_batch"],
+                       "per_rank": res["units"],
                        "shape": [cfg.get("h"), cfg.get("w")] if cfg["kind"] == "2d" else [cfg["n"]],
-                       "parallelism": f"dp{ws} ({cfg['shard']} shards)",
+                       "parallelism": f"dp{ws} ({cfg['shard']} shards, {res['shard']['scaling']} scaling)",
+                       "launch": res["launch_mode"],
                        "l2": "no flush: every step streams >= 4 GiB in and out, >> 126 MB L2",
                        "dtype_note": "fp32 I/O and levels 1-3; fp64 butterflies from level 4 (analysis)"},
             "gsamples_per_s": res["gsamples_per_s"],
@@ -774,6 +962,7 @@ def main():
             "gpu_launches": res["gpu_launches"],
             "clocks": res["clocks"],
             "parity": res["parity"],
+            "multi_gpu": multi,
             "workloads": breakdown,
             "direct_form": direct,
             "lowpass_u8": lowpass,

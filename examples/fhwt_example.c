@@ -71,7 +71,7 @@ int main(void) {
   CUDA(cudaMalloc((void**)&dr, bytes));
   CUDA(cudaMemcpy(dd, d, bytes, cudaMemcpyHostToDevice));
   fhwt_plan plan;
-  FHWT(fhwt_plan_2d(&plan, H, W, B, L, NULL));
+  FHWT(fhwt_plan_2d(&plan, H, W, B, L, NULL, 0));
   const size_t wsb = fhwt_plan_workspace_bytes(plan);
   if (wsb) CUDA(cudaMalloc(&ws, wsb));
   FHWT(fhwt_plan_analyze(plan, dd, dc, ws, NULL));
@@ -103,7 +103,7 @@ int main(void) {
   /* 3. validation before any launch */
   const uint64_t launches = fhwt_launch_count();
   fhwt_plan bad;
-  const fhwt_status st = fhwt_plan_2d(&bad, 100, 64, 1, 3, NULL);
+  const fhwt_status st = fhwt_plan_2d(&bad, 100, 64, 1, 3, NULL, -1);
   CHECK(st == FHWT_ERR_INSUFFICIENT_LENGTH, "100 x 64 at L=3 gave %s", fhwt_status_string(st));
   CHECK(fhwt_launch_count() == launches, "a rejected plan launched kernels");
   printf("100 x 64, L=3 rejected: %s (%s)\n", fhwt_status_string(st), fhwt_last_error_message());

@@ -31,6 +31,10 @@
  * from a later call).  fhwt_last_error_message() returns a thread-local description of the
  * last failure.  Non-finite inputs are not scanned; they propagate under IEEE rules.
  *
+ * Environment: the library reads no environment variable unless FHWT_TUNING=1 is set; then the
+ * FHWT_* sweep knobs of DESIGN.md §13b override the measured kernel / tile / ring-depth choices
+ * (bitwise-equal alternatives kept for A/B measurement and tests).
+ *
  * Precision: butterflies of levels 1-3 in fp32, from level 4 on in
  * fp64 (analysis), the hand-off between kernel passes in fp64; outputs rounded once to fp32.
  * Synthesis in fp32.
@@ -86,13 +90,18 @@ uint64_t fhwt_launch_count(void);          /* number of kernels this library has
 typedef struct fhwt_plan_s *fhwt_plan;
 
 /* 1-D: batch signals of n samples, `levels` dyadic levels.  Needs n % 2^levels == 0.
- * Errors: INVALID_ARG (p NULL, n/batch < 0), EMPTY, INVALID_LEVELS, ODD_LENGTH,
- * INSUFFICIENT_LENGTH, UNSUPPORTED_FILTER. */
-fhwt_status fhwt_plan_1d(fhwt_plan *p, int64_t n, int64_t batch, int levels, const fhwt_filter_bank *fb);
+ * device: the CUDA device the plan's calls run on (the library makes it current for the call and
+ * restores the caller's device afterwards; buffers and stream must belong to it), or -1 for the
+ * device that is current at each call.
+ * Errors: INVALID_ARG (p NULL, n/batch < 0, device < -1), EMPTY, INVALID_LEVELS, ODD_LENGTH,
+ * INSUFFICIENT_LENGTH, UNSUPPORTED_FILTER, NO_DEVICE (device >= device count), CUDA. */
+fhwt_status fhwt_plan_1d(fhwt_plan *p, int64_t n, int64_t batch, int levels, const fhwt_filter_bank *fb,
+                         int device);
 
-/* 2-D: batch images of h x w pixels, `levels` separable levels.  Needs h, w % 2^levels == 0. */
+/* 2-D: batch images of h x w pixels, `levels` separable levels.  Needs h, w % 2^levels == 0.
+ * device and errors as fhwt_plan_1d. */
 fhwt_status fhwt_plan_2d(fhwt_plan *p, int64_t h, int64_t w, int64_t batch, int levels,
-                         const fhwt_filter_bank *fb);
+                         const fhwt_filter_bank *fb, int device);
 
 fhwt_status fhwt_plan_destroy(fhwt_plan p);
 
@@ -156,7 +165,7 @@ fhwt_status fhwt_plan_pack_ll_2d(fhwt_plan p, const float *coeffs, float *ll_pac
  * End-to-end DWT + IDWT on HOST buffers (pinned memory recommended): the batch is streamed in
  * chunks of `chunk` images (or signals) through device staging buffers owned by the call, with
  * H2D copy, analysis, synthesis and D2H copies of coeffs (if h_coeffs != NULL) and d_R
- * overlapped across CUDA streams (3 by default; env FHWT_RT_STREAMS, 2..4).  Blocks until the
+ * overlapped across 3 CUDA streams.  Blocks until the
  * results are in host memory.
  * chunk <= 0 picks a default.  Errors as the device entry points, plus CUDA for copy failures. */
 fhwt_status fhwt_roundtrip_2d_host(const float *h_d, float *h_coeffs, float *h_dR, int64_t h, int64_t w,

@@ -24,7 +24,10 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.environ.get("FHWT_LIB") or os.path.join(_HERE, "libfhwt.so")   # FHWT_LIB: tuning sweeps only
+# FHWT_LIB (A/B of two builds in the tuning sweeps) is honoured only with FHWT_TUNING=1, like the
+# library's own FHWT_* knobs.
+lib_path = ((os.environ.get("FHWT_LIB") if os.environ.get("FHWT_TUNING") == "1" else None)
+            or os.path.join(_HERE, "libfhwt.so"))
 
 
 class FhwtError(RuntimeError):
@@ -113,8 +116,8 @@ def lib():
         "fhwt_last_error_message": (ctypes.c_char_p, []),
         "fhwt_version": (c_int, []),
         "fhwt_launch_count": (ctypes.c_uint64, []),
-        "fhwt_plan_1d": (st, [ctypes.POINTER(vp), i64, i64, c_int, ctypes.POINTER(FilterBank)]),
-        "fhwt_plan_2d": (st, [ctypes.POINTER(vp), i64, i64, i64, c_int, ctypes.POINTER(FilterBank)]),
+        "fhwt_plan_1d": (st, [ctypes.POINTER(vp), i64, i64, c_int, ctypes.POINTER(FilterBank), c_int]),
+        "fhwt_plan_2d": (st, [ctypes.POINTER(vp), i64, i64, i64, c_int, ctypes.POINTER(FilterBank), c_int]),
         "fhwt_plan_destroy": (st, [vp]),
         "fhwt_plan_workspace_bytes": (ctypes.c_size_t, [vp]),
         "fhwt_plan_analyze": (st, [vp, vp, vp, vp, vp]),
@@ -218,6 +221,18 @@ def _out_like(x, out):
         return _t().empty_like(x)
     if out.shape != x.shape:
         raise ShapeMismatch(f"out has shape {tuple(out.shape)}, expected {tuple(x.shape)}")
+    if out.device != x.device:
+        raise InvalidArgument(f"out is on {out.device}, input on {x.device}")
+    return out
+
+
+def _out_packed(out, numel, device, what):
+    """A caller-supplied output the kernel fills with `numel` elements: check its size and device
+    before the C ABI writes (an undersized buffer would be an out-of-bounds device write)."""
+    if out.numel() != numel:
+        raise ShapeMismatch(f"{what} has {out.numel()} elements, expected {numel}")
+    if out.device != device:
+        raise InvalidArgument(f"{what} is on {out.device}, expected {device}")
     return out
 
 
@@ -295,6 +310,17 @@ def synthesize_2d(coeffs, levels: int, out=None, stream=None):
     return out
 
 
+def _device(device) -> int:
+    """Plan device argument: None = the device current at each call (-1), else a CUDA index."""
+    if device is None:
+        return -1
+    if hasattr(device, "index"):   # torch.device
+        if device.type != "cuda":
+            raise InvalidArgument(f"plan device must be a CUDA device, got {device}")
+        return -1 if device.index is None else int(device.index)
+    return int(device)
+
+
 class _Plan:
     _kind = 0
 
@@ -308,16 +334,20 @@ class _Plan:
     def workspace_bytes(self) -> int:
         return int(lib().fhwt_plan_workspace_bytes(self._h))
 
-    def _ws(self, like, workspace):
+    def _ws(self, like, workspace, stream):
         import torch
         nb = self.workspace_bytes
         if nb == 0:
             return ctypes.c_void_p(0)
         if workspace is None:
-            ws = getattr(self, "_ws_cache", None)
-            if ws is None or ws.device != like.device:
+            # one cached buffer per (device, stream): calls on different streams may run
+            # concurrently and must not share the pass hand-off region
+            key = (like.get_device(), stream.value)
+            cache = self.__dict__.setdefault("_ws_cache", {})
+            ws = cache.get(key)
+            if ws is None:
                 ws = torch.empty(nb, dtype=torch.uint8, device=like.device)
-                self._ws_cache = ws
+                cache[key] = ws
             workspace = ws
         if workspace.numel() * workspace.element_size() < nb or not workspace.is_cuda:
             raise InvalidArgument(f"workspace must be a CUDA buffer of >= {nb} bytes")
@@ -331,16 +361,18 @@ class _Plan:
         self._check_shape(d)
         out = _out_like(d, out)
         with _guard_device(d):
-            _check(lib().fhwt_plan_analyze(self._h, _dev_f32(d, "d"), _dev_f32(out, "coeffs"), self._ws(d, workspace),
-                                           _stream(stream, d)))
+            st = _stream(stream, d)
+            _check(lib().fhwt_plan_analyze(self._h, _dev_f32(d, "d"), _dev_f32(out, "coeffs"),
+                                           self._ws(d, workspace, st), st))
         return out
 
     def synthesize(self, coeffs, out=None, workspace=None, stream=None):
         self._check_shape(coeffs)
         out = _out_like(coeffs, out)
         with _guard_device(coeffs):
+            st = _stream(stream, coeffs)
             _check(lib().fhwt_plan_synthesize(self._h, _dev_f32(coeffs, "coeffs"), _dev_f32(out, "d_R"),
-                                              self._ws(coeffs, workspace), _stream(stream, coeffs)))
+                                              self._ws(coeffs, workspace, st), st))
         return out
 
 
@@ -348,10 +380,11 @@ class Plan1d(_Plan):
     """fhwt_plan_1d handle: batch signals of n samples, `levels` levels, filter bank (default §II)."""
     _kind = 1
 
-    def __init__(self, n: int, batch: int, levels: int, filter_bank: FilterBank | None = None):
+    def __init__(self, n: int, batch: int, levels: int, filter_bank: FilterBank | None = None,
+                 device: int | None = None):
         h = ctypes.c_void_p()
         _check(lib().fhwt_plan_1d(ctypes.byref(h), int(n), int(batch), int(levels),
-                                  ctypes.byref(filter_bank) if filter_bank is not None else None))
+                                  ctypes.byref(filter_bank) if filter_bank is not None else None, _device(device)))
         self._h = h
         self.n, self.batch, self.levels = int(n), int(batch), int(levels)
         self._tail = (self.n,)
@@ -362,10 +395,11 @@ class Plan2d(_Plan):
     """fhwt_plan_2d handle: batch images of h x w, `levels` separable levels."""
     _kind = 2
 
-    def __init__(self, h: int, w: int, batch: int, levels: int, filter_bank: FilterBank | None = None):
+    def __init__(self, h: int, w: int, batch: int, levels: int, filter_bank: FilterBank | None = None,
+                 device: int | None = None):
         hd = ctypes.c_void_p()
         _check(lib().fhwt_plan_2d(ctypes.byref(hd), int(h), int(w), int(batch), int(levels),
-                                  ctypes.byref(filter_bank) if filter_bank is not None else None))
+                                  ctypes.byref(filter_bank) if filter_bank is not None else None, _device(device)))
         self._h = hd
         self.h, self.w, self.batch, self.levels = int(h), int(w), int(batch), int(levels)
         self._tail = (self.h, self.w)
@@ -378,6 +412,7 @@ class Plan2d(_Plan):
         L = self.levels
         if out is None:
             out = torch.empty((self.batch, self.h >> L, self.w >> L), dtype=torch.float32, device=coeffs.device)
+        _out_packed(out, self.batch * (self.h >> L) * (self.w >> L), coeffs.device, "ll")
         with _guard_device(coeffs):
             _check(lib().fhwt_plan_pack_ll_2d(self._h, _dev_f32(coeffs, "coeffs"), _dev_f32(out, "ll"),
                                               _stream(stream, coeffs)))
@@ -400,6 +435,8 @@ def pack_ll_2d(coeffs, levels: int, out=None, stream=None):
     shape = tuple(coeffs.shape[:-2]) + (h >> levels, w >> levels)
     if out is None:
         out = torch.empty(shape, dtype=coeffs.dtype, device=coeffs.device)
+    if levels >= 1:
+        _out_packed(out, batch * (h >> levels) * (w >> levels), coeffs.device, "ll")
     with _guard_device(coeffs):
         _check(lib().fhwt_pack_ll_2d(_dev_f32(coeffs, "coeffs"), _dev_f32(out, "ll"), h, w, batch, int(levels),
                                      _stream(stream, coeffs)))
@@ -413,12 +450,22 @@ def _host_f32(t, what):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _host_out(out, d, what):
+    """Host outputs of the round trip: the C ABI writes d.numel() floats into them."""
+    if out.shape != d.shape:
+        raise ShapeMismatch(f"{what} has shape {tuple(out.shape)}, expected {tuple(d.shape)}")
+    return out
+
+
 def roundtrip_2d_host(d, levels: int, coeffs_out=None, out=None, chunk: int = 0):
     """fhwt_roundtrip_2d_host: DWT + IDWT of HOST images, streamed through the current device."""
     import torch
     h, w, batch = _shape_2d(d)
     if out is None:
         out = torch.empty_like(d, pin_memory=d.is_pinned())
+    _host_out(out, d, "out")
+    if coeffs_out is not None:
+        _host_out(coeffs_out, d, "coeffs_out")
     _check(lib().fhwt_roundtrip_2d_host(_host_f32(d, "d"), _host_f32(coeffs_out, "coeffs") if coeffs_out is not None else None,
                                         _host_f32(out, "d_R"), h, w, batch, int(levels), int(chunk)))
     return out
@@ -429,6 +476,9 @@ def roundtrip_1d_host(d, levels: int, coeffs_out=None, out=None, chunk: int = 0)
     n, batch = _shape_1d(d)
     if out is None:
         out = torch.empty_like(d, pin_memory=d.is_pinned())
+    _host_out(out, d, "out")
+    if coeffs_out is not None:
+        _host_out(coeffs_out, d, "coeffs_out")
     _check(lib().fhwt_roundtrip_1d_host(_host_f32(d, "d"), _host_f32(coeffs_out, "coeffs") if coeffs_out is not None else None,
                                         _host_f32(out, "d_R"), n, batch, int(levels), int(chunk)))
     return out
@@ -528,6 +578,8 @@ def lowpass_2d_u8(d, levels: int, out=None, stream=None):
     shape = tuple(d.shape[:-2]) + (h >> levels, w >> levels)
     if out is None:
         out = torch.empty(shape, dtype=torch.float32, device=d.device)
+    if levels >= 1:
+        _out_packed(out, batch * (h >> levels) * (w >> levels), d.device, "ll")
     with torch.cuda.device(d.device):
         _check(lib().fhwt_lowpass_2d_u8(ctypes.c_void_p(d.data_ptr()), _dev_f32(out, "ll"), h, w, batch, int(levels),
                                         None, _stream(stream, d)))
@@ -544,6 +596,8 @@ def lowpass_2d_bf16(d, levels: int, out=None, stream=None):
     shape = tuple(d.shape[:-2]) + (h >> levels, w >> levels)
     if out is None:
         out = torch.empty(shape, dtype=torch.float32, device=d.device)
+    if levels >= 1:
+        _out_packed(out, batch * (h >> levels) * (w >> levels), d.device, "ll")
     with torch.cuda.device(d.device):
         _check(lib().fhwt_lowpass_2d_bf16(ctypes.c_void_p(d.data_ptr()), _dev_f32(out, "ll"), h, w, batch,
                                           int(levels), None, _stream(stream, d)))

@@ -38,18 +38,33 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile the library.  Several processes (torchrun ranks) may call this at once: the
+    build-and-replace runs under an exclusive file lock, each build writes its own per-process
+    temporary file, and a process that waited for the lock re-checks staleness instead of
+    rebuilding, so no rank can load a half-written library."""
+    import fcntl
     lib = out or LIB
     if not force and out is None and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", lib + ".tmp"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libfhwt.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
-    os.replace(lib + ".tmp", lib)
+    with open(lib + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if not force and out is None and not stale():   # another process built it meanwhile
+                return LIB
+            tmp = f"{lib}.{os.getpid()}.tmp"
+            cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+                   *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
+            res = subprocess.run(cmd, capture_output=True, text=True)
+            if res.returncode != 0:
+                sys.stderr.write(res.stdout + res.stderr)
+                if os.path.exists(tmp):
+                    os.unlink(tmp)
+                raise RuntimeError("nvcc failed building libfhwt.so")
+            if verbose:
+                sys.stderr.write(res.stderr)
+            os.replace(tmp, lib)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
     return lib
 
 

@@ -120,9 +120,20 @@ fhwt_status encode_2d(CUtensorMap* m, const void* base, bool f64, int64_t cols, 
   return FHWT_OK;
 }
 
-// Tuning knobs (defaults chosen by measurement); env overrides exist only
-// for the tile/stage sweeps in tools/.
+// Tuning knobs (defaults chosen by measurement).  The env overrides exist
+// only for the sweeps in tools/ and the A/B tests: every FHWT_* variable is ignored unless
+// FHWT_TUNING=1 is set too, so a stray variable in a user's environment cannot change which
+// kernel, tile or ring depth runs (results are bitwise equal either way; speed is not).
+}  // namespace
+namespace fhwt {
+bool tuning_enabled() {
+  const char* t = std::getenv("FHWT_TUNING");
+  return t && t[0] == '1' && t[1] == 0;
+}
+}  // namespace fhwt
+namespace {
 int env_int(const char* name, int dflt) {
+  if (!tuning_enabled()) return dflt;
   const char* v = std::getenv(name);
   return (v && *v) ? std::atoi(v) : dflt;
 }
@@ -226,6 +237,7 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 // ---------------------------------------------------------------------- plan object
 struct fhwt_plan_s {
   int kind;  // 1 or 2
+  int device;  // CUDA device the plan runs on; -1 = the device current at each call
   int64_t n, h, w, batch;
   int levels;
   std::vector<Pass> passes;
@@ -794,7 +806,7 @@ fhwt_status run_ana1d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     p.in_pitch = k == 0 ? n : pitch4(p.nin);
     p.out = p.final_pass ? nullptr : static_cast<void*>(ws + pl->ws_off[k]);
     p.out_pitch = p.final_pass ? 0 : pitch4(p.nin >> ps.Lp);
-    FHWT_CUDA(launch_ana1d(p, k > 0, s), "ana1d launch");
+    FHWT_CUDA(launch_ana1d(p, k > 0, s, pl->levels > kMaxLevels1dPass), "ana1d launch");
     if (tail) break;
   }
   return FHWT_OK;
@@ -848,8 +860,25 @@ size_t data_bytes(const fhwt_plan_s* p) {
   return size_t(p->batch) * (p->kind == 2 ? size_t(p->h) * size_t(p->w) : size_t(p->n)) * sizeof(float);
 }
 
+fhwt_status run_on_device(fhwt_plan p, const float* in, float* out, void* workspace, fhwt_stream_t st,
+                          bool analysis);
+
+// A plan bound to a device (fhwt_plan_1d/2d `device` >= 0) makes that device current for the
+// call and restores the caller's afterwards; -1 runs on whatever device is current.
 fhwt_status run(fhwt_plan p, const float* in, float* out, void* workspace, fhwt_stream_t st, bool analysis) {
   if (!p) return fail(FHWT_ERR_INVALID_ARG, "null plan");
+  if (p->device < 0) return run_on_device(p, in, out, workspace, st, analysis);
+  int cur = 0;
+  FHWT_CUDA(cudaGetDevice(&cur), "cudaGetDevice");
+  if (cur == p->device) return run_on_device(p, in, out, workspace, st, analysis);
+  FHWT_CUDA(cudaSetDevice(p->device), "cudaSetDevice(plan device)");
+  const fhwt_status r = run_on_device(p, in, out, workspace, st, analysis);
+  cudaSetDevice(cur);
+  return r;
+}
+
+fhwt_status run_on_device(fhwt_plan p, const float* in, float* out, void* workspace, fhwt_stream_t st,
+                          bool analysis) {
   FHWT_TRY(check_ptrs(in, out, data_bytes(p)));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
   char* ws = static_cast<char*>(workspace);
@@ -926,13 +955,26 @@ fhwt_status fhwt_haar_filter_bank(fhwt_filter_bank* out) {
   return FHWT_OK;
 }
 
-fhwt_status fhwt_plan_1d(fhwt_plan* p, int64_t n, int64_t batch, int levels, const fhwt_filter_bank* fb) {
+// device >= 0 must name an existing CUDA device (checked once, here); -1 = current at call time
+static fhwt_status check_device(int device) {
+  if (device < -1) return fail(FHWT_ERR_INVALID_ARG, "device %d (use -1 for the current device)", device);
+  if (device == -1) return FHWT_OK;
+  int n = 0;
+  FHWT_CUDA(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+  if (device >= n) return fail(FHWT_ERR_NO_DEVICE, "device %d of %d", device, n);
+  return FHWT_OK;
+}
+
+fhwt_status fhwt_plan_1d(fhwt_plan* p, int64_t n, int64_t batch, int levels, const fhwt_filter_bank* fb,
+                         int device) {
   if (!p) return fail(FHWT_ERR_INVALID_ARG, "null plan pointer");
   *p = nullptr;
   FHWT_TRY(check_1d(n, batch, levels));
   FHWT_TRY(check_bank(fb));
+  FHWT_TRY(check_device(device));
   auto* pl = new fhwt_plan_s{};
   pl->kind = 1;
+  pl->device = device;
   pl->n = n;
   pl->batch = batch;
   pl->levels = levels;
@@ -941,13 +983,16 @@ fhwt_status fhwt_plan_1d(fhwt_plan* p, int64_t n, int64_t batch, int levels, con
   return FHWT_OK;
 }
 
-fhwt_status fhwt_plan_2d(fhwt_plan* p, int64_t h, int64_t w, int64_t batch, int levels, const fhwt_filter_bank* fb) {
+fhwt_status fhwt_plan_2d(fhwt_plan* p, int64_t h, int64_t w, int64_t batch, int levels, const fhwt_filter_bank* fb,
+                         int device) {
   if (!p) return fail(FHWT_ERR_INVALID_ARG, "null plan pointer");
   *p = nullptr;
   FHWT_TRY(check_2d(h, w, batch, levels));
   FHWT_TRY(check_bank(fb));
+  FHWT_TRY(check_device(device));
   auto* pl = new fhwt_plan_s{};
   pl->kind = 2;
+  pl->device = device;
   pl->h = h;
   pl->w = w;
   pl->batch = batch;
@@ -983,7 +1028,7 @@ fhwt_status fhwt_synthesize(fhwt_plan p, const float* coeffs, float* dR, void* w
 
 fhwt_status fhwt_analyze_1d(const float* d, float* coeffs, int64_t n, int64_t batch, int levels, fhwt_stream_t s) {
   fhwt_plan p;
-  FHWT_TRY(fhwt_plan_1d(&p, n, batch, levels, nullptr));
+  FHWT_TRY(fhwt_plan_1d(&p, n, batch, levels, nullptr, -1));
   fhwt_status st = run(p, d, coeffs, nullptr, s, true);
   delete p;
   return st;
@@ -991,7 +1036,7 @@ fhwt_status fhwt_analyze_1d(const float* d, float* coeffs, int64_t n, int64_t ba
 
 fhwt_status fhwt_synthesize_1d(const float* coeffs, float* dR, int64_t n, int64_t batch, int levels, fhwt_stream_t s) {
   fhwt_plan p;
-  FHWT_TRY(fhwt_plan_1d(&p, n, batch, levels, nullptr));
+  FHWT_TRY(fhwt_plan_1d(&p, n, batch, levels, nullptr, -1));
   fhwt_status st = run(p, coeffs, dR, nullptr, s, false);
   delete p;
   return st;
@@ -1000,7 +1045,7 @@ fhwt_status fhwt_synthesize_1d(const float* coeffs, float* dR, int64_t n, int64_
 fhwt_status fhwt_analyze_2d(const float* d, float* coeffs, int64_t h, int64_t w, int64_t batch, int levels,
                             fhwt_stream_t s) {
   fhwt_plan p;
-  FHWT_TRY(fhwt_plan_2d(&p, h, w, batch, levels, nullptr));
+  FHWT_TRY(fhwt_plan_2d(&p, h, w, batch, levels, nullptr, -1));
   fhwt_status st = run(p, d, coeffs, nullptr, s, true);
   delete p;
   return st;
@@ -1009,7 +1054,7 @@ fhwt_status fhwt_analyze_2d(const float* d, float* coeffs, int64_t h, int64_t w,
 fhwt_status fhwt_synthesize_2d(const float* coeffs, float* dR, int64_t h, int64_t w, int64_t batch, int levels,
                                fhwt_stream_t s) {
   fhwt_plan p;
-  FHWT_TRY(fhwt_plan_2d(&p, h, w, batch, levels, nullptr));
+  FHWT_TRY(fhwt_plan_2d(&p, h, w, batch, levels, nullptr, -1));
   fhwt_status st = run(p, coeffs, dR, nullptr, s, false);
   delete p;
   return st;
@@ -1129,7 +1174,7 @@ fhwt_status roundtrip_host(fhwt_plan_s* full, const float* h_d, float* h_c, floa
 extern "C" fhwt_status fhwt_roundtrip_2d_host(const float* h_d, float* h_coeffs, float* h_dR, int64_t h, int64_t w,
                                               int64_t batch, int levels, int64_t chunk) {
   fhwt_plan p;
-  FHWT_TRY(fhwt_plan_2d(&p, h, w, batch, levels, nullptr));
+  FHWT_TRY(fhwt_plan_2d(&p, h, w, batch, levels, nullptr, -1));
   fhwt_status st = roundtrip_host(p, h_d, h_coeffs, h_dR, h * w, chunk);
   delete p;
   return st;
@@ -1138,7 +1183,7 @@ extern "C" fhwt_status fhwt_roundtrip_2d_host(const float* h_d, float* h_coeffs,
 extern "C" fhwt_status fhwt_roundtrip_1d_host(const float* h_d, float* h_coeffs, float* h_dR, int64_t n, int64_t batch,
                                               int levels, int64_t chunk) {
   fhwt_plan p;
-  FHWT_TRY(fhwt_plan_1d(&p, n, batch, levels, nullptr));
+  FHWT_TRY(fhwt_plan_1d(&p, n, batch, levels, nullptr, -1));
   fhwt_status st = roundtrip_host(p, h_d, h_coeffs, h_dR, n, chunk);
   delete p;
   return st;

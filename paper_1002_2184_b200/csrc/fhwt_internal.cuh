@@ -128,7 +128,9 @@ cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int fast_l
 int syn2d_threads(int fast_lp);   // CTA size of a synthesis variant (fast code as in launch_syn2d)
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm);
 cudaError_t syn2d_occupancy(int fast_lp, size_t smem, int* blocks_per_sm);
-cudaError_t launch_ana1d(const Haar1dParams& p, bool in_f64, cudaStream_t s);
+// f64all (first pass of a decomposition deeper than 10 levels): levels 1-3 in fp64 too, so the only
+// error left is the final rounding of each output (the 1-D reading R14)
+cudaError_t launch_ana1d(const Haar1dParams& p, bool in_f64, cudaStream_t s, bool f64all = false);
 cudaError_t launch_syn1d(const Haar1dParams& p, cudaStream_t s);
 cudaError_t launch_ana2d_l1_scalar(const float* d, float* c, int64_t h, int64_t w, int64_t batch, cudaStream_t s);
 cudaError_t launch_syn2d_l1_scalar(const float* c, float* d, int64_t h, int64_t w, int64_t batch, cudaStream_t s);
@@ -163,6 +165,7 @@ cudaError_t launch_small2d(const Small2dParams& p, bool analysis, int grid, size
                            bool one_d = false);
 
 void count_launch();
+bool tuning_enabled();   // FHWT_TUNING=1: honour the FHWT_* sweep knobs (fhwt_api.cu env_int)
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -12,6 +12,8 @@
 // values of index 32q + rotr5(l, m) — so every detail store of a warp is one contiguous segment;
 // levels 6-10 run lane-per-index.  HBM traffic: one read and one write per sample.
 // Precision: levels 1-3 fp32, levels >= 4 fp64 (SURVEY §8(c) C7 rule), outputs rounded once.
+#include <type_traits>
+
 #include "fhwt_internal.cuh"
 
 namespace fhwt {
@@ -38,6 +40,12 @@ __device__ __forceinline__ void load4(const float* p, float* x, int idx, int m) 
 #pragma unroll
     for (int e = 0; e < 4; ++e) x[e] = (idx + e < m) ? p[e] : 0.f;
   }
+}
+__device__ __forceinline__ void load4(const float* p, double* x, int idx, int m) {   // fp32 in, fp64 levels
+  float t[4];
+  load4(p, t, idx, m);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) x[e] = double(t[e]);
 }
 __device__ __forceinline__ void load4(const double* p, double* x, int idx, int m) {
   if (idx + 3 < m) {
@@ -135,9 +143,11 @@ __device__ __forceinline__ void ana1d_tail(const Haar1dParams& p, const double* 
   for (int k = 0; k < m; ++k) stg_stream1(crow + k, float(v[k]));
 }
 
-template <typename TIn>
+// F64ALL: levels 1..3 in fp64 as well (decompositions deeper than 10 levels, reading R14: the
+// fp32 rounding of levels 1-3 grows by up to sqrt(2) per further level, 2^(J/2 - 1.5) x at level J).
+template <typename TIn, bool F64ALL = false>
 __global__ void __launch_bounds__(kThreads1d) ana1d_kernel(const __grid_constant__ Haar1dParams p) {
-  using T1 = TIn;  // levels 1..3; levels >= 4 are fp64
+  using T1 = typename std::conditional<F64ALL, double, TIn>::type;  // levels 1..3; levels >= 4 are fp64
   __shared__ double tail_ll[kThreads1d / 32];
   const int lane = threadIdx.x & 31;
   const int64_t w = int64_t(blockIdx.x) * (kThreads1d / 32) + (threadIdx.x >> 5);
@@ -480,11 +490,13 @@ int grid1(int64_t total) {
 
 }  // namespace
 
-cudaError_t launch_ana1d(const Haar1dParams& p, bool in_f64, cudaStream_t s) {
+cudaError_t launch_ana1d(const Haar1dParams& p, bool in_f64, cudaStream_t s, bool f64all) {
   const int64_t blocks = (p.nwarps + (kThreads1d / 32) - 1) / (kThreads1d / 32);
   count_launch();
   if (in_f64)
     ana1d_kernel<double><<<unsigned(blocks), kThreads1d, 0, s>>>(p);
+  else if (f64all)
+    ana1d_kernel<float, true><<<unsigned(blocks), kThreads1d, 0, s>>>(p);
   else
     ana1d_kernel<float><<<unsigned(blocks), kThreads1d, 0, s>>>(p);
   return cudaGetLastError();

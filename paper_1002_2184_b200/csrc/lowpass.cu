@@ -404,7 +404,8 @@ int grid_lp(int64_t total) {   // grid-stride kernels: at most ~64 waves of resi
 
 int grid_exact(int64_t total) { return int((total + 255) / 256); }
 
-bool env_lowpass_warp() {   // A/B knob: FHWT_LOWPASS_WARP=0 keeps the two-launch wide path
+bool env_lowpass_warp() {   // A/B knob (with FHWT_TUNING=1): FHWT_LOWPASS_WARP=0 keeps the two-launch wide path
+  if (!tuning_enabled()) return true;
   const char* v = std::getenv("FHWT_LOWPASS_WARP");
   return !(v && *v == '0');
 }

@@ -4,8 +4,9 @@ One process per GPU over torch.distributed (NCCL on B200, gloo in the CPU tests)
 partitions into independent units (reading R1: pairs (x[2k], x[2k+1]) make every 2^L-aligned
 block independent), so sharding needs no halo exchange:
 
-* batched signals / images (c2, c4): rank r owns units [r*B, (r+1)*B) of a global batch N*B
-  (weak scaling, no collective on the data path);
+* batched signals / images (c2, c4): rank r owns units [r*U/N, (r+1)*U/N) of the fixed global
+  batch U (strong scaling: BASELINE c4 splits its 256 images across 1/2/4/8 GPUs; c2 its 4096
+  signals), no collective on the data path; `unit_shard` keeps the opt-in weak-scaling split;
 * one large image (c5): rank r owns rows [r*h/N, (r+1)*h/N), a multiple of 2^L rows; its band
   output equals rows [r*h/N >> j, (r+1)*h/N >> j) of every global level-j band.  The coarsest LL
   of all bands is all-gathered (the only exchange; 64 KiB for c5).
@@ -21,8 +22,20 @@ import torch
 import torch.distributed as dist
 
 
+def unit_range(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Strong scaling: (first unit, count) of `rank`'s contiguous share of `total` independent units
+    (images / signals).  Equal shares; the first total % world ranks take one unit more."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    if total < world:
+        raise ValueError(f"{total} units do not give each of {world} ranks one")
+    q, r = divmod(total, world)
+    first = rank * q + min(rank, r)
+    return first, q + (1 if rank < r else 0)
+
+
 def unit_shard(units_per_rank: int, rank: int) -> tuple[int, int]:
-    """Weak scaling: (first unit, count) owned by `rank`."""
+    """Weak scaling (opt-in): (first unit, count) owned by `rank` of a global batch world*units."""
     return rank * units_per_rank, units_per_rank
 
 
@@ -123,8 +136,13 @@ class PeerLLGather:
         return self._mem[(self._calls - 1) % 2]
 
     def __call__(self, coeffs: torch.Tensor, levels: int, stream=None) -> torch.Tensor:
+        """Gather on `stream` (default: the current stream).  The returned slot stays valid until
+        the call after next; read it on `stream` (or after synchronising with it): the slot
+        reuse argument above assumes the result is consumed in stream order."""
         from . import pack_ll_2d_peers
-        if coeffs.shape[-2] >> levels != self.rows or coeffs.shape[-1] >> levels != self.cols:
+        # one 2-D band per rank: a leading batch > 1 would make the kernel store past the rank's slot
+        if (coeffs.dim() < 2 or coeffs.shape[-2] >> levels != self.rows or coeffs.shape[-1] >> levels != self.cols
+                or coeffs.numel() != (self.rows << levels) * (self.cols << levels)):
             raise ValueError("coefficient band does not match the gather buffer")
         k = self._calls % 2
         stream = stream or torch.cuda.current_stream(self._mem.device)

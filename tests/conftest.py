@@ -17,3 +17,11 @@ def pytest_configure(config):
 def cuda_available():
     import torch
     return torch.cuda.is_available()
+
+
+@pytest.fixture(autouse=True)
+def _fhwt_tuning(monkeypatch):
+    """The library honours its FHWT_* sweep knobs only with FHWT_TUNING=1; the
+    A/B tests below set knobs through monkeypatch, so the gate is open for every test (the test of
+    the gate itself removes it)."""
+    monkeypatch.setenv("FHWT_TUNING", "1")

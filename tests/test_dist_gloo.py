@@ -83,7 +83,57 @@ def _weak_rank(rank):
     return {"first": first, "count": count, "coeffs": o.analyze_2d(x, 4)}
 
 
+def _strong_rank(rank):
+    """bench.py's strong-scaling split at world 2: c4's 256 images -> 128 per rank, c2's 4096
+    signals -> 2048, c5's rows -> two 16384-row bands; plus a reduced c4-like batch transformed
+    per rank (oracle stand-in) and the whole-job sample count bench reports (all-reduced)."""
+    import bench
+    sh = {k: bench.shard_of(bench.WORKLOADS[k], WORLD, rank) for k in ("c2", "c4", "c5")}
+    first, count = fdist.unit_range(6, WORLD, rank)
+    x = datagen.c4_batch(first, count, size=64)
+    total = bench.fdist_total(bench.WORKLOADS["c4"], WORLD, None, x.size, "cpu")
+    return {"shards": sh, "first": first, "count": count, "coeffs": o.analyze_2d(x, 4), "total": total}
+
+
 # ------------------------------------------------------------------ tests
+@pytest.mark.timeout(300)
+def test_strong_scaling_unit_split():
+    """BASELINE configs[3]: c4 is sharded by image index across the GPUs (strong scaling, a fixed
+    global batch of 256); c2 likewise by signal."""
+    res = _run("_strong_rank")
+    for r in range(WORLD):
+        assert isinstance(res[r], dict), res[r]
+    c4 = [res[r]["shards"]["c4"] for r in range(WORLD)]
+    assert [(s["first"], s["count"]) for s in c4] == [(0, 128), (128, 128)]
+    assert all(s["global_batch"] == 256 and s["scaling"] == "strong" for s in c4)
+    c2 = [res[r]["shards"]["c2"] for r in range(WORLD)]
+    assert [(s["first"], s["count"]) for s in c2] == [(0, 2048), (2048, 2048)]
+    c5 = [res[r]["shards"]["c5"] for r in range(WORLD)]
+    assert [(s["r0"], s["r1"]) for s in c5] == [(0, 16384), (16384, 32768)]
+    allx = datagen.c4_batch(0, 6, size=64)
+    ref = o.analyze_2d(allx, 4)
+    for r in range(WORLD):
+        f, c = res[r]["first"], res[r]["count"]
+        np.testing.assert_allclose(res[r]["coeffs"], ref[f:f + c], atol=1e-12)
+        assert res[r]["total"] == allx.size
+
+
+def test_unit_range_partitions():
+    for total in (1, 5, 6, 256, 4096, 257):
+        for world in (1, 2, 3, 4, 8):
+            if total < world:
+                with pytest.raises(ValueError):
+                    fdist.unit_range(total, world, 0)
+                continue
+            parts = [fdist.unit_range(total, world, r) for r in range(world)]
+            assert parts[0][0] == 0 and sum(c for _, c in parts) == total
+            assert all(parts[i][0] + parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+            assert max(c for _, c in parts) - min(c for _, c in parts) <= 1
+    assert fdist.unit_range(256, 8, 7) == (224, 32)
+    with pytest.raises(ValueError):
+        fdist.unit_range(8, 2, 2)
+
+
 @pytest.mark.timeout(300)
 def test_row_band_sharding_and_ll_gather():
     res = _run("_c5_like_rank")

@@ -405,6 +405,123 @@ def test_row_band_shards_bitwise_equal_full_image(world):
     assert torch.equal(torch.cat(lls, 0), full[:H >> L, :W >> L])
 
 
+# ------------------------------------------------------------------ rows a8 / f2 against the oracle
+@pytest.fixture(scope="module")
+def c5_2048():
+    """The c5 image recipe (datagen.c5_rows: rectangles from seed 4004, noise per 256-row band) at
+    2048 x 2048, and its fp64 oracle transform at L = 8 (c5's depth)."""
+    xh = datagen.c5_rows(0, 2048, size=2048)
+    return xh, o.analyze_2d(xh, 8)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_gathered_ll_matches_oracle(world, c5_2048):
+    """Row a8: the image split into `world` 2^8-aligned row bands, each band
+    transformed by its own plan as a rank would (ranks run one after another on one GPU: no kernel
+    waits on another).  Checked element-wise against oracle.analyze_2d of the WHOLE image at the
+    north_star bar (max|d| of the whole image, reading R9):
+    * every band's coefficients at their global Mallat rows (all 8 levels);
+    * every band's packed LL_8 (fhwt_pack_ll_2d, the all-gather's input);
+    * the gathered LL — the bands' packs in rank order, what all_gather_into_tensor delivers — and
+      the peer-memory gather (fhwt_pack_ll_2d_peers into a table of `world` buffers standing in for
+      the ranks' symmetric buffers): identical on every "rank" and equal to the oracle's LL_8.
+    The paper's image output is this LL (§V Fig. 12)."""
+    from paper_1002_2184_b200 import dist as fdist
+    xh, ref = c5_2048
+    H = W = 2048
+    L = 8
+    scale = float(np.abs(xh).max())
+    x = dev(xh)
+    lr, lc = H >> L, W >> L
+    bufs = [torch.full((lr, lc), float("nan"), device="cuda") for _ in range(world)]
+    table = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    packs = []
+    for r in range(world):
+        r0, r1 = fdist.row_band(H, world, r, L)
+        plan = fhwt.Plan2d(r1 - r0, W, 1, L)
+        band = plan.analyze(x[r0:r1])
+        bh = r1 - r0
+        got = host(band)
+        for j in range(1, L + 1):
+            g0, g1 = fdist.band_rows(r0, r1, j)
+            hj, wj, bj = H >> j, W >> j, bh >> j
+            for gs, rs in (((slice(0, bj), slice(wj, 2 * wj)), (slice(g0, g1), slice(wj, 2 * wj))),
+                           ((slice(bj, 2 * bj), slice(0, wj)), (slice(hj + g0, hj + g1), slice(0, wj))),
+                           ((slice(bj, 2 * bj), slice(wj, 2 * wj)), (slice(hj + g0, hj + g1), slice(wj, 2 * wj)))):
+                err = np.abs(got[gs] - ref[rs]).max() / scale
+                assert err <= TOL, (r, j, err)
+        ll = plan.pack_ll(band)[0]
+        g0, g1 = fdist.band_rows(r0, r1, L)
+        assert ll.shape == (g1 - g0, lc)
+        err = np.abs(host(ll) - ref[g0:g1, :lc]).max() / scale
+        assert err <= TOL, ("packed LL", r, err)
+        fhwt.pack_ll_2d_peers(band, L, table.data_ptr(), r, world)
+        packs.append(ll)
+    gathered = torch.cat(packs, 0)
+    torch.cuda.synchronize()
+    err = np.abs(host(gathered) - ref[:lr, :lc]).max() / scale
+    assert err <= TOL, ("gathered LL", err)
+    for b in bufs:   # every rank's gather buffer holds the same complete LL_8
+        assert torch.equal(b, gathered)
+
+
+def test_one_band_equals_whole_image_rows(c5_2048):
+    """P = 1 vs P = 8: the bitwise identity of band outputs and the unsharded
+    transform, here with the full image's plan (cooperative coarse levels) against band plans."""
+    from paper_1002_2184_b200 import dist as fdist
+    xh, _ = c5_2048
+    x = dev(xh)
+    full = fhwt.Plan2d(2048, 2048, 1, 8).analyze(x)
+    for r in (0, 3, 7):
+        r0, r1 = fdist.row_band(2048, 8, r, 8)
+        band = fhwt.Plan2d(r1 - r0, 2048, 1, 8).analyze(x[r0:r1])
+        g0, g1 = fdist.band_rows(r0, r1, 8)
+        assert torch.equal(band[:g1 - g0, :8], full[g0:g1, :8])
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_signal_shards_match_oracle(world):
+    """Row f2, batched: c2's signals split by index into `world` contiguous shards (bench.py's
+    strong split, dist.unit_range) — here 64 c2 signals of 65536 samples, J = 10 — each shard
+    transformed by its own plan; every signal equals oracle.decompose_1d at the north_star bar
+    (max|d| per signal, reading R9), and its round trip too.  SPEC.md:165-183."""
+    from paper_1002_2184_b200 import dist as fdist
+    total, n, J = 64, 65536, 10
+    for r in range(world):
+        first, count = fdist.unit_range(total, world, r)
+        xh = datagen.c2_batch(first, count, n=n)
+        plan = fhwt.Plan1d(n, count, J)
+        c = plan.analyze(dev(xh))
+        rr = plan.synthesize(c)
+        assert_close(host(c), o.decompose_1d(xh, J), xh, 1, what=f"shard {r} of {world}")
+        assert_close(host(rr), xh, xh, 1, what=f"shard {r} round trip")
+
+
+@pytest.mark.parametrize("world,J", [(2, 9), (4, 9), (8, 12)])
+def test_long_signal_segments_match_oracle(world, J):
+    """Row f2, one long signal: 2^J-aligned segments (dist.segment_1d) transformed independently;
+    every band of every segment, placed at its global Mallat offset (dist.segment_bands_1d), equals
+    oracle.decompose_1d of the WHOLE signal at the north_star bar, and the gathered coarse
+    approximations form the global a_J.  Segment starts are not multiples of the kernel's
+    1024-sample chunk for J = 9; J = 12 exercises the in-CTA levels 11-12."""
+    from paper_1002_2184_b200 import dist as fdist
+    N = 3 * 4096 * world if J < 12 else 8192 * world
+    xh = datagen.c2_signal(11, n=N)
+    ref = o.decompose_1d(xh, J)
+    scale = float(np.abs(xh).max())
+    x = dev(xh[None])
+    approx = []
+    for r in range(world):
+        s0, s1 = fdist.segment_1d(N, world, r, J)
+        seg = host(fhwt.analyze_1d(x[:, s0:s1].contiguous(), J)[0])
+        for band, (lo, go, ln) in fdist.segment_bands_1d(s0, s1, N, J).items():
+            err = np.abs(seg[lo:lo + ln] - ref[go:go + ln]).max() / scale
+            assert err <= TOL, (r, band, err)
+        approx.append(seg[:(s1 - s0) >> J])
+    err = np.abs(np.concatenate(approx) - ref[:N >> J]).max() / scale
+    assert err <= TOL, ("gathered a_J", err)
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_long_signal_segments_bitwise_equal(world):
     """§8(f) f2: a long signal split into 2^J-aligned segments (segment starts are not multiples
@@ -613,6 +730,60 @@ def test_short_signals_chunk_kernels(monkeypatch, n, batch, levels):
     rg = fhwt.synthesize_1d(c, levels)
     torch.cuda.synchronize()
     assert torch.equal(c, cg) and torch.equal(r, rg)
+
+
+def test_knobs_ignored_without_tuning(monkeypatch):
+    """With FHWT_TUNING unset the library ignores every other FHWT_* variable: FHWT_COOP=0 (two
+    launches for 5 < L <= 8 instead of the cooperative one) takes effect only behind the gate."""
+    x = dev(datagen.uniform((4, 1024, 1024), seed=8))
+    ref = fhwt.analyze_2d(x, 7)
+    monkeypatch.setenv("FHWT_COOP", "0")
+    monkeypatch.delenv("FHWT_TUNING")
+    n0 = fhwt.launch_count()
+    c = fhwt.analyze_2d(x, 7)
+    assert fhwt.launch_count() - n0 == 1
+    monkeypatch.setenv("FHWT_TUNING", "1")
+    n0 = fhwt.launch_count()
+    c2 = fhwt.analyze_2d(x, 7)
+    assert fhwt.launch_count() - n0 == 2
+    torch.cuda.synchronize()
+    assert torch.equal(c, ref) and torch.equal(c2, ref)
+
+
+def test_plan_device_argument():
+    """fhwt_plan_1d/2d `device`: a plan bound to device 0 gives the unbound plan's
+    result bitwise, and bad device indices are rejected at plan time.  (Switching devices inside a
+    call needs a second GPU; the driver's boxes have one.)"""
+    x = dev(datagen.uniform((2, 256, 256), seed=9))
+    a = fhwt.Plan2d(256, 256, 2, 4, device=0).analyze(x)
+    b = fhwt.Plan2d(256, 256, 2, 4).analyze(x)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    with pytest.raises(fhwt.NoDevice):
+        fhwt.Plan1d(1024, 1, 3, device=torch.cuda.device_count())
+    with pytest.raises(fhwt.InvalidArgument):
+        fhwt.Plan1d(1024, 1, 3, device=-2)
+
+
+def test_output_buffers_are_checked():
+    """Caller-supplied outputs of the packed / host entry points are size-checked before the
+    C ABI writes (an undersized buffer would be an out-of-bounds write)."""
+    x = dev(datagen.uniform((2, 256, 256), seed=10))
+    c = fhwt.analyze_2d(x, 5)
+    with pytest.raises(fhwt.ShapeMismatch):
+        fhwt.pack_ll_2d(c, 5, out=torch.empty((2, 8, 7), device="cuda"))
+    with pytest.raises(fhwt.ShapeMismatch):
+        fhwt.Plan2d(256, 256, 2, 5).pack_ll(c, out=torch.empty((1, 8, 8), device="cuda"))
+    u8 = torch.zeros((2, 256, 256), dtype=torch.uint8, device="cuda")
+    with pytest.raises(fhwt.ShapeMismatch):
+        fhwt.lowpass_2d_u8(u8, 5, out=torch.empty((2, 8, 4), device="cuda"))
+    with pytest.raises(fhwt.ShapeMismatch):
+        fhwt.lowpass_2d_bf16(u8.to(torch.bfloat16), 5, out=torch.empty((3, 8, 8), device="cuda"))
+    h = torch.zeros((2, 256, 256))
+    with pytest.raises(fhwt.ShapeMismatch):
+        fhwt.roundtrip_2d_host(h, 3, out=torch.empty((1, 256, 256)))
+    with pytest.raises(fhwt.ShapeMismatch):
+        fhwt.roundtrip_1d_host(torch.zeros((2, 1024)), 3, coeffs_out=torch.empty((2, 512)))
 
 
 def test_pack_ll_peers_table_layout():

@@ -59,8 +59,7 @@ def test_random_1d(seed):
     torch.cuda.synchronize()
     scale = np.abs(x).max(axis=1, keepdims=True)
     ref = o.decompose_1d(x, J)
-    # deep 1-D levels: coefficients reach 2^(J/2) max|d|; fp32 output rounding alone is
-    # 2^(J/2 - 24) max|d|, so the bar is the north_star's 1e-5 or that floor
-    tol = max(TOL, 4 * 2.0 ** (J / 2 - 24))
-    assert (np.abs(c.double().cpu().numpy() - ref) / scale).max() <= tol, (n, b, J)
+    # J <= 14 here: with levels 1-3 in fp64 for J > 10 (reading R14) the only error left
+    # is the output rounding, <= 2^(J/2 - 24) max|d| = 7.6e-6 at J = 14: the north_star bar holds
+    assert (np.abs(c.double().cpu().numpy() - ref) / scale).max() <= TOL, (n, b, J)
     assert (np.abs(r.double().cpu().numpy() - x) / scale).max() <= TOL, (n, b, J)

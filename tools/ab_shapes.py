@@ -2,6 +2,7 @@
 process and buffers).  python tools/ab_shapes.py 'FHWT_SYN_RAGGED_FAST=0' 'FHWT_SYN_RAGGED_FAST=1'"""
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import statistics
 import sys
 

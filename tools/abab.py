@@ -2,6 +2,7 @@
 python tools/abab.py 'L=5' 'L=8' 'L=8,FHWT_COOP=0' ...   (analysis unless SYN=1 in the spec)"""
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import statistics
 import sys
 

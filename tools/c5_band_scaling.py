@@ -4,6 +4,7 @@ efficiency T(1) / (P * T(P)) it implies before any communication (the all-gather
 coarsest LL runs beside the synthesis pass).  Not a multi-GPU measurement."""
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -2,6 +2,7 @@
 at L = 1..5 (L=1 is a single strided read+write pass).  python tools/ceiling_2d.py"""
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

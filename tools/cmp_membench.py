@@ -3,6 +3,7 @@
 import ctypes
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import statistics
 import subprocess
 import sys

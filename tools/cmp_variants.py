@@ -4,6 +4,7 @@ output with the first variant's.
 python tools/cmp_variants.py L 'ANA:FHWT_ANA_WARP=0' 'ANA:FHWT_ANA_WARP=1' 'SYN:FHWT_SYN_MODE=2' ..."""
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import statistics
 import sys
 import threading

@@ -1,6 +1,7 @@
 """Host-buffer round trip (fhwt_roundtrip_2d_host) on the c4 workload: chunk size x stream count."""
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import statistics
 import sys
 import time

@@ -2,6 +2,7 @@
 python tools/latency_small.py 'FHWT_SMALL_TILES=0' 'FHWT_SMALL_TILES=1'"""
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -1,5 +1,6 @@
 """Small shapes that exercise every kernel variant once (for compute-sanitizer runs)."""
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

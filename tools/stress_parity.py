@@ -3,6 +3,7 @@ every dispatch path (fast / ragged-clamped / masked / generic tiles, small-image
 chunks, cooperative and two-pass coarse levels, kernel-variant knobs), each against the fp64 oracle
 at the north_star tolerance, plus bitwise determinism.  python tools/stress_parity.py [N] [seed]"""
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -1,6 +1,7 @@
 """Persistent-grid size sweep: CTAs per SM x levels, both 2-D kernels, c4-shaped data."""
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

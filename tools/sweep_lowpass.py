@@ -1,5 +1,6 @@
 """Lowpass (f1) timing on the c4 uint8 batch."""
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -1,4 +1,5 @@
 # Short-signal chunk kernels: chunk size x ring depth x CTAs/SM (analysis / synthesis GB/s)
+export FHWT_TUNING=1   # the library honours FHWT_* knobs only behind this gate
 for ch in 4096 8192 16384; do for st in 2 3; do for c in 0 2 4 6; do
   echo "chunk=$ch stages=$st ctas=$c $(FHWT_SMALL1D_CHUNK=$ch FHWT_SMALL_STAGES=$st FHWT_SMALL_CTAS=$c python - <<'PY'
 import torch, paper_1002_2184_b200 as fhwt

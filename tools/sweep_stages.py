@@ -1,6 +1,7 @@
 """Stage-count x levels sweep of both 2-D kernels on c4-shaped data (256 x 2048^2)."""
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -3,6 +3,7 @@ launches individually (CUDA events) with NVML SM clock / power samples, to separ
 power-capped behaviour.  python tools/timeseries.py L N 'ANA:FHWT_ANA_WARP=0' ..."""
 import json
 import os
+os.environ.setdefault("FHWT_TUNING", "1")   # the library honours FHWT_* knobs only behind this gate
 import sys
 import time
 
