@@ -548,6 +548,30 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     // FHWT_ANA_FUSED=3: the fused2 path with a dedicated 9th tail warp (ana2d_fused3_kernel)
     const bool fused3 = fast_ok && p.fused == 3 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 && p.mask_mode == 0 &&
                         p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows;
+    // FHWT_ANA_FUSED=8: warp-specialised kernel (haar2d_ana.cu): 8 compute warps, each all five
+    // levels of its own 32 x 32 block, plus a TMA producer warp; no CTA barrier per tile
+    const bool ws8 = fast_ok && p.fused == 8 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 && p.mask_mode == 0 &&
+                     p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows;
+    if (ws8) {
+      p.stages = env_int("FHWT_ANA_STAGES", 2);
+      uint32_t ll1_off = 0, bar_off = 0;
+      const size_t wsmem = ana2d_ws_smem(p.stages, &ll1_off, &bar_off);
+      p.p_off[0] = ll1_off;
+      p.bar_off = bar_off;
+      int wbps = 0;
+      FHWT_CUDA(ana2d_ws_occupancy(wsmem, &wbps), "ws occupancy");
+      if (wbps < 1) return fail(FHWT_ERR_CUDA, "warp-specialised analysis does not fit (%zu B)", wsmem);
+      if (const int cap = env_int("FHWT_ANA_CTAS_PER_SM", 0)) wbps = std::min(wbps, cap);
+      const int64_t wgrid = std::min<int64_t>(p.ntiles, int64_t(wbps) * di.sms);
+      const bool wcoop = k == 0 && np == 2 && pl->passes[1].Lp <= 3 && env_int("FHWT_COOP", 1) != 0;
+      p.tail = wcoop ? pl->passes[1].Lp : 0;
+      if (env_int("FHWT_DEBUG_LAUNCH", 0))
+        std::fprintf(stderr, "[fhwt] ana2d ws8 stages %d smem %zu B ctas/SM %d grid %lld tail %d\n", p.stages, wsmem,
+                     wbps, (long long)wgrid, p.tail);
+      FHWT_CUDA(launch_ana2d_ws(p, map, int(wgrid), wsmem, s), "ana2d ws launch");
+      if (wcoop) break;
+      continue;
+    }
     const int vmode = fused3 ? 5 : 0;
     const int fast = fast_ok ? (vmode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
@@ -642,7 +666,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       p.hoff[j] = shifted ? 0 : int((W >> (ps.g0 + j)) & 3);
       bw[j] = shifted ? (p.TC >> j) + 4 : int(pitch4((p.TC >> j) + p.hoff[j]));
       p.box_pitch[j] = bw[j];
-      p.row_boxes[j] = bw[j] * 4 >= 1024 && (bw[j] * 4) % 128 == 0;   // see the analysis note
+      p.row_boxes[j] = bw[j] * 4 >= env_int("FHWT_SYN_ROWBOX_MIN", 1024) && (bw[j] * 4) % 128 == 0;   // see the analysis note
       FHWT_TRY(encode_2d(&maps.level[j], coeffs, false, W, B * H, W, bw[j], p.row_boxes[j] ? 1 : p.TR >> j));
     }
     if (kk + 1 == np) {

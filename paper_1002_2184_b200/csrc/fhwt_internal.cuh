@@ -127,6 +127,11 @@ cudaError_t launch_syn2d(const Syn2dParams& p, const TmaMaps2d& maps, int fast_l
                          cudaStream_t s);
 int syn2d_threads(int fast_lp);   // CTA size of a synthesis variant (fast code as in launch_syn2d)
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm);
+// Warp-specialised analysis of full 32 x 256 tiles at LP = 5 (haar2d_ana.cu, K1 v2)
+int ana2d_ws_threads();
+size_t ana2d_ws_smem(int stages, uint32_t* ll1_off, uint32_t* bar_off);
+cudaError_t ana2d_ws_occupancy(size_t smem, int* blocks_per_sm);
+cudaError_t launch_ana2d_ws(const Ana2dParams& p, const CUtensorMap& in_map, int grid, size_t smem, cudaStream_t s);
 cudaError_t syn2d_occupancy(int fast_lp, size_t smem, int* blocks_per_sm);
 // f64all (first pass of a decomposition deeper than 10 levels): levels 1-3 in fp64 too, so the only
 // error left is the final rounding of each output (the 1-D reading R14)

@@ -1,0 +1,239 @@
+// Warp-specialised 2-D Fast Haar analysis of 32 x 256 tiles, 5 levels per pass (c4, c5) — K1 v2.
+//
+// Method: the polyphase Fast Haar analysis bank (§III Fig. 4) applied
+// separably, rows then columns (reading R8); per 2x2 block [[a, b], [c, d]]
+// the row and column butterflies fold to one exact x1/2:
+//     LL = ½((a+b)+(c+d))  LH = ½((a+b)−(c+d))  HL = ½((a−b)+(c−d))  HH = ½((a−b)−(c−d)),
+// iterated on LL (Mallat), levels 1-3 in fp32 and 4-5 in fp64 (reading R13), every output rounded
+// once.  Same operations on the same operands, in the same order, as ana2d_kernel<float, 5, 32, 256>
+// (haar2d.cu): outputs are bitwise identical (tests/test_gpu_parity.py).
+//
+// B200 structure ("K1"): a 32 x 256 input tile is 8 independent 32 x 32 blocks
+// (Haar's 2-tap support with pairs (2k, 2k+1) closes a 2^5-aligned block under 5 levels), so
+//   * warp w of the 8 compute warps owns columns [32w, 32w + 32) of every tile and runs all five
+//     levels of its block alone: level 1 from the TMA stage (4 units of 2 x 4 pixels per lane),
+//     levels 2+3 from its 16 x 16 LL1 in warp-private shared memory (two lanes per 4 x 4 block,
+//     level 3 after a lane-pair shuffle), levels 4+5 in fp64 by warp shuffles.  No CTA barrier:
+//     only __syncwarp between levels.
+//   * warp 8 is the producer: one lane issues the 32 one-row TMA boxes (1 KB rows, measured faster
+//     than one 32-row box) of the CTA's next tile into a stage as soon as all 8 compute warps have
+//     arrived on that stage's "empty" mbarrier — which they do right after level 1, the stage's last
+//     reader.  The TMA issue is off the compute warps' path.
+// 2 CTAs per SM (288 threads each), `stages` 32 KB stages per CTA.
+#include <cooperative_groups.h>
+
+#include "fhwt_internal.cuh"
+#include "haar2d_coarse.cuh"
+
+namespace fhwt {
+
+namespace {
+
+constexpr int kWsComputeWarps = 8;
+constexpr int kWsThreads = 32 * (kWsComputeWarps + 1);
+constexpr int kLL1Pitch = 16;   // floats per LL1 row of a warp's 16 x 16 block
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Producer: the 32 one-row boxes of tile t (32-bit tile decode: a tile holds 8192 pixels, so tile
+// counts are < 2^31 for any buffer the TMA row range admits).
+__device__ __forceinline__ void ws_issue(const Ana2dParams& p, const CUtensorMap* map, unsigned char* dst,
+                                         uint64_t* full, uint32_t t, uint64_t pol) {
+  const uint32_t rt = t / uint32_t(p.tiles_c), ct = t - rt * uint32_t(p.tiles_c);
+  mbar_arrive_expect_tx(full, 32u * 1024u);
+  const int row = int(rt) * 32, col = int(ct) * 256;
+#pragma unroll 1
+  for (int r = 0; r < 32; ++r) tma_load_2d(dst + r * 1024, map, col, row + r, full, pol);
+}
+
+// Levels 1-5 of warp w's 32 x 32 block of one tile.  `release` is called after level 1 (the last
+// read of the stage).
+template <typename REL>
+__device__ __forceinline__ void ws_block(const Ana2dParams& p, const float* __restrict__ st, float* __restrict__ ll1,
+                                         int64_t b, int64_t row0, int64_t col0, int w, int lane, const REL& release) {
+  const int64_t W = p.W, H = p.H;
+  // ---- level 1: unit (orow, q) = 2 x 4 input pixels -> 1 x 2 outputs per band
+  {
+    const int64_t wg = W >> 1, hgW = (H >> 1) * W;
+    const int q = lane & 7;
+    float* const base = p.out + (b * H + (row0 >> 1)) * W + (col0 >> 1) + 16 * w + 2 * q;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int orow = (lane >> 3) + 4 * k;
+      const float4 t0 = *reinterpret_cast<const float4*>(st + (2 * orow) * 256 + 32 * w + 4 * q);
+      const float4 t1 = *reinterpret_cast<const float4*>(st + (2 * orow + 1) * 256 + 32 * w + 4 * q);
+      float ll[2], hl[2], lh[2], hh[2];
+      const float a0[2] = {t0.x, t0.z}, b0[2] = {t0.y, t0.w}, c0[2] = {t1.x, t1.z}, d0[2] = {t1.y, t1.w};
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const float s1 = a0[v] + b0[v], s2 = c0[v] + d0[v], d1 = a0[v] - b0[v], d2 = c0[v] - d0[v];
+        ll[v] = (s1 + s2) * 0.5f;
+        lh[v] = (s1 - s2) * 0.5f;
+        hl[v] = (d1 + d2) * 0.5f;
+        hh[v] = (d1 - d2) * 0.5f;
+      }
+      float* pr = base + int64_t(orow) * W;
+      stg_stream2(pr + wg, make_float2(hl[0], hl[1]));
+      stg_stream2(pr + hgW, make_float2(lh[0], lh[1]));
+      stg_stream2(pr + hgW + wg, make_float2(hh[0], hh[1]));
+      *reinterpret_cast<float2*>(ll1 + orow * kLL1Pitch + 2 * q) = make_float2(ll[0], ll[1]);
+    }
+  }
+  __syncwarp();
+  release();
+  // ---- levels 2 + 3: two lanes per 4 x 4 LL1 block (br, bc), lane h takes LL1 columns 2h, 2h+1
+  const int blk = lane >> 1, h = lane & 1, br = blk >> 2, bc = blk & 3;
+  float l3;
+  {
+    float x[4][2];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float2 v = *reinterpret_cast<const float2*>(ll1 + (4 * br + r) * kLL1Pitch + 4 * bc + 2 * h);
+      x[r][0] = v.x;
+      x[r][1] = v.y;
+    }
+    float ll[2];
+    const int64_t wg = W >> 2, hgW = (H >> 2) * W;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {   // level 2: row 2br + i, column 2bc + h of the warp's level-2 block
+      const float a = x[2 * i][0], bb = x[2 * i][1], c = x[2 * i + 1][0], d = x[2 * i + 1][1];
+      const float s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+      ll[i] = (s1 + s2) * 0.5f;
+      float* pr = p.out + (b * H + (row0 >> 2) + 2 * br + i) * W + (col0 >> 2) + 8 * w + 2 * bc + h;
+      stg_stream1(pr + wg, (d1 + d2) * 0.5f);
+      stg_stream1(pr + hgW, (s1 - s2) * 0.5f);
+      stg_stream1(pr + hgW + wg, (d1 - d2) * 0.5f);
+    }
+    const float o0 = __shfl_xor_sync(0xffffffffu, ll[0], 1), o1 = __shfl_xor_sync(0xffffffffu, ll[1], 1);
+    // level 3 on the 2 x 2 LL2 block (lane h = 0): a = (0, 0), b = (0, 1), c = (1, 0), d = (1, 1)
+    const float a = ll[0], bb = o0, c = ll[1], d = o1;
+    const float s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+    l3 = (s1 + s2) * 0.5f;
+    if (h == 0) {
+      const int64_t wg3 = W >> 3, hgW3 = (H >> 3) * W;
+      float* pr = p.out + (b * H + (row0 >> 3) + br) * W + (col0 >> 3) + 4 * w + bc;
+      stg_stream1(pr + wg3, (d1 + d2) * 0.5f);
+      stg_stream1(pr + hgW3, (s1 - s2) * 0.5f);
+      stg_stream1(pr + hgW3 + wg3, (d1 - d2) * 0.5f);
+    }
+  }
+  // ---- level 4 (fp64) on the 2 x 2 blocks of the warp's 4 x 4 LL3 (held by lanes 2 * (4 br + bc))
+  {
+    const double a = double(l3);
+    const double bb = double(__shfl_down_sync(0xffffffffu, l3, 2));    // (br, bc + 1)
+    const double c = double(__shfl_down_sync(0xffffffffu, l3, 8));     // (br + 1, bc)
+    const double d = double(__shfl_down_sync(0xffffffffu, l3, 10));    // (br + 1, bc + 1)
+    const double s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+    const double ll4 = (s1 + s2) * 0.5;
+    const bool act4 = h == 0 && (br & 1) == 0 && (bc & 1) == 0;   // lanes 0, 4, 16, 20
+    if (act4) {
+      const int64_t wg4 = W >> 4, hgW4 = (H >> 4) * W;
+      float* pr = p.out + (b * H + (row0 >> 4) + (br >> 1)) * W + (col0 >> 4) + 2 * w + (bc >> 1);
+      stg_stream1(pr + wg4, float((d1 + d2) * 0.5));
+      stg_stream1(pr + hgW4, float((s1 - s2) * 0.5));
+      stg_stream1(pr + hgW4 + wg4, float((d1 - d2) * 0.5));
+    }
+    // ---- level 5 on the 2 x 2 LL4 (lanes 0, 4, 16, 20) -> lane 0
+    const double a5 = ll4;
+    const double b5 = __shfl_down_sync(0xffffffffu, ll4, 4);
+    const double c5 = __shfl_down_sync(0xffffffffu, ll4, 16);
+    const double d5 = __shfl_down_sync(0xffffffffu, ll4, 20);
+    if (lane == 0) {
+      const double t1 = a5 + b5, t2 = c5 + d5, e1 = a5 - b5, e2 = c5 - d5;
+      const int64_t wg5 = W >> 5, hgW5 = (H >> 5) * W;
+      float* pr = p.out + (b * H + (row0 >> 5)) * W + (col0 >> 5) + w;
+      stg_stream1(pr + wg5, float((e1 + e2) * 0.5));
+      stg_stream1(pr + hgW5, float((t1 - t2) * 0.5));
+      stg_stream1(pr + hgW5 + wg5, float((e1 - e2) * 0.5));
+      const double ll5 = (t1 + t2) * 0.5;
+      if (p.final_pass) {
+        stg_stream1(pr, float(ll5));
+      } else {   // fp64 hand-off of LL5 to the coarse levels (pitch = padded Win >> 5)
+        const int64_t wpitch = ((p.Win >> 5) + 3) & ~int64_t(3);
+        p.ws_out[(b * (p.Hin >> 5) + (row0 >> 5)) * wpitch + (col0 >> 5) + w] = ll5;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWsThreads, 2) ana2d_ws_kernel(const __grid_constant__ Ana2dParams p,
+                                                                 const __grid_constant__ CUtensorMap in_map) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* empty = full + p.stages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    prefetch_tmap(&in_map);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWsComputeWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t ntiles = uint32_t(p.ntiles), grid = gridDim.x;
+  if (warp == kWsComputeWarps) {   // producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int it = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += grid, ++it) {
+        const int s = it % p.stages;
+        if (it >= p.stages) mbar_wait(&empty[s], uint32_t(it / p.stages - 1) & 1u);
+        ws_issue(p, &in_map, smem + s * p.stage_bytes, &full[s], t, pol);
+      }
+    }
+  } else {
+    float* ll1 = reinterpret_cast<float*>(smem + p.p_off[0]) + warp * (16 * kLL1Pitch);
+    int it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += grid, ++it) {
+      const int s = it % p.stages;
+      mbar_wait(&full[s], uint32_t(it / p.stages) & 1u);
+      const uint32_t rt = t / uint32_t(p.tiles_c), ct = t - rt * uint32_t(p.tiles_c);
+      const uint32_t b = rt / uint32_t(p.tiles_r);
+      const int64_t row0 = int64_t(rt - b * uint32_t(p.tiles_r)) * 32, col0 = int64_t(ct) * 256;
+      uint64_t* e = &empty[s];
+      ws_block(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), ll1, b, row0, col0, warp, lane, [&] {
+        if (lane == 0) mbar_arrive(e);
+      });
+    }
+  }
+  if (p.tail > 0) {   // cooperative launch: every CTA is resident, so the grid barrier is safe
+    cooperative_groups::this_grid().sync();
+    if (p.tail == 1) ana_coarse<1>(p);
+    else if (p.tail == 2) ana_coarse<2>(p);
+    else ana_coarse<3>(p);
+  }
+}
+
+}  // namespace
+
+int ana2d_ws_threads() { return kWsThreads; }
+
+// shared memory: stages x 32 KB | 8 x 1 KB LL1 scratch | full[stages], empty[stages]
+size_t ana2d_ws_smem(int stages, uint32_t* ll1_off, uint32_t* bar_off) {
+  *ll1_off = uint32_t(stages) * 32768u;
+  *bar_off = *ll1_off + kWsComputeWarps * 16 * kLL1Pitch * 4;
+  return size_t(*bar_off) + 16 * size_t(stages);
+}
+
+cudaError_t ana2d_ws_occupancy(size_t smem, int* blocks_per_sm) {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute((const void*)ana2d_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (const void*)ana2d_ws_kernel, kWsThreads, smem);
+}
+
+cudaError_t launch_ana2d_ws(const Ana2dParams& p, const CUtensorMap& in_map, int grid, size_t smem, cudaStream_t s) {
+  count_launch();
+  void* args[] = {const_cast<Ana2dParams*>(&p), const_cast<CUtensorMap*>(&in_map)};
+  if (p.tail > 0)
+    return cudaLaunchCooperativeKernel((const void*)ana2d_ws_kernel, dim3(grid), dim3(kWsThreads), args, smem, s);
+  return cudaLaunchKernel((const void*)ana2d_ws_kernel, dim3(grid), dim3(kWsThreads), args, smem, s);
+}
+
+}  // namespace fhwt

@@ -537,7 +537,7 @@ def test_long_signal_segments_bitwise_equal(world):
             assert torch.equal(seg[lo:lo + ln], full[go:go + ln]), (r, band)
 
 
-@pytest.mark.parametrize("knob,values", [("FHWT_ANA_FUSED", ["1", "0", "3", "6"]),
+@pytest.mark.parametrize("knob,values", [("FHWT_ANA_FUSED", ["1", "0", "3", "6", "8"]),
                                          ("FHWT_SYN_MODE", ["0", "2", "3"]),
                                          ("FHWT_COOP", ["1", "0"])])
 @pytest.mark.parametrize("levels", [1, 3, 5, 7])
@@ -561,6 +561,26 @@ def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
         assert torch.equal(c, outs[0][0]) and torch.equal(r, outs[0][1])
     assert_close(host(outs[0][0]), o.analyze_2d(x, levels), x, 2, what=f"variants L={levels}")
     assert_close(host(outs[0][1]), x, x, 2, what=f"variants round trip L={levels}")
+
+
+@pytest.mark.parametrize("shape,levels", [((4, 512, 2048), 5), ((4, 512, 2048), 7), ((1, 2048, 4096), 8),
+                                          ((8, 256, 1024), 6), ((300, 32, 256), 5)])
+@pytest.mark.parametrize("stages", ["2", "3"])
+def test_warp_specialised_analysis_bitwise(monkeypatch, capfd, shape, levels, stages):
+    """K1 v2 (haar2d_ana.cu, FHWT_ANA_FUSED=8): warp-local levels 1-5 of 32 x 32 blocks with a TMA
+    producer warp gives the default kernel's coefficients bitwise, with and without the cooperative
+    coarse levels (L = 6..8); the debug line proves the variant ran."""
+    x = dev(datagen.uniform(shape, seed=levels + 17, lo=-1.0, hi=2.0))
+    ref = fhwt.analyze_2d(x, levels)
+    monkeypatch.setenv("FHWT_ANA_FUSED", "8")
+    monkeypatch.setenv("FHWT_ANA_STAGES", stages)
+    monkeypatch.setenv("FHWT_DEBUG_LAUNCH", "1")
+    c = fhwt.analyze_2d(x, levels)
+    torch.cuda.synchronize()
+    assert "ana2d ws8" in capfd.readouterr().err
+    assert torch.equal(c, ref)
+    if levels <= 5:
+        assert_close(host(c), o.analyze_2d(host(x), levels), host(x), 2, what="ws8 vs oracle")
 
 
 @pytest.mark.parametrize("batch,n,levels", [(16, 2048, 11), (8, 4096, 12), (8, 4096, 11), (4, 8192, 13),

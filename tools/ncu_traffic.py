@@ -1,12 +1,15 @@
 """profiles/ncu_traffic.json from `ncu -i REPORT --page raw --csv` exports of full-size captures
-(tools/profile_case.py c4 256 / c2 4096 / c5 32768): per kernel, DRAM bytes per launch next to
-the algorithmic bytes (8 B per sample per transform).  bench.py reads the result as `traffic`.
+(tools/profile_case.py c4 256 / c2 4096 / c5 32768): per kernel, the SURVEY §8(d) step-5 counters —
+DRAM bytes per launch next to the algorithmic bytes (8 B per sample per transform), DRAM
+throughput as % of peak, global store sectors per request, shared-memory bank conflicts.  bench.py
+reads `dram_bytes_per_launch` as the roofline's `traffic`.
 python tools/ncu_traffic.py out.json c4=raw_c4.csv [c2=raw_c2.csv c5=raw_c5.csv]"""
 import csv
 import json
 import sys
 
 SAMPLES = {"c4": 256 * 2048 * 2048, "c2": 4096 * 65536, "c5": 32768 * 32768}
+SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "ms": 1, "us": 1e-3, "ns": 1e-6}
 
 
 def kind(name):
@@ -18,8 +21,12 @@ def kind(name):
 
 
 def main(out, *specs):
-    res = {"_source": "ncu --set full --clock-control none on tools/profile_case.py <workload> at full size; "
-                      "dram__bytes_read.sum + dram__bytes_write.sum per launch (largest launch of each kind)"}
+    res = {"_source": "ncu --set full --clock-control none on tools/profile_case.py <workload> at full size "
+                      "(largest launch of each kind); dram bytes = dram__bytes_read.sum + dram__bytes_write.sum, "
+                      "dram_throughput_pct = gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed, "
+                      "store sectors/request = l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum / "
+                      "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum (4 = full 128-B lines per request), "
+                      "smem bank conflicts = l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_{ld,st}.sum"}
     for spec in specs:
         wl, path = spec.split("=")
         rows = list(csv.reader(open(path)))
@@ -27,9 +34,13 @@ def main(out, *specs):
         col = {k: i for i, k in enumerate(hdr)}
 
         def val(r, k):
-            u = units[col[k]]
-            v = float(r[col[k]].replace(",", ""))
-            return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "ms": 1, "us": 1e-3}.get(u, 1)
+            if k not in col or not r[col[k]]:
+                return None
+            return float(r[col[k]].replace(",", "")) * SCALE.get(units[col[k]], 1)
+
+        def ratio(r, a, b):
+            x, y = val(r, a), val(r, b)
+            return x / y if x is not None and y else None
 
         best = {}
         for r in rows[2:]:
@@ -40,12 +51,25 @@ def main(out, *specs):
             rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
             if k not in best or rd + wr > best[k]["dram_bytes_per_launch"]:
                 alg = 8 * SAMPLES[wl]
-                best[k] = {"kernel": name, "dram_bytes_per_launch": rd + wr, "dram_read_bytes_per_launch": rd,
-                           "dram_write_bytes_per_launch": wr, "algorithmic_bytes_per_launch": alg,
-                           "traffic_over_algorithmic": (rd + wr) / alg,
-                           "ncu_duration_ms": val(r, "gpu__time_duration.sum"),
-                           "dram_throughput_pct": r[col.get("dram__throughput.avg.pct_of_peak_sustained_elapsed",
-                                                            col["gpu__time_duration.sum"])]}
+                best[k] = {
+                    "kernel": name, "dram_bytes_per_launch": rd + wr, "dram_read_bytes_per_launch": rd,
+                    "dram_write_bytes_per_launch": wr, "algorithmic_bytes_per_launch": alg,
+                    "traffic_over_algorithmic": (rd + wr) / alg,
+                    "ncu_duration_ms": val(r, "gpu__time_duration.sum"),
+                    "dram_throughput_pct": val(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                    "global_store_sectors_per_request": ratio(r, "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum",
+                                                              "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum"),
+                    "global_load_sectors_per_request": ratio(r, "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+                                                             "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"),
+                    "l2_write_sectors_per_request": ratio(r, "lts__t_sectors_srcunit_tex_op_write.sum",
+                                                          "lts__t_requests_srcunit_tex_op_write.sum"),
+                    "smem_bank_conflicts_ld": val(r, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"),
+                    "smem_bank_conflicts_st": val(r, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum"),
+                    "smem_wavefronts_ld": val(r, "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"),
+                    "smem_wavefronts_st": val(r, "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum"),
+                    "registers_per_thread": val(r, "launch__registers_per_thread"),
+                    "issue_active_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                }
         res[wl] = best
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
