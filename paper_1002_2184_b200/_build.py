@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["fhwt_api.cu", "haar2d.cu", "haar2d_ana.cu", "haar2d_small.cu", "haar1d.cu", "direct.cu", "lowpass.cu"]
+SOURCES = ["fhwt_api.cu", "haar2d.cu", "haar2d_ana.cu", "haar2d_syn.cu", "haar2d_small.cu", "haar1d.cu", "direct.cu", "lowpass.cu"]
 LIB = os.path.join(HERE, "libfhwt.so")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -550,8 +550,30 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
                         p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows;
     // FHWT_ANA_FUSED=8: warp-specialised kernel (haar2d_ana.cu): 8 compute warps, each all five
     // levels of its own 32 x 32 block, plus a TMA producer warp; no CTA barrier per tile
-    const bool ws8 = fast_ok && p.fused == 8 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 && p.mask_mode == 0 &&
-                     p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows;
+    const bool ws8 = fast_ok && (p.fused == 8 || p.fused == 7) && ps.Lp == 5 && p.TR == 32 && p.TC == 256 &&
+                     p.mask_mode == 0 && p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows;
+    // FHWT_ANA_FUSED=7: the default fused tile chain with a dedicated TMA producer warp
+    if (ws8) p.row_boxes = env_int("FHWT_ANA_POLL", 0) ? 2 : 1;   // 2: producer polls (test_wait)
+    if (ws8 && p.fused == 7) {
+      p.stages = env_int("FHWT_ANA_STAGES", 2);
+      p.p_off[0] = uint32_t(p.stages) * 32768u;            // LL3, 4 x 32 fp32
+      p.p_off[1] = p.p_off[0] + 512u;                      // LL1, 16 x 128 fp32
+      p.bar_off = p.p_off[1] + 8192u;                      // full[stages], empty[stages]
+      const size_t fsmem = size_t(p.bar_off) + 16 * size_t(p.stages);
+      int fbps = 0;
+      FHWT_CUDA(ana2d_fp_occupancy(fsmem, &fbps), "fp occupancy");
+      if (fbps < 1) return fail(FHWT_ERR_CUDA, "producer-warp analysis does not fit (%zu B)", fsmem);
+      if (const int cap = env_int("FHWT_ANA_CTAS_PER_SM", 0)) fbps = std::min(fbps, cap);
+      const int64_t fgrid = std::min<int64_t>(p.ntiles, int64_t(fbps) * di.sms);
+      const bool fcoop = k == 0 && np == 2 && pl->passes[1].Lp <= 3 && env_int("FHWT_COOP", 1) != 0;
+      p.tail = fcoop ? pl->passes[1].Lp : 0;
+      if (env_int("FHWT_DEBUG_LAUNCH", 0))
+        std::fprintf(stderr, "[fhwt] ana2d fp7 stages %d smem %zu B ctas/SM %d grid %lld tail %d\n", p.stages, fsmem,
+                     fbps, (long long)fgrid, p.tail);
+      FHWT_CUDA(launch_ana2d_fp(p, map, int(fgrid), fsmem, s), "ana2d fp launch");
+      if (fcoop) break;
+      continue;
+    }
     if (ws8) {
       p.stages = env_int("FHWT_ANA_STAGES", 2);
       uint32_t ll1_off = 0, bar_off = 0;
@@ -707,6 +729,28 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       parts[0] = {0, p.Win / p.TC, true};
       parts[1] = {p.Win / p.TC, 1, false};
       nparts = 2;
+    }
+    // FHWT_SYN_MODE=7 (haar2d_syn.cu): level-1 bands copied by each warp into its private slice,
+    // coarse boxes by TMA; 32 x 256 full tiles of a 5-level first pass (c4, c5)
+    if (env_int("FHWT_SYN_MODE", 3) == 7 && kk == 0 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 && aligned &&
+        !ragged && !shifted && !p.clamp_rows && p.out_pitch == W) {
+      p.ct0 = 0;
+      p.stages = env_int("FHWT_SYN_STAGES", 2);
+      const size_t wsm = syn2d_wp_layout(&p);
+      int wbps = 0;
+      FHWT_CUDA(syn2d_wp_occupancy(wsm, &wbps), "syn wp occupancy");
+      if (wbps < 1) return fail(FHWT_ERR_CUDA, "warp-private synthesis does not fit (%zu B)", wsm);
+      if (const int cap = env_int("FHWT_CTAS_PER_SM", 0)) wbps = std::min(wbps, cap);
+      const int64_t wgrid = std::min<int64_t>(p.ntiles, int64_t(wbps) * di.sms);
+      if (coop) {
+        p.head = pl->passes[1].Lp;
+        p.ll_ws_out = reinterpret_cast<float*>(ws + pl->ws_off[0]);
+      }
+      if (env_int("FHWT_DEBUG_LAUNCH", 0))
+        std::fprintf(stderr, "[fhwt] syn2d wp7 stages %d smem %zu B ctas/SM %d grid %lld head %d\n", p.stages, wsm,
+                     wbps, (long long)wgrid, p.head);
+      FHWT_CUDA(launch_syn2d_wp(p, maps, int(wgrid), wsm, s), "syn2d wp launch");
+      continue;
     }
     for (int part = 0; part < nparts; ++part) {
       const bool full = parts[part].full;

@@ -132,6 +132,14 @@ int ana2d_ws_threads();
 size_t ana2d_ws_smem(int stages, uint32_t* ll1_off, uint32_t* bar_off);
 cudaError_t ana2d_ws_occupancy(size_t smem, int* blocks_per_sm);
 cudaError_t launch_ana2d_ws(const Ana2dParams& p, const CUtensorMap& in_map, int grid, size_t smem, cudaStream_t s);
+// Synthesis with warp-private level-1 slices (haar2d_syn.cu, FHWT_SYN_MODE=7): 32 x 256 tiles, LP = 5
+size_t syn2d_wp_layout(Syn2dParams* p);   // fills box_off, p_off, stage_bytes, bar_off; returns smem bytes
+cudaError_t syn2d_wp_occupancy(size_t smem, int* blocks_per_sm);
+cudaError_t launch_syn2d_wp(const Syn2dParams& p, const TmaMaps2d& maps, int grid, size_t smem, cudaStream_t s);
+// The default fused tile chain with a dedicated TMA producer warp (haar2d_ana.cu, FHWT_ANA_FUSED=7)
+int ana2d_fp_threads();
+cudaError_t ana2d_fp_occupancy(size_t smem, int* blocks_per_sm);
+cudaError_t launch_ana2d_fp(const Ana2dParams& p, const CUtensorMap& in_map, int grid, size_t smem, cudaStream_t s);
 cudaError_t syn2d_occupancy(int fast_lp, size_t smem, int* blocks_per_sm);
 // f64all (first pass of a decomposition deeper than 10 levels): levels 1-3 in fp64 too, so the only
 // error left is the final rounding of each output (the 1-D reading R14)

@@ -50,6 +50,27 @@ __device__ __forceinline__ int64_t tile_row0(const P& p, int64_t rt) {
   return (p.clamp_rows && r + p.TR > p.Hin) ? p.Hin - p.TR : r;
 }
 
+// Phase timing of the fused analysis tile chain (diagnostic build only: -DFHWT_PHASE_TIMING, see
+// tools/phase_timing.py).  Thread 0 (warp 0) and thread 224 (warp 7, the levels-4+5 lanes) add the
+// clock64() cycles of each phase of every tile to g_phase[16 * w + k]; the default build has no trace of it.
+#ifdef FHWT_PHASE_TIMING
+__device__ unsigned long long g_phase[32];
+__device__ __forceinline__ void phase_mark(int k) {
+  __shared__ long long last[2];
+  const int t = threadIdx.x;
+  if (t == 0 || t == 224) {
+    const int w = t ? 1 : 0;
+    const long long now = clock64();
+    if (k >= 0) atomicAdd(&g_phase[16 * w + k], (unsigned long long)(now - last[w]));
+    if (k == 0) atomicAdd(&g_phase[16 * w + 15], 1ull);
+    last[w] = now;
+  }
+}
+#define FHWT_PHASE(k) phase_mark(k)
+#else
+#define FHWT_PHASE(k) ((void)0)
+#endif
+
 // Threads per CTA of a compile-time fast variant: one 2 x 2V unit per thread on level 1 of the
 // smallest tiles (8 x 128: 64 threads), so small-tile shapes (e.g. 1080-row frames) run many
 // independent CTAs per SM instead of a few latency-bound 256-thread ones; 256 from 32 x 128 up.
@@ -357,8 +378,11 @@ __device__ __forceinline__ void ana_fused_tile(const Ana2dParams& p, const float
   float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]);   // 16 x 128
   float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);   // 4 x 32
   ana_level<float, float, 2, 32, 256, true>(p, stage, 32, 256, 1, b, row0, col0, ll1, false);
+  FHWT_PHASE(1);
   __syncthreads();
+  FHWT_PHASE(2);
   refill();
+  FHWT_PHASE(3);
   const int tid = threadIdx.x;
   if (p.fused == 6) {   // levels 2 + 3 over all 256 threads: two lanes per 4 x 4 LL1 block, level 3
                         // after a lane-pair shuffle of the LL2 columns
@@ -412,8 +436,10 @@ __device__ __forceinline__ void ana_fused_tile(const Ana2dParams& p, const float
     const float l3 = ana_pair<float, float, 2, LP>(p, x, b, row0, col0, br, bc);
     if constexpr (LP > 3) ll3[br * 32 + bc] = l3;
   }
+  FHWT_PHASE(4);
   if constexpr (LP > 3) {
     __syncthreads();
+    FHWT_PHASE(5);
     if (tid >= 224 && tid < 232) {   // levels 4 (+ 5): warp 7 lanes 0..7, block q of LL3 (4 x 32)
       const int q = tid - 224;
       float x[4][4];
@@ -424,6 +450,7 @@ __device__ __forceinline__ void ana_fused_tile(const Ana2dParams& p, const float
       }
       if constexpr (LP == 5) {
         ana_pair<double, double, 4, 5>(p, x, b, row0, col0, 0, q);
+        FHWT_PHASE(6);
       } else {   // LP == 4: level 4 only, on the two 2 x 4 halves of the block
         const int64_t W = p.W;
 #pragma unroll
@@ -449,47 +476,6 @@ __device__ __forceinline__ void ana_fused_tile(const Ana2dParams& p, const float
           stg_stream2(pr + hgW + wg, make_float2(hh[0], hh[1]));
           if (p.final_pass) stg_stream2(pr, make_float2(llv[0], llv[1]));
         }
-      }
-    }
-  }
-}
-
-// Synthesis mirror: one lane per 2 x 2 quad of LL5; the lane walks its own path down from
-// LL_{5+T} (recomputing the few shared upper butterflies instead of exchanging them) and writes
-// its quad of the fp32 LL5 hand-off, the input of the tile phase.  Same fp32 operations as the
-// level-by-level pass.
-template <int T>
-__device__ __forceinline__ void syn_coarse(const Syn2dParams& p) {
-  constexpr int Q = 1 << (T - 1), G = Q * Q;
-  const int64_t hl = p.H >> 5, wl = p.W >> 5, wp = (wl + 3) & ~int64_t(3);
-  const int64_t rc = wl >> T, per = (hl >> T) * rc, total = p.batch * per * G;
-  const int64_t W = p.W;
-  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = q / G, t = q - r * G;
-    const int64_t b = r / per, rem = r - b * per, by = rem / rc, bx = rem - by * rc;
-    const int64_t y6 = by * Q + t / Q, x6 = bx * Q + (t % Q);
-    float bhl[T], blh[T], bhh[T];   // bands along the path, level 5+T first (all loads up front)
-#pragma unroll
-    for (int i = 0; i < T; ++i) {
-      const int g = 5 + T - i;
-      const float* pr = p.coeffs + (b * p.H + (y6 >> (g - 6))) * W + (x6 >> (g - 6));
-      bhl[i] = pr[W >> g];
-      blh[i] = pr[(p.H >> g) * W];
-      bhh[i] = pr[(p.H >> g) * W + (W >> g)];
-    }
-    float ll = p.coeffs[(b * p.H + by) * W + bx];
-#pragma unroll
-    for (int i = 0; i < T; ++i) {
-      const int g = 5 + T - i;
-      const float s = ll + blh[i], tt = bhl[i] + bhh[i], s2 = ll - blh[i], t2 = bhl[i] - bhh[i];
-      const float t0 = (s + tt) * 0.5f, t1 = (s - tt) * 0.5f, b0 = (s2 + t2) * 0.5f, b1 = (s2 - t2) * 0.5f;
-      if (i == T - 1) {   // level 6 -> this lane's 2 x 2 quad of LL5
-        float* o = p.ll_ws_out + (b * hl + 2 * y6) * wp + 2 * x6;
-        *reinterpret_cast<float2*>(o) = make_float2(t0, t1);
-        *reinterpret_cast<float2*>(o + wp) = make_float2(b0, b1);
-      } else {           // child of LL_g on this lane's path: position at level g - 1
-        const int cy = int(y6 >> (g - 7)) & 1, cx = int(x6 >> (g - 7)) & 1;
-        ll = cy ? (cx ? b1 : b0) : (cx ? t1 : t0);
       }
     }
   }
@@ -613,9 +599,12 @@ __device__ __forceinline__ void ana2d_tiles(const Ana2dParams& p, const CUtensor
     }
   }
   int it = 0;
+  FHWT_PHASE(-1);
   for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
     const int s = it % p.stages;
+    FHWT_PHASE(7);
     mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+    FHWT_PHASE(0);
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
     const int64_t row0 = CLAMPR ? tile_row0(p, rt - b * p.tiles_r) : (rt - b * p.tiles_r) * p.TR;
@@ -1241,11 +1230,15 @@ int grid_for(int64_t total, int threads) {
 
 // The dynamic-smem cap is raised to the device's opt-in maximum (not to `smem`), so a cached
 // occupancy answer for a small configuration never leaves the cap below a later, larger launch.
+// (minus the kernel's static shared memory, which shares the same per-block budget)
 static cudaError_t raise_smem_cap(const void* fn) {
   int dev = 0, optin = 0;
+  cudaFuncAttributes fa{};
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, fn);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - int(fa.sharedSizeBytes));
   return e;
 }
 
@@ -1412,6 +1405,17 @@ cudaError_t launch_pack_ll_peers(const float* c, float* const* peers, int rank, 
                                                                                              w, batch, levels);
   return cudaGetLastError();
 }
+
+#ifdef FHWT_PHASE_TIMING
+extern "C" int fhwt_debug_phases(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_phase, sizeof(g_phase)) != cudaSuccess) return -1;
+  if (reset) {
+    static const unsigned long long zero[32] = {};
+    if (cudaMemcpyToSymbol(g_phase, zero, sizeof(zero)) != cudaSuccess) return -1;
+  }
+  return 32;
+}
+#endif
 
 cudaError_t launch_pack_ll(const float* c, float* ll, int64_t h, int64_t w, int64_t batch, int levels,
                            cudaStream_t s) {

@@ -37,6 +37,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Producer-side wait on an "empty" barrier by polling mbarrier.test_wait (never suspends the warp)
+// instead of the try_wait loop: the refill should leave as soon as the consumers release the stage.
+__device__ __forceinline__ void mbar_wait_poll(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
 // Producer: the 32 one-row boxes of tile t (32-bit tile decode: a tile holds 8192 pixels, so tile
 // counts are < 2^31 for any buffer the TMA row range admits).
 __device__ __forceinline__ void ws_issue(const Ana2dParams& p, const CUtensorMap* map, unsigned char* dst,
@@ -180,7 +193,12 @@ __global__ void __launch_bounds__(kWsThreads, 2) ana2d_ws_kernel(const __grid_co
       int it = 0;
       for (uint32_t t = blockIdx.x; t < ntiles; t += grid, ++it) {
         const int s = it % p.stages;
-        if (it >= p.stages) mbar_wait(&empty[s], uint32_t(it / p.stages - 1) & 1u);
+        if (it >= p.stages) {
+          if (p.row_boxes == 2)
+            mbar_wait_poll(&empty[s], uint32_t(it / p.stages - 1) & 1u);
+          else
+            mbar_wait(&empty[s], uint32_t(it / p.stages - 1) & 1u);
+        }
         ws_issue(p, &in_map, smem + s * p.stage_bytes, &full[s], t, pol);
       }
     }
@@ -207,7 +225,190 @@ __global__ void __launch_bounds__(kWsThreads, 2) ana2d_ws_kernel(const __grid_co
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Fused tile chain with a dedicated TMA producer warp (FHWT_ANA_FUSED=7).  The compute side is the
+// default kernel's (haar2d.cu ana_fused_tile, 32 x 256 tiles, LP = 5): level 1 by all 256 compute
+// threads (a warp stores 256-B row segments of every band), a barrier, levels 2+3 by warps 0-3
+// (one 4 x 4 LL1 block per thread), a barrier, levels 4+5 in fp64 by 8 lanes of warp 7, which
+// overlap the next tile's level 1.  What changes is the refill: the default kernel's warp 0 issues
+// the 32 one-row TMA boxes of the next tile between the two barriers, and with the TMA engine
+// busy that loop takes thousands of cycles (tools/phase_timing.py: ~6000 SM cycles per tile)
+// that the second barrier then waits for.  Here warp 8 issues them: the compute warps sync with
+// a named barrier of 256 threads (bar.sync 1, 256) that the producer never joins, thread 0 arrives
+// on the stage's "empty" mbarrier after the first barrier, and the producer waits on it.
+constexpr int kFpThreads = 256 + 32;
+
+__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// level J+1 on a 2 x 2 block of level-J LL values (same operands, order and types as haar2d.cu ana_pair)
+template <typename T>
+__device__ __forceinline__ T fp_quad(const Ana2dParams& p, T a, T bb, T c, T d, int64_t b, int64_t row, int64_t col, int g) {
+  const T s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+  const int64_t W = p.W, wg = W >> g, hgW = (p.H >> g) * W;
+  float* pr = p.out + (b * p.H + row) * W + col;
+  stg_stream1(pr + wg, float((d1 + d2) * T(0.5)));
+  stg_stream1(pr + hgW, float((s1 - s2) * T(0.5)));
+  stg_stream1(pr + hgW + wg, float((d1 - d2) * T(0.5)));
+  return (s1 + s2) * T(0.5);
+}
+
+// levels J, J+1 of one thread's 4 x 4 block x of level J-1 LL (haar2d.cu ana_pair, TA -> TB)
+template <typename TA, typename TB, int J>
+__device__ __forceinline__ TB fp_pair(const Ana2dParams& p, const float (&x)[4][4], int64_t b, int64_t row0,
+                                      int64_t col0, int br, int bc) {
+  const int64_t W = p.W;
+  TA ll[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    float hl[2], lh[2], hh[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const TA a = TA(x[2 * i][2 * k]), bb = TA(x[2 * i][2 * k + 1]);
+      const TA c = TA(x[2 * i + 1][2 * k]), d = TA(x[2 * i + 1][2 * k + 1]);
+      const TA s1 = a + bb, s2 = c + d, d1 = a - bb, d2 = c - d;
+      ll[i][k] = (s1 + s2) * TA(0.5);
+      lh[k] = float((s1 - s2) * TA(0.5));
+      hl[k] = float((d1 + d2) * TA(0.5));
+      hh[k] = float((d1 - d2) * TA(0.5));
+    }
+    float* pr = p.out + (b * p.H + (row0 >> J) + 2 * br + i) * W + (col0 >> J) + 2 * bc;
+    const int64_t wg = W >> J, hgW = (p.H >> J) * W;
+    stg_stream2(pr + wg, make_float2(hl[0], hl[1]));
+    stg_stream2(pr + hgW, make_float2(lh[0], lh[1]));
+    stg_stream2(pr + hgW + wg, make_float2(hh[0], hh[1]));
+  }
+  return fp_quad<TB>(p, TB(ll[0][0]), TB(ll[0][1]), TB(ll[1][0]), TB(ll[1][1]), b, (row0 >> (J + 1)) + br,
+                     (col0 >> (J + 1)) + bc, J + 1);
+}
+
+__global__ void __launch_bounds__(kFpThreads, 2) ana2d_fp_kernel(const __grid_constant__ Ana2dParams p,
+                                                                 const __grid_constant__ CUtensorMap in_map) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* empty = full + p.stages;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    prefetch_tmap(&in_map);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t ntiles = uint32_t(p.ntiles), grid = gridDim.x;
+  if (tid >= 256) {   // producer warp
+    if (tid == 256) {
+      const uint64_t pol = policy_evict_first();
+      int it = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += grid, ++it) {
+        const int s = it % p.stages;
+        if (it >= p.stages) {
+          if (p.row_boxes == 2)
+            mbar_wait_poll(&empty[s], uint32_t(it / p.stages - 1) & 1u);
+          else
+            mbar_wait(&empty[s], uint32_t(it / p.stages - 1) & 1u);
+        }
+        ws_issue(p, &in_map, smem + s * p.stage_bytes, &full[s], t, pol);
+      }
+    }
+  } else {
+    float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]);   // 16 x 128
+    float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);   // 4 x 32
+    const int64_t W = p.W, H = p.H;
+    int it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += grid, ++it) {
+      const int s = it % p.stages;
+      mbar_wait(&full[s], uint32_t(it / p.stages) & 1u);
+      const uint32_t rt = t / uint32_t(p.tiles_c), ct = t - rt * uint32_t(p.tiles_c);
+      const uint32_t b = rt / uint32_t(p.tiles_r);
+      const int64_t row0 = int64_t(rt - b * uint32_t(p.tiles_r)) * 32, col0 = int64_t(ct) * 256;
+      const float* st = reinterpret_cast<const float*>(smem + s * p.stage_bytes);
+      {   // level 1: unit u = tid + 256 k -> (orow, oc) = (u / 64, 2 (u % 64)), a 2 x 4 input block
+        const int64_t wg = W >> 1, hgW = (H >> 1) * W;
+        float* const base = p.out + (int64_t(b) * H + (row0 >> 1)) * W + (col0 >> 1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int u = tid + 256 * k, orow = u >> 6, oc = 2 * (u & 63);
+          const float4 t0 = *reinterpret_cast<const float4*>(st + (2 * orow) * 256 + 2 * oc);
+          const float4 t1 = *reinterpret_cast<const float4*>(st + (2 * orow + 1) * 256 + 2 * oc);
+          const float a0[2] = {t0.x, t0.z}, b0[2] = {t0.y, t0.w}, c0[2] = {t1.x, t1.z}, d0[2] = {t1.y, t1.w};
+          float ll[2], hl[2], lh[2], hh[2];
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const float s1 = a0[v] + b0[v], s2 = c0[v] + d0[v], d1 = a0[v] - b0[v], d2 = c0[v] - d0[v];
+            ll[v] = (s1 + s2) * 0.5f;
+            lh[v] = (s1 - s2) * 0.5f;
+            hl[v] = (d1 + d2) * 0.5f;
+            hh[v] = (d1 - d2) * 0.5f;
+          }
+          float* pr = base + int64_t(orow) * W + oc;
+          stg_stream2(pr + wg, make_float2(hl[0], hl[1]));
+          stg_stream2(pr + hgW, make_float2(lh[0], lh[1]));
+          stg_stream2(pr + hgW + wg, make_float2(hh[0], hh[1]));
+          *reinterpret_cast<float2*>(ll1 + orow * 128 + oc) = make_float2(ll[0], ll[1]);
+        }
+      }
+      bar_compute();   // LL1 complete; every compute warp is done with the stage
+      if (tid == 0) mbar_arrive(&empty[s]);
+      if (tid < 128) {   // levels 2 + 3: block (br, bc) of LL1, 4 x 32 blocks
+        const int br = tid >> 5, bc = tid & 31;
+        float x[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float4 v = *reinterpret_cast<const float4*>(ll1 + (4 * br + r) * 128 + 4 * bc);
+          x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+        }
+        ll3[br * 32 + bc] = fp_pair<float, float, 2>(p, x, b, row0, col0, br, bc);
+      }
+      bar_compute();   // LL3 complete
+      if (tid >= 224 && tid < 232) {   // levels 4 + 5 (fp64): block q of LL3 (4 x 32)
+        const int q = tid - 224;
+        float x[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float4 v = *reinterpret_cast<const float4*>(ll3 + r * 32 + 4 * q);
+          x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+        }
+        const double ll5 = fp_pair<double, double, 4>(p, x, b, row0, col0, 0, q);
+        if (p.final_pass) {
+          stg_stream1(p.out + (int64_t(b) * H + (row0 >> 5)) * W + (col0 >> 5) + q, float(ll5));
+        } else {   // fp64 hand-off of LL5 to the coarse levels (pitch = padded Win >> 5)
+          const int64_t wpitch = ((p.Win >> 5) + 3) & ~int64_t(3);
+          p.ws_out[(int64_t(b) * (p.Hin >> 5) + (row0 >> 5)) * wpitch + (col0 >> 5) + q] = ll5;
+        }
+      }
+    }
+  }
+  if (p.tail > 0) {   // cooperative launch: every CTA is resident, so the grid barrier is safe
+    cooperative_groups::this_grid().sync();
+    if (p.tail == 1) ana_coarse<1>(p);
+    else if (p.tail == 2) ana_coarse<2>(p);
+    else ana_coarse<3>(p);
+  }
+}
+
 }  // namespace
+
+int ana2d_fp_threads() { return kFpThreads; }
+
+cudaError_t ana2d_fp_occupancy(size_t smem, int* blocks_per_sm) {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute((const void*)ana2d_fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (const void*)ana2d_fp_kernel, kFpThreads, smem);
+}
+
+cudaError_t launch_ana2d_fp(const Ana2dParams& p, const CUtensorMap& in_map, int grid, size_t smem, cudaStream_t s) {
+  count_launch();
+  void* args[] = {const_cast<Ana2dParams*>(&p), const_cast<CUtensorMap*>(&in_map)};
+  if (p.tail > 0)
+    return cudaLaunchCooperativeKernel((const void*)ana2d_fp_kernel, dim3(grid), dim3(kFpThreads), args, smem, s);
+  return cudaLaunchKernel((const void*)ana2d_fp_kernel, dim3(grid), dim3(kFpThreads), args, smem, s);
+}
 
 int ana2d_ws_threads() { return kWsThreads; }
 

@@ -1,4 +1,5 @@
-// Coarse analysis levels 6..5+T of the 2-D first pass (shared by haar2d.cu and haar2d_ana.cu).
+// Coarse levels 6..5+T of the 2-D first passes (analysis and synthesis), shared by haar2d.cu,
+// haar2d_ana.cu and haar2d_syn.cu.
 #pragma once
 
 #include "fhwt_internal.cuh"
@@ -56,6 +57,47 @@ __device__ __forceinline__ void ana_coarse(const Ana2dParams& p) {
         coarse_store3(p, g, b, y6 >> (g - 6), x6 >> (g - 6), ll, vr, vd, vdr, &ll);
     }
     if (valid && t == 0) stg_stream1(p.out + (b * p.H + by) * p.W + bx, float(ll));
+  }
+}
+
+// Synthesis mirror: one lane per 2 x 2 quad of LL5; the lane walks its own path down from
+// LL_{5+T} (recomputing the few shared upper butterflies instead of exchanging them) and writes
+// its quad of the fp32 LL5 hand-off, the input of the tile phase.  Same fp32 operations as the
+// level-by-level pass.
+template <int T>
+__device__ __forceinline__ void syn_coarse(const Syn2dParams& p) {
+  constexpr int Q = 1 << (T - 1), G = Q * Q;
+  const int64_t hl = p.H >> 5, wl = p.W >> 5, wp = (wl + 3) & ~int64_t(3);
+  const int64_t rc = wl >> T, per = (hl >> T) * rc, total = p.batch * per * G;
+  const int64_t W = p.W;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = q / G, t = q - r * G;
+    const int64_t b = r / per, rem = r - b * per, by = rem / rc, bx = rem - by * rc;
+    const int64_t y6 = by * Q + t / Q, x6 = bx * Q + (t % Q);
+    float bhl[T], blh[T], bhh[T];   // bands along the path, level 5+T first (all loads up front)
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      const int g = 5 + T - i;
+      const float* pr = p.coeffs + (b * p.H + (y6 >> (g - 6))) * W + (x6 >> (g - 6));
+      bhl[i] = pr[W >> g];
+      blh[i] = pr[(p.H >> g) * W];
+      bhh[i] = pr[(p.H >> g) * W + (W >> g)];
+    }
+    float ll = p.coeffs[(b * p.H + by) * W + bx];
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      const int g = 5 + T - i;
+      const float s = ll + blh[i], tt = bhl[i] + bhh[i], s2 = ll - blh[i], t2 = bhl[i] - bhh[i];
+      const float t0 = (s + tt) * 0.5f, t1 = (s - tt) * 0.5f, b0 = (s2 + t2) * 0.5f, b1 = (s2 - t2) * 0.5f;
+      if (i == T - 1) {   // level 6 -> this lane's 2 x 2 quad of LL5
+        float* o = p.ll_ws_out + (b * hl + 2 * y6) * wp + 2 * x6;
+        *reinterpret_cast<float2*>(o) = make_float2(t0, t1);
+        *reinterpret_cast<float2*>(o + wp) = make_float2(b0, b1);
+      } else {           // child of LL_g on this lane's path: position at level g - 1
+        const int cy = int(y6 >> (g - 7)) & 1, cx = int(x6 >> (g - 7)) & 1;
+        ll = cy ? (cx ? b1 : b0) : (cx ? t1 : t0);
+      }
+    }
   }
 }
 

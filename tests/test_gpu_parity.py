@@ -566,21 +566,43 @@ def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
 @pytest.mark.parametrize("shape,levels", [((4, 512, 2048), 5), ((4, 512, 2048), 7), ((1, 2048, 4096), 8),
                                           ((8, 256, 1024), 6), ((300, 32, 256), 5)])
 @pytest.mark.parametrize("stages", ["2", "3"])
-def test_warp_specialised_analysis_bitwise(monkeypatch, capfd, shape, levels, stages):
-    """K1 v2 (haar2d_ana.cu, FHWT_ANA_FUSED=8): warp-local levels 1-5 of 32 x 32 blocks with a TMA
-    producer warp gives the default kernel's coefficients bitwise, with and without the cooperative
-    coarse levels (L = 6..8); the debug line proves the variant ran."""
+@pytest.mark.parametrize("variant,tag", [("8", "ana2d ws8"), ("7", "ana2d fp7")])
+def test_warp_specialised_analysis_bitwise(monkeypatch, capfd, shape, levels, stages, variant, tag):
+    """The haar2d_ana.cu analysis kernels — FHWT_ANA_FUSED=8 (warp-local levels 1-5 of 32 x 32
+    blocks + TMA producer warp) and 7 (the default fused chain + TMA producer warp) — give the
+    default kernel's coefficients bitwise, with and without the cooperative coarse levels (L = 6..8);
+    the debug line proves the variant ran."""
     x = dev(datagen.uniform(shape, seed=levels + 17, lo=-1.0, hi=2.0))
     ref = fhwt.analyze_2d(x, levels)
-    monkeypatch.setenv("FHWT_ANA_FUSED", "8")
+    monkeypatch.setenv("FHWT_ANA_FUSED", variant)
     monkeypatch.setenv("FHWT_ANA_STAGES", stages)
     monkeypatch.setenv("FHWT_DEBUG_LAUNCH", "1")
     c = fhwt.analyze_2d(x, levels)
     torch.cuda.synchronize()
-    assert "ana2d ws8" in capfd.readouterr().err
+    assert tag in capfd.readouterr().err
     assert torch.equal(c, ref)
     if levels <= 5:
         assert_close(host(c), o.analyze_2d(host(x), levels), host(x), 2, what="ws8 vs oracle")
+
+
+@pytest.mark.parametrize("shape,levels", [((4, 512, 2048), 5), ((4, 512, 2048), 7), ((1, 2048, 4096), 8),
+                                          ((8, 256, 1024), 6), ((300, 32, 256), 5)])
+@pytest.mark.parametrize("stages", ["2", "3"])
+def test_warp_private_synthesis_bitwise(monkeypatch, capfd, shape, levels, stages):
+    """haar2d_syn.cu (FHWT_SYN_MODE=7): each warp copies its own level-1 band slice with cp.async,
+    the coarse boxes stay on TMA; the reconstruction equals the default kernel's bitwise, with and
+    without the cooperative coarse levels; the debug line proves the variant ran."""
+    x = dev(datagen.uniform(shape, seed=levels + 31, lo=-1.0, hi=2.0))
+    c = fhwt.analyze_2d(x, levels)
+    ref = fhwt.synthesize_2d(c, levels)
+    monkeypatch.setenv("FHWT_SYN_MODE", "7")
+    monkeypatch.setenv("FHWT_SYN_STAGES", stages)
+    monkeypatch.setenv("FHWT_DEBUG_LAUNCH", "1")
+    r = fhwt.synthesize_2d(c, levels)
+    torch.cuda.synchronize()
+    assert "syn2d wp7" in capfd.readouterr().err
+    assert torch.equal(r, ref)
+    assert_close(host(r), host(x), host(x), 2, what="wp7 round trip")
 
 
 @pytest.mark.parametrize("batch,n,levels", [(16, 2048, 11), (8, 4096, 12), (8, 4096, 11), (4, 8192, 13),

@@ -36,8 +36,11 @@ def membench(kind, x, y):
     B, H, W = x.shape
     vp, i64 = ctypes.c_void_p, ctypes.c_int64
     reps = int(os.environ.get("FHWT_TIMEIT_REPS", "10"))
-    if kind == "tma":
-        return _MB.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 296, 3, reps, 256, 1, 0)
+    if kind.startswith("tma"):   # tma[:box rows[:stages]]
+        parts = kind.split("/")
+        bh = int(parts[1]) if len(parts) > 1 else 1
+        st = int(parts[2]) if len(parts) > 2 else 3
+        return _MB.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 296, st, reps, 256, bh, 0)
     return _MB.mb_tile_ldg(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 592, reps)
 
 
@@ -108,7 +111,7 @@ def main():
                 t = timeit(lambda: c.copy_(x))
                 same[spec] = True
             elif spec.startswith("MB"):   # tools/membench.cu pattern: MB:tma | MB:ldg
-                t = membench(spec.split(":")[1], x, c)
+                t = membench(spec.split(":", 1)[1], x, c)
                 same[spec] = None
             elif spec.startswith("ANA"):
                 t = timeit(lambda: plan.analyze(x, out=c, workspace=ws))
