@@ -286,6 +286,7 @@ int choose_tr_first(int64_t rows, int Lp, int min_tr) {
 // use w itself (generic kernels).
 int choose_tc(int64_t w, int pref) {
   if (pref < 256) return int(std::min<int64_t>(pref, w));
+  if (pref == 512 && w % 512 == 0) return 512;   // synthesis sweep: 1-KB level-1 band rows (row boxes)
   if (w < 128) return env_int("FHWT_NARROW_FAST", 1) && w >= 16 && w % 16 == 0 ? 128 : int(w);   // one masked tile
   if (w % 256 == 0) return 256;
   // w % 256 == 128: 256-column tiles with the last one overlapping (clamp_last) when that repeats at
@@ -550,28 +551,27 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
                         p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows;
     // FHWT_ANA_FUSED=8: warp-specialised kernel (haar2d_ana.cu): 8 compute warps, each all five
     // levels of its own 32 x 32 block, plus a TMA producer warp; no CTA barrier per tile
-    const bool ws8 = fast_ok && (p.fused == 8 || p.fused == 7) && ps.Lp == 5 && p.TR == 32 && p.TC == 256 &&
+    const bool ws8 = fast_ok && (p.fused == 8 || p.fused == 11) && ps.Lp == 5 && p.TR == 32 &&
+                     p.TC == 256 &&
                      p.mask_mode == 0 && p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows;
-    // FHWT_ANA_FUSED=7: the default fused tile chain with a dedicated TMA producer warp
-    if (ws8) p.row_boxes = env_int("FHWT_ANA_POLL", 0) ? 2 : 1;   // 2: producer polls (test_wait)
-    if (ws8 && p.fused == 7) {
-      p.stages = env_int("FHWT_ANA_STAGES", 2);
-      p.p_off[0] = uint32_t(p.stages) * 32768u;            // LL3, 4 x 32 fp32
-      p.p_off[1] = p.p_off[0] + 512u;                      // LL1, 16 x 128 fp32
-      p.bar_off = p.p_off[1] + 8192u;                      // full[stages], empty[stages]
-      const size_t fsmem = size_t(p.bar_off) + 16 * size_t(p.stages);
-      int fbps = 0;
-      FHWT_CUDA(ana2d_fp_occupancy(fsmem, &fbps), "fp occupancy");
-      if (fbps < 1) return fail(FHWT_ERR_CUDA, "producer-warp analysis does not fit (%zu B)", fsmem);
-      if (const int cap = env_int("FHWT_ANA_CTAS_PER_SM", 0)) fbps = std::min(fbps, cap);
-      const int64_t fgrid = std::min<int64_t>(p.ntiles, int64_t(fbps) * di.sms);
-      const bool fcoop = k == 0 && np == 2 && pl->passes[1].Lp <= 3 && env_int("FHWT_COOP", 1) != 0;
-      p.tail = fcoop ? pl->passes[1].Lp : 0;
+    // FHWT_ANA_FUSED=11: the default chain with register (LDG) loads, no input staging
+    if (ws8 && p.fused == 11) {
+      p.in = d;
+      p.p_off[0] = 0;                                      // LL3, 4 x 32 fp32
+      p.p_off[1] = 512u;                                   // LL1, 16 x 128 fp32
+      const size_t lsmem = 512u + 8192u;
+      int lbps = 0;
+      const int lvar = env_int("FHWT_ANA_LDG", 0);
+      FHWT_CUDA(ana2d_ldg_occupancy(lsmem, &lbps, lvar), "ldg occupancy");
+      if (const int cap = env_int("FHWT_ANA_CTAS_PER_SM", 0)) lbps = std::min(lbps, cap);
+      const int64_t lgrid = std::min<int64_t>(p.ntiles, int64_t(std::max(lbps, 1)) * di.sms);
+      const bool lcoop = k == 0 && np == 2 && pl->passes[1].Lp <= 3 && env_int("FHWT_COOP", 1) != 0;
+      p.tail = lcoop ? pl->passes[1].Lp : 0;
       if (env_int("FHWT_DEBUG_LAUNCH", 0))
-        std::fprintf(stderr, "[fhwt] ana2d fp7 stages %d smem %zu B ctas/SM %d grid %lld tail %d\n", p.stages, fsmem,
-                     fbps, (long long)fgrid, p.tail);
-      FHWT_CUDA(launch_ana2d_fp(p, map, int(fgrid), fsmem, s), "ana2d fp launch");
-      if (fcoop) break;
+        std::fprintf(stderr, "[fhwt] ana2d ldg11 smem %zu B ctas/SM %d grid %lld tail %d\n", lsmem, lbps,
+                     (long long)lgrid, p.tail);
+      FHWT_CUDA(launch_ana2d_ldg(p, int(lgrid), lsmem, s, lvar), "ana2d ldg launch");
+      if (lcoop) break;
       continue;
     }
     if (ws8) {
@@ -634,7 +634,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     int tr = choose_tr(H, 5), tc = int(std::min<int64_t>(env_int("FHWT_SYN_TC", 256), W));
     if (tc == 256 && W % 256 && W % 128 == 0) tc = 128;
     shrink_for_small(B, H, W, 5, di.sms, &tr, &tc);
-    coop = tr == 32 && tc == 256 && W % 256 == 0;
+    coop = tr == 32 && ((tc == 256 && W % 256 == 0) || (tc == 512 && W % 512 == 0));
   }
   for (size_t kk = np; kk-- > 0;) {
     if (coop && kk == 1) continue;
@@ -702,8 +702,8 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
                          p.row_boxes[ps.Lp] ? 1 : p.TR >> ps.Lp));
     }
     // compile-time tile geometry (fast variants); full = no ragged edge and every box 16-B aligned
-    const bool geom = (p.TR == 32 || p.TR == 16 || p.TR == 8) && (p.TC == 256 || p.TC == 128) &&
-                      p.out_pitch % 4 == 0;
+    const bool geom = (p.TR == 32 || p.TR == 16 || p.TR == 8) &&
+                      (p.TC == 256 || p.TC == 128 || (p.TC == 512 && p.TR == 32)) && p.out_pitch % 4 == 0;
     bool aligned = geom && (W >> (ps.g0 + 1)) % 2 == 0;
     for (int j = 1; j <= ps.Lp; ++j) aligned = aligned && p.hoff[j] == 0 && bw[j] == (p.TC >> j);
     // A ragged width with aligned boxes runs as two launches: the full tiles on the fast path
@@ -764,7 +764,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       int mode = full ? env_int("FHWT_SYN_MODE", 3) : 0;
       if (mode != 0 && mode != 3) mode = 2;
       // warp-decoupled variant: 32 x 256 and 32 x 128 tiles (one warp per 32 columns)
-      if (mode == 3 && !(p.TR == 32 && (p.TC == 256 || (p.TC == 128 && warp128)))) mode = 2;
+      if (mode == 3 && !(p.TR == 32 && (p.TC == 256 || p.TC == 512 || (p.TC == 128 && warp128)))) mode = 2;
       if (shifted) mode = 6;
       // stage layout: LL box, then per level j three boxes (128-B aligned: TMA destinations need it;
       // with cp.async a 16-B packing would admit a 3rd CTA/SM, which measured slower: 5.54 vs 6.10 TB/s)

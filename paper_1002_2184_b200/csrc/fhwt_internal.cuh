@@ -52,6 +52,7 @@ struct Ana2dParams {
   int l2hint;            // 1: TMA loads carry an L2 evict_first policy (sweep knob FHWT_ANA_L2HINT)
   int row_boxes;         // 1: the map's box is one row and TR boxes are issued per tile (rows of
                          // 128-B multiples; TMA smem destinations must be 128-B aligned); 0: one TR-row box
+  const float* in;       // first-pass input (fp32 d), read directly by the register-load kernel (haar2d_ana.cu)
 };
 
 struct Syn2dParams {
@@ -136,10 +137,10 @@ cudaError_t launch_ana2d_ws(const Ana2dParams& p, const CUtensorMap& in_map, int
 size_t syn2d_wp_layout(Syn2dParams* p);   // fills box_off, p_off, stage_bytes, bar_off; returns smem bytes
 cudaError_t syn2d_wp_occupancy(size_t smem, int* blocks_per_sm);
 cudaError_t launch_syn2d_wp(const Syn2dParams& p, const TmaMaps2d& maps, int grid, size_t smem, cudaStream_t s);
-// The default fused tile chain with a dedicated TMA producer warp (haar2d_ana.cu, FHWT_ANA_FUSED=7)
-int ana2d_fp_threads();
-cudaError_t ana2d_fp_occupancy(size_t smem, int* blocks_per_sm);
-cudaError_t launch_ana2d_fp(const Ana2dParams& p, const CUtensorMap& in_map, int grid, size_t smem, cudaStream_t s);
+// ... and the same fused chain with register (LDG) loads, no input staging (FHWT_ANA_FUSED=11;
+// variant: 0 = 3 CTAs/SM, 1 = 4 CTAs/SM, 2 = next tile prefetched into registers at 2 CTAs/SM)
+cudaError_t ana2d_ldg_occupancy(size_t smem, int* blocks_per_sm, int variant);
+cudaError_t launch_ana2d_ldg(const Ana2dParams& p, int grid, size_t smem, cudaStream_t s, int variant);
 cudaError_t syn2d_occupancy(int fast_lp, size_t smem, int* blocks_per_sm);
 // f64all (first pass of a decomposition deeper than 10 levels): levels 1-3 in fp64 too, so the only
 // error left is the final rounding of each output (the 1-D reading R14)

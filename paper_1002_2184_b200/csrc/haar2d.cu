@@ -285,9 +285,8 @@ struct Refill {
   uint32_t bytes, row_bytes;
   uint64_t pol;   // must be warp-uniform (computed by every thread): a divergent cache-hint operand
                   // makes each TMA issue a waterfall loop (analysis 6.57 -> 6.15 TB/s)
-  unsigned issue_warp = 0;   // the warp whose lane 0 issues the refill
   __device__ __forceinline__ void operator()() const {
-    if ((threadIdx.x >> 5) == issue_warp && next < p->ntiles)
+    if (threadIdx.x < 32 && next < p->ntiles)
       ana_issue_tile<CLAMPR, U32>(*p, map, dst, bar, next, bytes, row_bytes, pol);
   }
 };
@@ -608,10 +607,8 @@ __device__ __forceinline__ void ana2d_tiles(const Ana2dParams& p, const CUtensor
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
     const int64_t row0 = CLAMPR ? tile_row0(p, rt - b * p.tiles_r) : (rt - b * p.tiles_r) * p.TR;
-    // fused 9: the refill is issued by warp 4, idle during levels 2+3 (warps 0-3), instead of warp 0
     const Refill<CLAMPR, (LPFAST >= 4)> refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s],
-                                               tile + int64_t(p.stages) * gridDim.x, tile_bytes, row_bytes, pol,
-                                               p.fused == 9 ? 4u : 0u};
+                                               tile + int64_t(p.stages) * gridDim.x, tile_bytes, row_bytes, pol};
     // mask_mode 1: the last column tile is ragged (masked stores); aligned_levels < LP: the coarse
     // levels' band offsets are odd (alignment-checked stores there).  With clamp_last the last tile
     // instead starts at Win - TC (full, overlapping its neighbour: identical values stored twice).
@@ -1054,7 +1051,7 @@ __global__ void __launch_bounds__(TCF, FHWT_MINB_SYN * 256 / TCF) syn2d_warp_ker
     fence_mbar_init();
   }
   __syncthreads();
-  if constexpr (LP == 5 && !SHIFT && TCF == 256) {
+  if constexpr (LP == 5 && !SHIFT && TCF >= 256) {
     if (p.head > 0) {   // cooperative launch: coarse levels -> fp32 LL5 hand-off, then a grid barrier
       if (p.head == 1) syn_coarse<1>(p);
       else if (p.head == 2) syn_coarse<2>(p);
@@ -1315,6 +1312,10 @@ struct SynWS {
   static const void* get() { return (const void*)syn2d_warp_kernel<LP, true>; }
 };
 template <int LP>
+struct SynW512 {
+  static const void* get() { return (const void*)syn2d_warp_kernel<LP, false, 512>; }
+};
+template <int LP>
 struct SynW128 {
   static const void* get() { return (const void*)syn2d_warp_kernel<LP, false, 128>; }
 };
@@ -1334,6 +1335,7 @@ static const void* syn2d_fn(int fast) {
   if (fast == 0) return (const void*)syn2d_kernel<0, 0, 0, 0>;
   const int mode = (fast >> 24) & 0xff;
   const bool narrow = ((fast >> 4) & 0xfff) == 128;
+  if (mode == 3 && ((fast >> 4) & 0xfff) == 512) return (fast & 15) == 5 ? SynW512<5>::get() : nullptr;
   if (mode == 3) return narrow ? warp_fn<SynW128>(fast & 15) : warp_fn<SynW>(fast & 15);
   if (mode == 6) return narrow ? warp_fn<SynWS128>(fast & 15) : warp_fn<SynWS>(fast & 15);
   return mode == 2 ? by_geometry<SynF2>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15)

@@ -37,19 +37,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Producer-side wait on an "empty" barrier by polling mbarrier.test_wait (never suspends the warp)
-// instead of the try_wait loop: the refill should leave as soon as the consumers release the stage.
-__device__ __forceinline__ void mbar_wait_poll(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-
 // Producer: the 32 one-row boxes of tile t (32-bit tile decode: a tile holds 8192 pixels, so tile
 // counts are < 2^31 for any buffer the TMA row range admits).
 __device__ __forceinline__ void ws_issue(const Ana2dParams& p, const CUtensorMap* map, unsigned char* dst,
@@ -193,12 +180,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) ana2d_ws_kernel(const __grid_co
       int it = 0;
       for (uint32_t t = blockIdx.x; t < ntiles; t += grid, ++it) {
         const int s = it % p.stages;
-        if (it >= p.stages) {
-          if (p.row_boxes == 2)
-            mbar_wait_poll(&empty[s], uint32_t(it / p.stages - 1) & 1u);
-          else
-            mbar_wait(&empty[s], uint32_t(it / p.stages - 1) & 1u);
-        }
+        if (it >= p.stages) mbar_wait(&empty[s], uint32_t(it / p.stages - 1) & 1u);
         ws_issue(p, &in_map, smem + s * p.stage_bytes, &full[s], t, pol);
       }
     }
@@ -226,20 +208,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) ana2d_ws_kernel(const __grid_co
 }
 
 // ------------------------------------------------------------------------------------------------
-// Fused tile chain with a dedicated TMA producer warp (FHWT_ANA_FUSED=7).  The compute side is the
-// default kernel's (haar2d.cu ana_fused_tile, 32 x 256 tiles, LP = 5): level 1 by all 256 compute
-// threads (a warp stores 256-B row segments of every band), a barrier, levels 2+3 by warps 0-3
-// (one 4 x 4 LL1 block per thread), a barrier, levels 4+5 in fp64 by 8 lanes of warp 7, which
-// overlap the next tile's level 1.  What changes is the refill: the default kernel's warp 0 issues
-// the 32 one-row TMA boxes of the next tile between the two barriers, and with the TMA engine
-// busy that loop takes thousands of cycles (tools/phase_timing.py: ~6000 SM cycles per tile)
-// that the second barrier then waits for.  Here warp 8 issues them: the compute warps sync with
-// a named barrier of 256 threads (bar.sync 1, 256) that the producer never joins, thread 0 arrives
-// on the stage's "empty" mbarrier after the first barrier, and the producer waits on it.
-constexpr int kFpThreads = 256 + 32;
-
-__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
+// The default kernel's fused tile chain (haar2d.cu ana_fused_tile, 32 x 256 tiles, LP = 5) written
+// once more for the register-load variant below: level 1 by all 256 threads (a warp stores 256-B
+// row segments of every band), a barrier, levels 2+3 by warps 0-3 (one 4 x 4 LL1 block per
+// thread), a barrier, levels 4+5 in fp64 by 8 lanes of warp 7, which overlap the next tile's level 1.
 // level J+1 on a 2 x 2 block of level-J LL values (same operands, order and types as haar2d.cu ana_pair)
 template <typename T>
 __device__ __forceinline__ T fp_quad(const Ana2dParams& p, T a, T bb, T c, T d, int64_t b, int64_t row, int64_t col, int g) {
@@ -281,105 +253,80 @@ __device__ __forceinline__ TB fp_pair(const Ana2dParams& p, const float (&x)[4][
                      (col0 >> (J + 1)) + bc, J + 1);
 }
 
-__global__ void __launch_bounds__(kFpThreads, 2) ana2d_fp_kernel(const __grid_constant__ Ana2dParams p,
-                                                                 const __grid_constant__ CUtensorMap in_map) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
-  uint64_t* empty = full + p.stages;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    prefetch_tmap(&in_map);
-    for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    fence_mbar_init();
+// The compute side of one tile of the fused chain (256 compute threads): level 1, barrier, levels
+// 2+3 (warps 0-3), barrier, levels 4+5 (warp 7 lanes 0-7).  `after1` runs right after the first
+// barrier (the stage has been read for the last time); BAR is the 256-thread barrier.
+// Level-1 input of the fused chain from the TMA stage in shared memory.
+struct SmemL1 {
+  const float* st;
+  __device__ __forceinline__ void operator()(int k, int orow, int oc, float4& t0, float4& t1) const {
+    t0 = *reinterpret_cast<const float4*>(st + (2 * orow) * 256 + 2 * oc);
+    t1 = *reinterpret_cast<const float4*>(st + (2 * orow + 1) * 256 + 2 * oc);
   }
-  __syncthreads();
-  const uint32_t ntiles = uint32_t(p.ntiles), grid = gridDim.x;
-  if (tid >= 256) {   // producer warp
-    if (tid == 256) {
-      const uint64_t pol = policy_evict_first();
-      int it = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += grid, ++it) {
-        const int s = it % p.stages;
-        if (it >= p.stages) {
-          if (p.row_boxes == 2)
-            mbar_wait_poll(&empty[s], uint32_t(it / p.stages - 1) & 1u);
-          else
-            mbar_wait(&empty[s], uint32_t(it / p.stages - 1) & 1u);
-        }
-        ws_issue(p, &in_map, smem + s * p.stage_bytes, &full[s], t, pol);
-      }
-    }
-  } else {
-    float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]);   // 16 x 128
-    float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);   // 4 x 32
-    const int64_t W = p.W, H = p.H;
-    int it = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += grid, ++it) {
-      const int s = it % p.stages;
-      mbar_wait(&full[s], uint32_t(it / p.stages) & 1u);
-      const uint32_t rt = t / uint32_t(p.tiles_c), ct = t - rt * uint32_t(p.tiles_c);
-      const uint32_t b = rt / uint32_t(p.tiles_r);
-      const int64_t row0 = int64_t(rt - b * uint32_t(p.tiles_r)) * 32, col0 = int64_t(ct) * 256;
-      const float* st = reinterpret_cast<const float*>(smem + s * p.stage_bytes);
-      {   // level 1: unit u = tid + 256 k -> (orow, oc) = (u / 64, 2 (u % 64)), a 2 x 4 input block
-        const int64_t wg = W >> 1, hgW = (H >> 1) * W;
-        float* const base = p.out + (int64_t(b) * H + (row0 >> 1)) * W + (col0 >> 1);
+};
+
+template <typename BAR, typename AFTER, typename SRC = SmemL1>
+__device__ __forceinline__ void fp_tile(const Ana2dParams& p, const SRC& src, float* ll1, float* ll3,
+                                        uint32_t b, int64_t row0, int64_t col0, int tid, const BAR& bar,
+                                        const AFTER& after1) {
+  const int64_t W = p.W, H = p.H;
+  {   // level 1: unit u = tid + 256 k -> (orow, oc) = (u / 64, 2 (u % 64)), a 2 x 4 input block
+    const int64_t wg = W >> 1, hgW = (H >> 1) * W;
+    float* const base = p.out + (int64_t(b) * H + (row0 >> 1)) * W + (col0 >> 1);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int u = tid + 256 * k, orow = u >> 6, oc = 2 * (u & 63);
-          const float4 t0 = *reinterpret_cast<const float4*>(st + (2 * orow) * 256 + 2 * oc);
-          const float4 t1 = *reinterpret_cast<const float4*>(st + (2 * orow + 1) * 256 + 2 * oc);
-          const float a0[2] = {t0.x, t0.z}, b0[2] = {t0.y, t0.w}, c0[2] = {t1.x, t1.z}, d0[2] = {t1.y, t1.w};
-          float ll[2], hl[2], lh[2], hh[2];
+    for (int k = 0; k < 4; ++k) {
+      const int u = tid + 256 * k, orow = u >> 6, oc = 2 * (u & 63);
+      float4 t0, t1;
+      src(k, orow, oc, t0, t1);
+      const float a0[2] = {t0.x, t0.z}, b0[2] = {t0.y, t0.w}, c0[2] = {t1.x, t1.z}, d0[2] = {t1.y, t1.w};
+      float ll[2], hl[2], lh[2], hh[2];
 #pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const float s1 = a0[v] + b0[v], s2 = c0[v] + d0[v], d1 = a0[v] - b0[v], d2 = c0[v] - d0[v];
-            ll[v] = (s1 + s2) * 0.5f;
-            lh[v] = (s1 - s2) * 0.5f;
-            hl[v] = (d1 + d2) * 0.5f;
-            hh[v] = (d1 - d2) * 0.5f;
-          }
-          float* pr = base + int64_t(orow) * W + oc;
-          stg_stream2(pr + wg, make_float2(hl[0], hl[1]));
-          stg_stream2(pr + hgW, make_float2(lh[0], lh[1]));
-          stg_stream2(pr + hgW + wg, make_float2(hh[0], hh[1]));
-          *reinterpret_cast<float2*>(ll1 + orow * 128 + oc) = make_float2(ll[0], ll[1]);
-        }
+      for (int v = 0; v < 2; ++v) {
+        const float s1 = a0[v] + b0[v], s2 = c0[v] + d0[v], d1 = a0[v] - b0[v], d2 = c0[v] - d0[v];
+        ll[v] = (s1 + s2) * 0.5f;
+        lh[v] = (s1 - s2) * 0.5f;
+        hl[v] = (d1 + d2) * 0.5f;
+        hh[v] = (d1 - d2) * 0.5f;
       }
-      bar_compute();   // LL1 complete; every compute warp is done with the stage
-      if (tid == 0) mbar_arrive(&empty[s]);
-      if (tid < 128) {   // levels 2 + 3: block (br, bc) of LL1, 4 x 32 blocks
-        const int br = tid >> 5, bc = tid & 31;
-        float x[4][4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const float4 v = *reinterpret_cast<const float4*>(ll1 + (4 * br + r) * 128 + 4 * bc);
-          x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
-        }
-        ll3[br * 32 + bc] = fp_pair<float, float, 2>(p, x, b, row0, col0, br, bc);
-      }
-      bar_compute();   // LL3 complete
-      if (tid >= 224 && tid < 232) {   // levels 4 + 5 (fp64): block q of LL3 (4 x 32)
-        const int q = tid - 224;
-        float x[4][4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const float4 v = *reinterpret_cast<const float4*>(ll3 + r * 32 + 4 * q);
-          x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
-        }
-        const double ll5 = fp_pair<double, double, 4>(p, x, b, row0, col0, 0, q);
-        if (p.final_pass) {
-          stg_stream1(p.out + (int64_t(b) * H + (row0 >> 5)) * W + (col0 >> 5) + q, float(ll5));
-        } else {   // fp64 hand-off of LL5 to the coarse levels (pitch = padded Win >> 5)
-          const int64_t wpitch = ((p.Win >> 5) + 3) & ~int64_t(3);
-          p.ws_out[(int64_t(b) * (p.Hin >> 5) + (row0 >> 5)) * wpitch + (col0 >> 5) + q] = ll5;
-        }
-      }
+      float* pr = base + int64_t(orow) * W + oc;
+      stg_stream2(pr + wg, make_float2(hl[0], hl[1]));
+      stg_stream2(pr + hgW, make_float2(lh[0], lh[1]));
+      stg_stream2(pr + hgW + wg, make_float2(hh[0], hh[1]));
+      *reinterpret_cast<float2*>(ll1 + orow * 128 + oc) = make_float2(ll[0], ll[1]);
     }
   }
+  bar();   // LL1 complete; every compute warp is done with the stage
+  after1();
+  if (tid < 128) {   // levels 2 + 3: block (br, bc) of LL1, 4 x 32 blocks
+    const int br = tid >> 5, bc = tid & 31;
+    float x[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(ll1 + (4 * br + r) * 128 + 4 * bc);
+      x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+    }
+    ll3[br * 32 + bc] = fp_pair<float, float, 2>(p, x, b, row0, col0, br, bc);
+  }
+  bar();   // LL3 complete
+  if (tid >= 224 && tid < 232) {   // levels 4 + 5 (fp64): block q of LL3 (4 x 32)
+    const int q = tid - 224;
+    float x[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(ll3 + r * 32 + 4 * q);
+      x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+    }
+    const double ll5 = fp_pair<double, double, 4>(p, x, b, row0, col0, 0, q);
+    if (p.final_pass) {
+      stg_stream1(p.out + (int64_t(b) * H + (row0 >> 5)) * W + (col0 >> 5) + q, float(ll5));
+    } else {   // fp64 hand-off of LL5 to the coarse levels (pitch = padded Win >> 5)
+      const int64_t wpitch = ((p.Win >> 5) + 3) & ~int64_t(3);
+      p.ws_out[(int64_t(b) * (p.Hin >> 5) + (row0 >> 5)) * wpitch + (col0 >> 5) + q] = ll5;
+    }
+  }
+}
+
+__device__ __forceinline__ void ana_tail(const Ana2dParams& p) {
   if (p.tail > 0) {   // cooperative launch: every CTA is resident, so the grid barrier is safe
     cooperative_groups::this_grid().sync();
     if (p.tail == 1) ana_coarse<1>(p);
@@ -388,26 +335,80 @@ __global__ void __launch_bounds__(kFpThreads, 2) ana2d_fp_kernel(const __grid_co
   }
 }
 
-}  // namespace
+// ------------------------------------------------------------------------------------------------
+// Register loads (FHWT_ANA_FUSED=11): no input staging at all — every thread loads its four 2 x 4
+// input blocks straight into registers (LDG.128, a warp reads 512 contiguous bytes per row), as
+// tools/membench.cu k_tile_ldg does (6.5 TB/s at 4 CTAs/SM); latency is hidden by occupancy
+// (up to 4 CTAs/SM, shared memory holds only LL1 / LL3), not by a TMA ring.
+struct GlobalL1 {
+  const float4 (&v)[8];
+  __device__ __forceinline__ void operator()(int k, int, int, float4& t0, float4& t1) const {
+    t0 = v[2 * k];
+    t1 = v[2 * k + 1];
+  }
+};
 
-int ana2d_fp_threads() { return kFpThreads; }
-
-cudaError_t ana2d_fp_occupancy(size_t smem, int* blocks_per_sm) {
-  int dev = 0, optin = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute((const void*)ana2d_fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (const void*)ana2d_fp_kernel, kFpThreads, smem);
+__device__ __forceinline__ void ldg_tile_loads(const Ana2dParams& p, uint32_t t, int tid, float4 (&v)[8]) {
+  const uint32_t rt = t / uint32_t(p.tiles_c), ct = t - rt * uint32_t(p.tiles_c);
+  const float* src = p.in + int64_t(rt) * 32 * p.W + int64_t(ct) * 256;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int u = tid + 256 * k, orow = u >> 6, oc = 2 * (u & 63);
+    v[2 * k] = ldg_stream4(src + int64_t(2 * orow) * p.W + 2 * oc);
+    v[2 * k + 1] = ldg_stream4(src + int64_t(2 * orow + 1) * p.W + 2 * oc);
+  }
 }
 
-cudaError_t launch_ana2d_fp(const Ana2dParams& p, const CUtensorMap& in_map, int grid, size_t smem, cudaStream_t s) {
+// MINB: resident CTAs per SM the registers are capped for; PREFETCH: the next tile's loads are
+// issued before the current tile is computed (registers double-buffered).
+template <int MINB, bool PREFETCH>
+__global__ void __launch_bounds__(256, MINB) ana2d_ldg_kernel(const __grid_constant__ Ana2dParams p) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const uint32_t ntiles = uint32_t(p.ntiles), grid = gridDim.x;
+  float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]);
+  float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);
+  float4 v[8];
+  [[maybe_unused]] float4 nv[8];
+  if constexpr (PREFETCH) {
+    if (blockIdx.x < ntiles) ldg_tile_loads(p, blockIdx.x, tid, nv);
+  }
+  for (uint32_t t = blockIdx.x; t < ntiles; t += grid) {
+    const uint32_t rt = t / uint32_t(p.tiles_c), ct = t - rt * uint32_t(p.tiles_c);
+    const uint32_t b = rt / uint32_t(p.tiles_r);
+    const int64_t row0 = int64_t(rt - b * uint32_t(p.tiles_r)) * 32, col0 = int64_t(ct) * 256;
+    if constexpr (PREFETCH) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = nv[i];
+      if (t + grid < ntiles) ldg_tile_loads(p, t + grid, tid, nv);
+    } else {
+      ldg_tile_loads(p, t, tid, v);
+    }
+    // (no barrier after the tile: the next tile's level 1 writes LL1 after every warp passed this
+    // tile's second barrier, and warp 7's levels 4+5 read LL3 before it reaches the next first one)
+    fp_tile(p, GlobalL1{v}, ll1, ll3, b, row0, col0, tid, [] { __syncthreads(); }, [] {});
+  }
+  ana_tail(p);
+}
+
+template <int MINB, bool PF>
+static const void* ldg_fn() { return (const void*)ana2d_ldg_kernel<MINB, PF>; }
+
+static const void* ldg_variant(int v) {   // FHWT_ANA_LDG: 0 = 3 CTAs/SM, 1 = 4 CTAs/SM, 2 = prefetch at 2
+  return v == 1 ? ldg_fn<4, false>() : v == 2 ? ldg_fn<2, true>() : ldg_fn<3, false>();
+}
+
+}  // namespace
+
+cudaError_t ana2d_ldg_occupancy(size_t smem, int* blocks_per_sm, int variant) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, ldg_variant(variant), 256, smem);
+}
+
+cudaError_t launch_ana2d_ldg(const Ana2dParams& p, int grid, size_t smem, cudaStream_t s, int variant) {
   count_launch();
-  void* args[] = {const_cast<Ana2dParams*>(&p), const_cast<CUtensorMap*>(&in_map)};
-  if (p.tail > 0)
-    return cudaLaunchCooperativeKernel((const void*)ana2d_fp_kernel, dim3(grid), dim3(kFpThreads), args, smem, s);
-  return cudaLaunchKernel((const void*)ana2d_fp_kernel, dim3(grid), dim3(kFpThreads), args, smem, s);
+  void* args[] = {const_cast<Ana2dParams*>(&p)};
+  if (p.tail > 0) return cudaLaunchCooperativeKernel(ldg_variant(variant), dim3(grid), dim3(256), args, smem, s);
+  return cudaLaunchKernel(ldg_variant(variant), dim3(grid), dim3(256), args, smem, s);
 }
 
 int ana2d_ws_threads() { return kWsThreads; }

@@ -566,7 +566,7 @@ def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
 @pytest.mark.parametrize("shape,levels", [((4, 512, 2048), 5), ((4, 512, 2048), 7), ((1, 2048, 4096), 8),
                                           ((8, 256, 1024), 6), ((300, 32, 256), 5)])
 @pytest.mark.parametrize("stages", ["2", "3"])
-@pytest.mark.parametrize("variant,tag", [("8", "ana2d ws8"), ("7", "ana2d fp7")])
+@pytest.mark.parametrize("variant,tag", [("8", "ana2d ws8"), ("11", "ana2d ldg11")])
 def test_warp_specialised_analysis_bitwise(monkeypatch, capfd, shape, levels, stages, variant, tag):
     """The haar2d_ana.cu analysis kernels — FHWT_ANA_FUSED=8 (warp-local levels 1-5 of 32 x 32
     blocks + TMA producer warp) and 7 (the default fused chain + TMA producer warp) — give the
