@@ -16,7 +16,7 @@ NVCC_FLAGS = [
     # IEEE per-operation rounding (R10): no a*b+c contraction across butterfly levels
     # ((x0+x1)*s + (x2+x3)*s would otherwise fuse), so every kernel path rounds identically.
     "-fmad=false",
-    "-Xcompiler", "-fPIC,-O2", "-shared",
+    "-Xcompiler", "-fPIC,-O2",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr", "-diag-suppress", "128",
 ]
@@ -51,17 +51,33 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         try:
             if not force and out is None and not stale():   # another process built it meanwhile
                 return LIB
+            import tempfile
+            from concurrent.futures import ThreadPoolExecutor
             tmp = f"{lib}.{os.getpid()}.tmp"
-            cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
-                   *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
-            res = subprocess.run(cmd, capture_output=True, text=True)
-            if res.returncode != 0:
-                sys.stderr.write(res.stdout + res.stderr)
-                if os.path.exists(tmp):
-                    os.unlink(tmp)
-                raise RuntimeError("nvcc failed building libfhwt.so")
+            with tempfile.TemporaryDirectory(prefix="fhwt_build_") as od:
+                # one nvcc per translation unit, in parallel, then one link step
+                def compile_one(src):
+                    obj = os.path.join(od, os.path.splitext(src)[0] + ".o")
+                    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+                           "-c", os.path.join(CSRC, src), "-o", obj]
+                    return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+                with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+                    results = list(ex.map(compile_one, SOURCES))
+                logs = "".join(r.stdout + r.stderr for _, r in results)
+                res = None
+                if all(r.returncode == 0 for _, r in results):
+                    res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                                          *[o for o, _ in results], "-o", tmp],
+                                         capture_output=True, text=True)
+                    logs += res.stdout + res.stderr
+                if res is None or res.returncode != 0:
+                    sys.stderr.write(logs)
+                    if os.path.exists(tmp):
+                        os.unlink(tmp)
+                    raise RuntimeError("nvcc failed building libfhwt.so")
             if verbose:
-                sys.stderr.write(res.stderr)
+                sys.stderr.write(logs)
             os.replace(tmp, lib)
         finally:
             fcntl.flock(lk, fcntl.LOCK_UN)

@@ -101,6 +101,19 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+int env_int(const char* name, int dflt);
+
+// L2 sector promotion of the TMA tensor maps (FHWT_TMA_L2PROMO: 0 none, 1 64 B, 2 128 B, 3 256 B;
+// default 256 B)
+CUtensorMapL2promotion l2_promotion() {
+  switch (env_int("FHWT_TMA_L2PROMO", 3)) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 // 2-D row-major tensor view: `cols` x `rows` elements, row pitch `pitch_elems`, box bw x bh.
 fhwt_status encode_2d(CUtensorMap* m, const void* base, bool f64, int64_t cols, int64_t rows, int64_t pitch_elems,
                       int bw, int bh) {
@@ -113,7 +126,7 @@ fhwt_status encode_2d(CUtensorMap* m, const void* base, bool f64, int64_t cols, 
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(FHWT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): dims %lld x %lld pitch %lld box %d x %d", int(r),
                 (long long)cols, (long long)rows, (long long)pitch_elems, bw, bh);
@@ -503,7 +516,10 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     // them per tile from one thread.  B200 (tools/membench.py, tools/sweep_2d.py): 32 one-row
     // 1-KB boxes stream at 6.9 TB/s where one 32-row box stops at 6.1 TB/s; smaller row boxes
     // are request-bound and slower than multi-row boxes.
-    p.l2hint = env_int("FHWT_ANA_L2HINT", 1);
+    // TMA loads without an L2 cache-policy operand (0) by default: in the bench's DWT+IDWT step the
+    // hint-free instruction form streams c4 analysis at 6.35 TB/s against 6.20 with any policy
+    // (evict_first / evict_normal / evict_last all 6.20; tools/bench_ab.sh, profiles/r02_l2_policy.md)
+    p.l2hint = env_int("FHWT_ANA_L2HINT", 0);
     // Level-pair fusion (32 x 256 tiles), measured: LP = 5 levels 2+3 by 128 threads and 4+5 by 8 (+3 %);
     // LP = 3, 4 level by level.  Mode 6 (LP = 3: levels 2+3 by all 256 threads, two lanes per 4 x 4
     // LL1 block) won on two boxes (+1-3.5 %) and lost on two (-7 %, 2048^2 images): kept as an option.
@@ -527,6 +543,8 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
       const size_t sz = (in64 || ps.g0 + j >= kFirstF64Level) ? 8 : 4;
       pb[j & 1] = std::max(pb[j & 1], size_t(p.TR >> j) * size_t(p.TC >> j) * sz);
     }
+    // FHWT_ANA_FUSED=12 double-buffers LL1 (haar2d.cu ana_fused12_tile)
+    if (!in64 && p.fused == 12) pb[1] = std::max(pb[1], 2 * size_t(16 * 128) * 4);
     // compile-time 32 x 256 variant: first pass, full tiles (then every band offset is 8-B aligned)
     const bool fast_ok = !in64 && ps.g0 == 0 && (p.TR == 32 || p.TR == 16 || p.TR == 8) &&
                          (p.TC == 256 || p.TC == 128) && (p.Win % p.TC == 0 || env_int("FHWT_ANA_RAGGED_FAST", 1) != 0);
@@ -640,6 +658,9 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
     if (coop && kk == 1) continue;
     const Pass ps = pl->passes[kk];
     Syn2dParams p{};
+    // warp-kernel TMA loads: 3 = no policy operand (default; c4 synthesis 6.34 TB/s against 6.28 with
+    // evict_first, 6.30 evict_normal, 6.31 evict_last: profiles/r02_l2_policy.md)
+    p.l2mode = env_int("FHWT_SYN_L2MODE", 3);
     p.H = H;
     p.W = W;
     p.Hin = H >> ps.g0;

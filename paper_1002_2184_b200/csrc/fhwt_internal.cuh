@@ -49,7 +49,7 @@ struct Ana2dParams {
   int fused;             // 32 x 256 fast tiles, LP >= 3: levels 2+3 and 4+5 fused (FHWT_ANA_FUSED, default 1)
   int tail;              // > 0: after the tiles, a grid barrier and levels 6..5+tail of the fp64 LL5
                          // hand-off in the same (cooperative) launch (ana_coarse); 0: none
-  int l2hint;            // 1: TMA loads carry an L2 evict_first policy (sweep knob FHWT_ANA_L2HINT)
+  int l2hint;            // TMA loads: 0 no cache-policy operand (default), 1 evict_first, 2 evict_normal, 3 evict_last
   int row_boxes;         // 1: the map's box is one row and TR boxes are issued per tile (rows of
                          // 128-B multiples; TMA smem destinations must be 128-B aligned); 0: one TR-row box
   const float* in;       // first-pass input (fp32 d), read directly by the register-load kernel (haar2d_ana.cu)
@@ -83,6 +83,7 @@ struct Syn2dParams {
                            // barrier, then the tiles, in one cooperative launch (syn_coarse); 0: none
   float* ll_ws_out;        // head > 0: the LL5 workspace the head phase writes (same buffer as ll_ws)
   int row_boxes[6];        // per pass-level j: one-row boxes (1) or one (TR >> j)-row box (0); see Ana2dParams
+  int l2mode;              // warp kernel's TMA loads: 0 L2::evict_first, 1 evict_normal, 2 evict_last, 3 no policy (default)
 };
 
 struct TmaMaps2d {
@@ -248,6 +249,16 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

@@ -380,7 +380,7 @@ __device__ __forceinline__ void ana_fused_tile(const Ana2dParams& p, const float
   FHWT_PHASE(1);
   __syncthreads();
   FHWT_PHASE(2);
-  refill();
+  if (p.fused != 13) refill();   // 13: refill after the second barrier (later read-ahead; experiment)
   FHWT_PHASE(3);
   const int tid = threadIdx.x;
   if (p.fused == 6) {   // levels 2 + 3 over all 256 threads: two lanes per 4 x 4 LL1 block, level 3
@@ -438,6 +438,7 @@ __device__ __forceinline__ void ana_fused_tile(const Ana2dParams& p, const float
   FHWT_PHASE(4);
   if constexpr (LP > 3) {
     __syncthreads();
+    if (p.fused == 13) refill();
     FHWT_PHASE(5);
     if (tid >= 224 && tid < 232) {   // levels 4 (+ 5): warp 7 lanes 0..7, block q of LL3 (4 x 32)
       const int q = tid - 224;
@@ -476,6 +477,58 @@ __device__ __forceinline__ void ana_fused_tile(const Ana2dParams& p, const float
           if (p.final_pass) stg_stream2(pr, make_float2(llv[0], llv[1]));
         }
       }
+    }
+  }
+}
+
+// Named CTA barrier 1 (barrier 0 is __syncthreads): producers arrive without waiting, consumers
+// wait; `count` threads in total (a multiple of 32).  Orders the producers' shared-memory writes
+// before the consumers' reads (PTX bar.arrive / bar.sync memory ordering).
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// FHWT_ANA_FUSED=12 (32 x 256 tiles, LP = 5): the fused chain with the refill OFF the per-tile
+// critical path.  Warp 0 issues the stage refill after barrier 1 and goes straight on to the next
+// tile's level 1; warps 1-4 run levels 2+3 and arrive on named barrier 1; only warp 7 waits there
+// (levels 4+5 need LL3); warps 5-6 go on to the next tile.  The only CTA-wide barrier per tile is
+// barrier 1 (level 1 done: stage consumed, LL1 complete).  LL1 is double-buffered (it & 1): the
+// next tile's level 1 may write LL1 while warps 1-4 still read this tile's.  Same operations on
+// the same operands as ana_fused_tile: bitwise identical output.
+template <typename RF>
+__device__ __forceinline__ void ana_fused12_tile(const Ana2dParams& p, const float* stage, unsigned char* smem,
+                                                 int64_t b, int64_t row0, int64_t col0, int it, const RF& refill) {
+  float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]) + (it & 1) * (16 * 128);
+  float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);   // 4 x 32
+  ana_level<float, float, 2, 32, 256, true>(p, stage, 32, 256, 1, b, row0, col0, ll1, false);
+  __syncthreads();
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    refill();
+  } else if (warp <= 4) {   // levels 2 + 3: block (br, bc) of LL1, 4 x 32 blocks
+    const int t = tid - 32, br = t >> 5, bc = t & 31;
+    float x[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(ll1 + (4 * br + r) * 128 + 4 * bc);
+      x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+    }
+    ll3[br * 32 + bc] = ana_pair<float, float, 2, 5>(p, x, b, row0, col0, br, bc);
+    named_bar_arrive(1, 160);
+  } else if (warp == 7) {   // levels 4 + 5: lanes 0..7, block q of LL3 (4 x 32)
+    named_bar_sync(1, 160);
+    const int q = tid - 224;
+    if (q < 8) {
+      float x[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float4 v = *reinterpret_cast<const float4*>(ll3 + r * 32 + 4 * q);
+        x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+      }
+      ana_pair<double, double, 4, 5>(p, x, b, row0, col0, 0, q);
     }
   }
 }
@@ -588,7 +641,7 @@ __device__ __forceinline__ void ana2d_tiles(const Ana2dParams& p, const CUtensor
   const int tid = threadIdx.x;
   const uint32_t row_bytes = uint32_t(p.TC) * uint32_t(sizeof(TIn));
   const uint32_t tile_bytes = uint32_t(p.TR) * row_bytes;
-  const uint64_t pol = policy_evict_first();   // warp-uniform (see Refill)
+  const uint64_t pol = p.l2hint == 2 ? policy_evict_normal() : p.l2hint == 3 ? policy_evict_last() : policy_evict_first();   // warp-uniform (see Refill)
   if (tid < 32) {
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
@@ -626,7 +679,10 @@ __device__ __forceinline__ void ana2d_tiles(const Ana2dParams& p, const CUtensor
       }
     }
     if constexpr (LPFAST >= 3 && TRF == 32 && TCF == 256) {
-      if (p.fused) {   // 2 barriers per tile (see ana_fused_tile)
+      if (LPFAST == 5 && p.fused == 12) {   // 1 CTA barrier per tile, refill off the critical path
+        ana_fused12_tile(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, row0, col0, it,
+                         refill);
+      } else if (p.fused) {   // 2 barriers per tile (see ana_fused_tile)
         ana_fused_tile<LPFAST>(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, row0, col0,
                                refill);
       } else {
@@ -894,13 +950,23 @@ __device__ __forceinline__ void syn_issue_tile(const Syn2dParams& p, const TmaMa
   }
 }
 
+// TMA load with (HINT) or without the L2 cache-policy operand.  Measured in the bench's step
+// (tools/bench_ab.sh): the hint-free form of the instruction streams faster than any policy passed
+// through .L2::cache_hint (analysis 6.20 -> 6.35 TB/s with the same evict_normal default policy).
+template <bool HINT>
+__device__ __forceinline__ void tma_load_2d_h(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                              uint64_t pol) {
+  if constexpr (HINT) tma_load_2d(dst, map, c0, c1, bar, pol);
+  else tma_load_2d_nohint(dst, map, c0, c1, bar);
+}
+
 // --------------------------------------------------- warp-decoupled synthesis (32 x 256 tiles)
 // Mirror of ana2d_warp_kernel: warp w rebuilds output columns [32w, 32w + 32) of a tile from the
 // level-j coefficient blocks at columns [(32w) >> j, (32w + 32) >> j) of the staged boxes.
 // SHIFT: band blocks that do not start 16-B aligned (W >> g or the clamped last tile's column
 // offset not a multiple of 4): every box starts at the aligned column at or below the block and is 4
 // columns wider (box_pitch = (TC >> j) + 4); the compute phase adds the shift (column & 3).
-template <bool SHIFT = false, bool CLAMPR = true>
+template <bool SHIFT = false, bool CLAMPR = true, bool HINT = true>
 __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* base,
                                                     uint64_t* bar, int64_t t, uint64_t pol) {
   const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
@@ -913,7 +979,7 @@ __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const 
   const int64_t llrow = p.ll_from_ws ? b * (p.Hin >> L) + (row0 >> L) : b * p.H + (row0 >> L);
   const int llrows = p.row_boxes[L] ? (p.TR >> L) : 1;
   for (int r = 0; r < llrows; ++r)
-    tma_load_2d(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int((col0 >> L) & AL), int(llrow + r), bar,
+    tma_load_2d_h<HINT>(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int((col0 >> L) & AL), int(llrow + r), bar,
                 pol);
   for (int j = L; j >= 1; --j) {
     const int g = p.g0 + j;
@@ -922,9 +988,9 @@ __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const 
     const int rb = p.box_pitch[j] * 4;
     const int nrows = p.row_boxes[j] ? (p.TR >> j) : 1;
     for (int r = 0; r < nrows; ++r) {
-      tma_load_2d(base + p.box_off[j][0] + r * rb, &maps.level[j], int((wg + bc) & AL), int(br + r), bar, pol);
-      tma_load_2d(base + p.box_off[j][1] + r * rb, &maps.level[j], int(bc & AL), int(br + hg + r), bar, pol);
-      tma_load_2d(base + p.box_off[j][2] + r * rb, &maps.level[j], int((wg + bc) & AL), int(br + hg + r), bar, pol);
+      tma_load_2d_h<HINT>(base + p.box_off[j][0] + r * rb, &maps.level[j], int((wg + bc) & AL), int(br + r), bar, pol);
+      tma_load_2d_h<HINT>(base + p.box_off[j][1] + r * rb, &maps.level[j], int(bc & AL), int(br + hg + r), bar, pol);
+      tma_load_2d_h<HINT>(base + p.box_off[j][2] + r * rb, &maps.level[j], int((wg + bc) & AL), int(br + hg + r), bar, pol);
     }
   }
 }
@@ -1001,11 +1067,14 @@ __device__ __forceinline__ void syn2d_warp_tiles(const Syn2dParams& p, const Tma
                                                  uint64_t* bars, unsigned* cnt, WarpScratch* sc) {
   constexpr unsigned NW = TCF / 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint64_t pol = policy_evict_first();
+  const uint64_t pol = p.l2mode == 0 ? policy_evict_first() : p.l2mode == 1 ? policy_evict_normal() : policy_evict_last();
   if (tid == 0)
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
-      if (t < p.ntiles) syn_issue_tile_lane<SHIFT, CLAMPR>(p, maps, smem + s * p.stage_bytes, &bars[s], t, pol);
+      if (t < p.ntiles) {
+        if (p.l2mode == 3) syn_issue_tile_lane<SHIFT, CLAMPR, false>(p, maps, smem + s * p.stage_bytes, &bars[s], t, pol);
+        else syn_issue_tile_lane<SHIFT, CLAMPR>(p, maps, smem + s * p.stage_bytes, &bars[s], t, pol);
+      }
     }
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
@@ -1026,7 +1095,10 @@ __device__ __forceinline__ void syn2d_warp_tiles(const Syn2dParams& p, const Tma
       // showed in 2.6 % of the stall samples)
       if ((atom_add_acq_rel_cta(&cnt[s], 1u) & (NW - 1)) == NW - 1) {
         const int64_t nt = tile + int64_t(p.stages) * gridDim.x;
-        if (nt < p.ntiles) syn_issue_tile_lane<SHIFT, CLAMPR>(p, maps, smem + s * p.stage_bytes, &bars[s], nt, pol);
+        if (nt < p.ntiles) {
+          if (p.l2mode == 3) syn_issue_tile_lane<SHIFT, CLAMPR, false>(p, maps, smem + s * p.stage_bytes, &bars[s], nt, pol);
+          else syn_issue_tile_lane<SHIFT, CLAMPR>(p, maps, smem + s * p.stage_bytes, &bars[s], nt, pol);
+        }
       }
     }
   }

@@ -44,8 +44,13 @@ __device__ __forceinline__ void ws_issue(const Ana2dParams& p, const CUtensorMap
   const uint32_t rt = t / uint32_t(p.tiles_c), ct = t - rt * uint32_t(p.tiles_c);
   mbar_arrive_expect_tx(full, 32u * 1024u);
   const int row = int(rt) * 32, col = int(ct) * 256;
+  if (p.l2hint) {
 #pragma unroll 1
-  for (int r = 0; r < 32; ++r) tma_load_2d(dst + r * 1024, map, col, row + r, full, pol);
+    for (int r = 0; r < 32; ++r) tma_load_2d(dst + r * 1024, map, col, row + r, full, pol);
+  } else {
+#pragma unroll 1
+    for (int r = 0; r < 32; ++r) tma_load_2d_nohint(dst + r * 1024, map, col, row + r, full);
+  }
 }
 
 // Levels 1-5 of warp w's 32 x 32 block of one tile.  `release` is called after level 1 (the last
@@ -360,8 +365,10 @@ __device__ __forceinline__ void ldg_tile_loads(const Ana2dParams& p, uint32_t t,
 }
 
 // MINB: resident CTAs per SM the registers are capped for; PREFETCH: the next tile's loads are
-// issued before the current tile is computed (registers double-buffered).
-template <int MINB, bool PREFETCH>
+// issued before the current tile is computed (registers double-buffered); AFTER1: the next tile's
+// loads are issued right after this tile's level 1 (into the same registers, which level 1 was the
+// last reader of), so they fly while levels 2-5 run — no extra registers.
+template <int MINB, bool PREFETCH, bool AFTER1 = false>
 __global__ void __launch_bounds__(256, MINB) ana2d_ldg_kernel(const __grid_constant__ Ana2dParams p) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -373,10 +380,19 @@ __global__ void __launch_bounds__(256, MINB) ana2d_ldg_kernel(const __grid_const
   if constexpr (PREFETCH) {
     if (blockIdx.x < ntiles) ldg_tile_loads(p, blockIdx.x, tid, nv);
   }
+  if constexpr (AFTER1) {
+    if (blockIdx.x < ntiles) ldg_tile_loads(p, blockIdx.x, tid, v);
+  }
   for (uint32_t t = blockIdx.x; t < ntiles; t += grid) {
     const uint32_t rt = t / uint32_t(p.tiles_c), ct = t - rt * uint32_t(p.tiles_c);
     const uint32_t b = rt / uint32_t(p.tiles_r);
     const int64_t row0 = int64_t(rt - b * uint32_t(p.tiles_r)) * 32, col0 = int64_t(ct) * 256;
+    if constexpr (AFTER1) {
+      fp_tile(p, GlobalL1{v}, ll1, ll3, b, row0, col0, tid, [] { __syncthreads(); }, [&] {
+        if (t + grid < ntiles) ldg_tile_loads(p, t + grid, tid, v);
+      });
+      continue;
+    }
     if constexpr (PREFETCH) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = nv[i];
@@ -391,11 +407,17 @@ __global__ void __launch_bounds__(256, MINB) ana2d_ldg_kernel(const __grid_const
   ana_tail(p);
 }
 
-template <int MINB, bool PF>
-static const void* ldg_fn() { return (const void*)ana2d_ldg_kernel<MINB, PF>; }
+template <int MINB, bool PF, bool A1 = false>
+static const void* ldg_fn() { return (const void*)ana2d_ldg_kernel<MINB, PF, A1>; }
 
-static const void* ldg_variant(int v) {   // FHWT_ANA_LDG: 0 = 3 CTAs/SM, 1 = 4 CTAs/SM, 2 = prefetch at 2
-  return v == 1 ? ldg_fn<4, false>() : v == 2 ? ldg_fn<2, true>() : ldg_fn<3, false>();
+// FHWT_ANA_LDG: 0 = 3 CTAs/SM, 1 = 4 CTAs/SM, 2 = prefetch at 2, 3 = next tile's loads after level 1
+// at 3 CTAs/SM, 4 = the same at 2 CTAs/SM
+static const void* ldg_variant(int v) {
+  return v == 1   ? ldg_fn<4, false>()
+         : v == 2 ? ldg_fn<2, true>()
+         : v == 3 ? ldg_fn<3, false, true>()
+         : v == 4 ? ldg_fn<2, false, true>()
+                  : ldg_fn<3, false>();
 }
 
 }  // namespace

@@ -537,7 +537,7 @@ def test_long_signal_segments_bitwise_equal(world):
             assert torch.equal(seg[lo:lo + ln], full[go:go + ln]), (r, band)
 
 
-@pytest.mark.parametrize("knob,values", [("FHWT_ANA_FUSED", ["1", "0", "3", "6", "8"]),
+@pytest.mark.parametrize("knob,values", [("FHWT_ANA_FUSED", ["1", "0", "3", "6", "8", "12"]),
                                          ("FHWT_SYN_MODE", ["0", "2", "3"]),
                                          ("FHWT_COOP", ["1", "0"])])
 @pytest.mark.parametrize("levels", [1, 3, 5, 7])

@@ -27,7 +27,7 @@ def membench(kind, x, y):
     if _MB is None:
         here = os.path.dirname(os.path.abspath(__file__))
         so = os.path.join(here, "membench.so")
-        if not os.path.exists(so):
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(os.path.join(here, "membench.cu")):
             subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared",
                                    "-Xcompiler", "-fPIC", os.path.join(here, "membench.cu"), "-o", so])
         _MB = ctypes.CDLL(so)
@@ -40,7 +40,9 @@ def membench(kind, x, y):
         parts = kind.split("/")
         bh = int(parts[1]) if len(parts) > 1 else 1
         st = int(parts[2]) if len(parts) > 2 else 3
-        return _MB.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 296, st, reps, 256, bh, 0)
+        iss = int(parts[3]) if len(parts) > 3 else 1   # warps issuing the one-row boxes
+        return _MB.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 296, st, reps, 256, bh, 0,
+                               iss)
     return _MB.mb_tile_ldg(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 592, reps)
 
 
@@ -103,7 +105,8 @@ def main():
                 os.environ[k] = v
 
     for rnd in range(int(os.environ.get("ROUNDS", "5"))):
-        for spec in cases:
+        k0 = rnd % len(cases)   # rotate the order every round: no case always runs first
+        for spec in cases[k0:] + cases[:k0]:
             setenv(spec)
             time.sleep(float(base_env.get("SLEEP", "0")))   # SLEEP > 0: burst (power-cap recovered) timing
             mon.tag = spec
@@ -115,11 +118,11 @@ def main():
                 same[spec] = None
             elif spec.startswith("ANA"):
                 t = timeit(lambda: plan.analyze(x, out=c, workspace=ws))
-                if rnd == 0:
+                if spec not in same:
                     same[spec] = bool(torch.equal(c, c_ref))
             else:
                 t = timeit(lambda: plan.synthesize(c_ref, out=r, workspace=ws))
-                if rnd == 0:
+                if spec not in same:
                     same[spec] = bool(torch.equal(r, r_ref))
             res[spec].append(8 * x.numel() / t / 1e6)
             mon.tag = None

@@ -64,20 +64,33 @@ __device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta
 
 __global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtensorMap map, float* __restrict__ y,
                                                   int64_t H, int64_t W, int64_t batch, int stages, int bw, int bh,
-                                                  const float* __restrict__ xsrc, int bulk) {
+                                                  const float* __restrict__ xsrc, int bulk, int issuers) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * 32768);
   const int64_t tiles_c = W / 256, tiles_r = H / 32, ntiles = batch * tiles_r * tiles_c;
   const int t = threadIdx.x;
   if (t == 0) {
-    for (int s = 0; s < stages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bars[s])));
+    for (int s = 0; s < stages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bars[s])), "r"(issuers));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // issuers > 1: lane 0 of warps 0..issuers-1 each arrive (expect_tx of its share) and issue
+  // rows [k * 32 / issuers, (k + 1) * 32 / issuers) of the one-row boxes (bh == 1 only)
   auto issue = [&](int64_t tile, int s) {
     const int64_t rt = tile / tiles_c, ct = tile - rt * tiles_c;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&bars[s])), "r"(32768)
+    const int k = t >> 5, per = 32 / issuers;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&bars[s])), "r"(32768 / issuers)
                  : "memory");
+    if (issuers > 1) {
+      for (int r = k * per; r < (k + 1) * per; ++r)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                su32(smem + s * 32768 + r * 1024)),
+            "l"(reinterpret_cast<uint64_t>(&map)), "r"(int(ct * 256)), "r"(int(rt * 32 + r)), "r"(su32(&bars[s]))
+            : "memory");
+      return;
+    }
     if (bulk) {  // 32 one-row bulk copies of 1 KB (cp.async.bulk, no tensor map)
       const int64_t b = rt / tiles_r, row0 = (rt - b * tiles_r) * 32;
       for (int r = 0; r < 32; ++r)
@@ -95,7 +108,8 @@ __global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtens
             "l"(reinterpret_cast<uint64_t>(&map)), "r"(int(ct * 256 + bx)), "r"(int(rt * 32 + by)), "r"(su32(&bars[s]))
             : "memory");
   };
-  if (t == 0)
+  const bool issuer = (t & 31) == 0 && (t >> 5) < issuers;
+  if (issuer)
     for (int s = 0; s < stages; ++s)
       if (blockIdx.x + int64_t(s) * gridDim.x < ntiles) issue(blockIdx.x + int64_t(s) * gridDim.x, s);
   int it = 0;
@@ -124,7 +138,7 @@ __global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtens
       stg2(pr + hw + wh, make_float2(a.y - c.y, a.w - c.w));
     }
     __syncthreads();
-    if (t == 0 && tile + int64_t(stages) * gridDim.x < ntiles) issue(tile + int64_t(stages) * gridDim.x, s);
+    if (issuer && tile + int64_t(stages) * gridDim.x < ntiles) issue(tile + int64_t(stages) * gridDim.x, s);
   }
 }
 
@@ -165,7 +179,7 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 float mb_tile_tma(const float* x, float* y, int64_t H, int64_t W, int64_t batch, int blocks, int stages, int reps,
-                  int bw, int bh, int bulk) {
+                  int bw, int bh, int bulk, int issuers) {
   void* fp = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
@@ -183,9 +197,9 @@ float mb_tile_tma(const float* x, float* y, int64_t H, int64_t W, int64_t batch,
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int i = 0; i < 2; ++i) k_tile_tma<<<blocks, 256, smem>>>(map, y, H, W, batch, stages, bw, bh, x, bulk);
+  for (int i = 0; i < 2; ++i) k_tile_tma<<<blocks, 256, smem>>>(map, y, H, W, batch, stages, bw, bh, x, bulk, issuers);
   cudaEventRecord(a);
-  for (int i = 0; i < reps; ++i) k_tile_tma<<<blocks, 256, smem>>>(map, y, H, W, batch, stages, bw, bh, x, bulk);
+  for (int i = 0; i < reps; ++i) k_tile_tma<<<blocks, 256, smem>>>(map, y, H, W, batch, stages, bw, bh, x, bulk, issuers);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
