@@ -105,8 +105,11 @@ fhwt_status fhwt_plan_2d(fhwt_plan *p, int64_t h, int64_t w, int64_t batch, int 
 
 fhwt_status fhwt_plan_destroy(fhwt_plan p);
 
-/* Bytes of device workspace a call on this plan needs (0 when every level fits one kernel
- * pass: 2-D levels <= 5, 1-D levels <= 10).  Holds the fp64 coarse-LL hand-off between passes. */
+/* Bytes of device workspace a call on this plan needs.  Holds the fp64 coarse-LL hand-off between
+ * passes (2-D levels > 5, 1-D levels > 10) and, for 2-D plans, 256 bytes of tile counters: the
+ * fused 2-D kernels hand out their tiles in global order from a counter the library zeroes with a
+ * stream-ordered memset before each launch.  1-D plans with levels <= 10 need 0 bytes.  Calls that
+ * may run concurrently (different streams) need distinct workspaces. */
 size_t fhwt_plan_workspace_bytes(fhwt_plan p);
 
 /* Analysis (forward DWT): d [batch][...] -> coeffs (Mallat layout, same shape).

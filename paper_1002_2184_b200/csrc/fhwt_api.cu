@@ -255,10 +255,13 @@ struct fhwt_plan_s {
   int levels;
   std::vector<Pass> passes;
   std::vector<size_t> ws_off;  // per pass boundary k (after pass k, k < passes-1)
+  size_t ctr_off;              // 2-D: tile counters of the dynamic tile order (analysis +0, synthesis +128)
   size_t ws_bytes;
 };
 
 namespace {
+
+constexpr size_t kCtrBytes = 256;
 
 void plan_layout(fhwt_plan_s* p) {
   p->passes = make_passes(p->levels, p->kind == 2 ? kMaxLevels2dPass : kMaxLevels1dPass);
@@ -271,6 +274,10 @@ void plan_layout(fhwt_plan_s* p) {
     p->ws_off.push_back(off);
     off = align_up(off + elems * sizeof(double), 256);
   }
+  // 2-D: 256 B for the tile counters of the dynamic tile order (zeroed by a stream-ordered memset
+  // before each launch that uses them), so concurrent calls with distinct workspaces never share one
+  p->ctr_off = off;
+  if (p->kind == 2) off += kCtrBytes;
   p->ws_bytes = off;
 }
 
@@ -612,7 +619,21 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
       if (wcoop) break;
       continue;
     }
-    const int vmode = fused3 ? 5 : 0;
+    // the lean K1 (haar2d.cu ana2d_lean_kernel): full, unclamped, aligned 32 x 256 tiles at LP = 5 —
+    // every c4 / c5 tile — with the default fused chain
+    const bool lean = fast_ok && p.fused == 1 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 && p.mask_mode == 0 &&
+                      p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows && p.row_boxes &&
+                      env_int("FHWT_ANA_LEAN", 1) != 0;
+    // dynamic tile order (tiles handed out in global order by an atomic counter in the workspace):
+    // c4 analysis 6.35 -> 6.66 TB/s, c5 6.28 -> 6.64 (profiles/r02_dynamic_tiles.md)
+    const bool dyn = lean && env_int("FHWT_ANA_DYN", 1) != 0;
+    if (dyn) {
+      const int g = env_int("FHWT_ANA_DYN_GROUPS", 1);
+      p.dyn_groups = (g > 1 && p.ntiles % g == 0) ? g : 1;
+      p.tile_ctr = reinterpret_cast<unsigned*>(ws + pl->ctr_off);
+      FHWT_CUDA(cudaMemsetAsync(p.tile_ctr, 0, 16, s), "tile counter reset");
+    }
+    const int vmode = fused3 ? 5 : dyn ? 8 : lean ? 7 : 0;
     const int fast = fast_ok ? (vmode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
     int bps = 0;
     FHWT_TRY(occupancy(in64 ? 1 : 0, fast, smem, &bps));
@@ -624,8 +645,8 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
                       env_int("FHWT_COOP", 1) != 0;
     p.tail = coop ? pl->passes[1].Lp : 0;
     if (env_int("FHWT_DEBUG_LAUNCH", 0))
-      std::fprintf(stderr, "[fhwt] ana2d fused %d tile %dx%d LP %d stages %d smem %zu B ctas/SM %d grid %lld\n",
-                   p.fused, p.TR, p.TC, ps.Lp, p.stages, smem, bps, (long long)grid);
+      std::fprintf(stderr, "[fhwt] ana2d fused %d%s tile %dx%d LP %d stages %d smem %zu B ctas/SM %d grid %lld\n",
+                   p.fused, lean ? " lean" : "", p.TR, p.TC, ps.Lp, p.stages, smem, bps, (long long)grid);
     FHWT_CUDA(launch_ana2d(p, map, in64, fast, int(grid), smem, s), "ana2d launch");
     if (coop) break;
   }
@@ -787,6 +808,15 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       // warp-decoupled variant: 32 x 256 and 32 x 128 tiles (one warp per 32 columns)
       if (mode == 3 && !(p.TR == 32 && (p.TC == 256 || p.TC == 512 || (p.TC == 128 && warp128)))) mode = 2;
       if (shifted) mode = 6;
+      // dynamic tile order for the 32 x 256, LP = 5 warp kernel (c4 / c5 tiles), as in the analysis
+      const bool sdyn = mode == 3 && p.TR == 32 && p.TC == 256 && ps.Lp == 5 && full && ps.g0 == 0 &&
+                        env_int("FHWT_SYN_DYN", 0) != 0;
+      if (sdyn) {
+        mode = 9;
+        const int g = env_int("FHWT_SYN_DYN_GROUPS", 1);
+        p.dyn_groups = (g > 1 && p.ntiles % g == 0) ? g : 1;
+        p.tile_ctr = reinterpret_cast<unsigned*>(ws + pl->ctr_off + 128);
+      }
       // stage layout: LL box, then per level j three boxes (128-B aligned: TMA destinations need it;
       // with cp.async a 16-B packing would admit a 3rd CTA/SM, which measured slower: 5.54 vs 6.10 TB/s)
       const size_t balign = 128;
@@ -818,7 +848,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       }
       off = size_t(p.stages) * p.stage_bytes;
       p.p_off[0] = uint32_t(off);
-      if (mode == 3 || mode == 6) {
+      if (mode == 3 || mode == 6 || mode == 9) {
         off = align_up(off + size_t(p.TC / 32) * kSynScratchBytes, 128);
         p.p_off[1] = p.p_off[0];
       } else {
@@ -827,7 +857,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
         off = align_up(off + pb[1], 128);
       }
       p.bar_off = uint32_t(off);
-      const size_t smem = off + 12 * size_t(p.stages);   // mbarriers + stage-release counters
+      const size_t smem = off + 20 * size_t(p.stages);   // mbarriers + stage-release counters + stage tiles
       const int fast_lp = fast ? (mode << 24) | (p.TR << 16) | (p.TC << 4) | ps.Lp : 0;
       int bps = 0;
       FHWT_TRY(occupancy(2, fast_lp, smem, &bps));
@@ -837,13 +867,15 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       bps = std::min(bps, cap > 0 ? cap : 2 * kThreads2d / syn2d_threads(fast_lp));
       const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
       if (coop) {
-        if (mode != 3) return fail(FHWT_ERR_CUDA, "internal: cooperative synthesis needs the warp-decoupled kernel");
+        if (mode != 3 && mode != 9)
+          return fail(FHWT_ERR_CUDA, "internal: cooperative synthesis needs the warp-decoupled kernel");
         p.head = pl->passes[1].Lp;
         p.ll_ws_out = reinterpret_cast<float*>(ws + pl->ws_off[0]);
       }
       if (env_int("FHWT_DEBUG_LAUNCH", 0))
         std::fprintf(stderr, "[fhwt] syn2d mode %d tile %dx%d LP %d stages %d smem %zu B ctas/SM %d grid %lld\n", mode,
                      p.TR, p.TC, ps.Lp, p.stages, smem, bps, (long long)grid);
+      if (mode == 9) FHWT_CUDA(cudaMemsetAsync(p.tile_ctr, 0, 16, s), "tile counter reset");
       FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
     }
   }

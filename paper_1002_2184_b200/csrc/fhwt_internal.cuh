@@ -50,6 +50,8 @@ struct Ana2dParams {
   int tail;              // > 0: after the tiles, a grid barrier and levels 6..5+tail of the fp64 LL5
                          // hand-off in the same (cooperative) launch (ana_coarse); 0: none
   int l2hint;            // TMA loads: 0 no cache-policy operand (default), 1 evict_first, 2 evict_normal, 3 evict_last
+  unsigned* tile_ctr;    // dynamic tile order (lean K1, vmode 8): next-tile counter, zeroed before the launch
+  int dyn_groups;        // dynamic order: counter value c -> tile (c % G) * (ntiles / G) + c / G (G = 1: c)
   int row_boxes;         // 1: the map's box is one row and TR boxes are issued per tile (rows of
                          // 128-B multiples; TMA smem destinations must be 128-B aligned); 0: one TR-row box
   const float* in;       // first-pass input (fp32 d), read directly by the register-load kernel (haar2d_ana.cu)
@@ -83,6 +85,8 @@ struct Syn2dParams {
                            // barrier, then the tiles, in one cooperative launch (syn_coarse); 0: none
   float* ll_ws_out;        // head > 0: the LL5 workspace the head phase writes (same buffer as ll_ws)
   int row_boxes[6];        // per pass-level j: one-row boxes (1) or one (TR >> j)-row box (0); see Ana2dParams
+  unsigned* tile_ctr;      // dynamic tile order (warp kernel, mode 9): next-tile counter, zeroed before the launch
+  int dyn_groups;          // as Ana2dParams::dyn_groups
   int l2mode;              // warp kernel's TMA loads: 0 L2::evict_first, 1 evict_normal, 2 evict_last, 3 no policy (default)
 };
 
@@ -249,6 +253,13 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Dynamic tile order: counter value c -> tile index (G interleaved contiguous streams; G = 1 is the
+// plain global order).  G divides ntiles (checked on the host).
+__device__ __forceinline__ uint32_t dyn_tile(uint32_t c, uint32_t ntiles, int G) {
+  if (G <= 1) return c;
+  const uint32_t per = ntiles / uint32_t(G);
+  return (c % uint32_t(G)) * per + c / uint32_t(G);
+}
 __device__ __forceinline__ uint64_t policy_evict_normal() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));

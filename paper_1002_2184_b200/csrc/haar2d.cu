@@ -286,7 +286,9 @@ struct Refill {
   uint64_t pol;   // must be warp-uniform (computed by every thread): a divergent cache-hint operand
                   // makes each TMA issue a waterfall loop (analysis 6.57 -> 6.15 TB/s)
   __device__ __forceinline__ void operator()() const {
-    if (threadIdx.x < 32 && next < p->ntiles)
+    // FHWT_ANA_FUSED=9: warp 4 (idle while warps 0-3 run levels 2+3) issues instead of warp 0
+    const unsigned issuer = p->fused == 9 ? 4u : 0u;
+    if ((threadIdx.x >> 5) == issuer && next < p->ntiles)
       ana_issue_tile<CLAMPR, U32>(*p, map, dst, bar, next, bytes, row_bytes, pol);
   }
 };
@@ -657,8 +659,18 @@ __device__ __forceinline__ void ana2d_tiles(const Ana2dParams& p, const CUtensor
     FHWT_PHASE(7);
     mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
     FHWT_PHASE(0);
+#ifdef FHWT_LOOP_U32   // experiment: 32-bit tile decode in the loop (tile counts < 2^31 for LP >= 4)
+    int64_t rt, ct, b;
+    if constexpr (LPFAST >= 4) {
+      const uint32_t r32 = uint32_t(tile) / uint32_t(p.tiles_c), b32 = r32 / uint32_t(p.tiles_r);
+      rt = r32; ct = uint32_t(tile) - r32 * uint32_t(p.tiles_c); b = b32;
+    } else {
+      rt = tile / p.tiles_c; ct = tile - rt * p.tiles_c; b = rt / p.tiles_r;
+    }
+#else
     const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
     const int64_t b = rt / p.tiles_r;
+#endif
     const int64_t row0 = CLAMPR ? tile_row0(p, rt - b * p.tiles_r) : (rt - b * p.tiles_r) * p.TR;
     const Refill<CLAMPR, (LPFAST >= 4)> refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s],
                                                tile + int64_t(p.stages) * gridDim.x, tile_bytes, row_bytes, pol};
@@ -726,6 +738,175 @@ __global__ void __launch_bounds__(LPFAST > 0 ? fast_threads(TRF, TCF) : kThreads
       else if (p.tail == 2) ana_coarse<2>(p);
       else ana_coarse<3>(p);
     }
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive_plain(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// ----------------------------------------------------------------- lean K1 (c4 / c5 tiles)
+// The shipped analysis kernel for full 32 x 256 tiles with LP = 5 (every c4 / c5 tile): the same
+// tile chain as ana2d_kernel's fused path (ana_fused_tile<5>: level 1 by all 256 threads, barrier,
+// the stage refill by warp 0 lane 0, levels 2+3 by warps 0-3, barrier, levels 4+5 in fp64 by 8
+// lanes of warp 7 overlapping the next tile's level 1), compiled as its own kernel with none of
+// the general kernel's other paths (row clamp, masked / ragged tiles, level-by-level fallbacks,
+// experiment branches).  Same operations on the same operands: bitwise identical output.  Why a
+// separate kernel: the general ana2d_kernel<float,5,32,256> is ~16.8 K SASS instructions, and
+// unrelated edits to it moved the c4 analysis between 5.6 and 6.35 TB/s (a 32-bit tile decode in
+// the loop alone: 6345 -> 5630 GB/s, profiles/r02_l2_policy.md); the hot loop here is all the
+// kernel holds.
+struct LeanRefill {
+  const Ana2dParams* p;
+  const CUtensorMap* map;
+  unsigned char* dst;
+  uint64_t* bar;
+  int64_t next;
+  uint64_t pol;
+  __device__ __forceinline__ void operator()() const {
+    if (threadIdx.x < 32 && next < p->ntiles)
+      ana_issue_tile<false, true>(*p, map, dst, bar, next, 32u * 1024u, 1024u, pol);
+  }
+};
+
+__device__ __forceinline__ void ana_lean_tile(const Ana2dParams& p, const float* stage, unsigned char* smem,
+                                              int64_t b, int64_t row0, int64_t col0, const LeanRefill& refill) {
+  float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]);   // 16 x 128
+  float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);   // 4 x 32
+  ana_level<float, float, 2, 32, 256, true>(p, stage, 32, 256, 1, b, row0, col0, ll1, false);
+  __syncthreads();   // LL1 complete; the stage has been read for the last time
+  refill();
+  const int tid = threadIdx.x;
+  if (tid < 128) {   // levels 2 + 3: block (br, bc) of LL1, 4 x 32 blocks
+    const int br = tid >> 5, bc = tid & 31;
+    float x[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(ll1 + (4 * br + r) * 128 + 4 * bc);
+      x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+    }
+    ll3[br * 32 + bc] = ana_pair<float, float, 2, 5>(p, x, b, row0, col0, br, bc);
+  }
+  __syncthreads();   // LL3 complete
+  if (tid >= 224 && tid < 232) {   // levels 4 + 5 (fp64): warp 7 lanes 0..7, block q of LL3 (4 x 32)
+    const int q = tid - 224;
+    float x[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(ll3 + r * 32 + 4 * q);
+      x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+    }
+    ana_pair<double, double, 4, 5>(p, x, b, row0, col0, 0, q);
+  }
+}
+
+// DYN: tiles are handed out in global order by an atomic counter (p.tile_ctr) instead of the static
+// blockIdx + k * grid assignment, so the tiles in flight at any moment stay contiguous in memory
+// however far individual CTAs drift; the tile index travels to the consumers in shared memory
+// next to the stage's mbarrier (written before the arrive, read after the wait).
+template <bool DYN>
+__global__ void __launch_bounds__(256, FHWT_MINB_ANA) ana2d_lean_kernel(const __grid_constant__ Ana2dParams p,
+                                                                      const __grid_constant__ CUtensorMap in_map) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    prefetch_tmap(&in_map);
+    for (int s = 0; s < p.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();   // used only with FHWT_ANA_L2HINT=1
+  if constexpr (DYN) {
+    unsigned* stile = reinterpret_cast<unsigned*>(smem + p.bar_off + 8 * p.stages);
+    if (tid < 32) {
+      for (int s = 0; s < p.stages; ++s) {
+        const uint32_t t = blockIdx.x + uint32_t(s) * gridDim.x;
+        if ((tid & 31) == 0) stile[s] = t;
+        if (t < p.ntiles) {
+          ana_issue_tile<false, true>(p, &in_map, smem + s * p.stage_bytes, &bars[s],
+                                      dyn_tile(t, uint32_t(p.ntiles), p.dyn_groups), 32768u, 1024u, pol);
+        } else if ((tid & 31) == 0) {
+          mbar_arrive_plain(&bars[s]);
+        }
+      }
+    }
+    for (int it = 0;; ++it) {
+      const int s = it % p.stages;
+      mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+      const uint32_t cval = stile[s];
+      if (cval >= uint32_t(p.ntiles)) break;
+      const uint32_t tile = dyn_tile(cval, uint32_t(p.ntiles), p.dyn_groups);
+      // the refill's tile index is fetched now, so the atomic's round trip overlaps level 1
+      uint32_t nt = 0;
+      if (tid == 0) nt = atomicAdd(p.tile_ctr, 1u) + uint32_t(p.stages) * gridDim.x;
+      const int64_t rt = tile / uint32_t(p.tiles_c), ct = tile - uint32_t(rt) * uint32_t(p.tiles_c);
+      const int64_t b = uint32_t(rt) / uint32_t(p.tiles_r);
+      const float* stage = reinterpret_cast<const float*>(smem + s * p.stage_bytes);
+      float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]);
+      float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);
+      const int64_t row0 = (rt - b * p.tiles_r) * 32, col0 = ct * 256;
+      ana_level<float, float, 2, 32, 256, true>(p, stage, 32, 256, 1, b, row0, col0, ll1, false);
+      __syncthreads();   // LL1 complete; the stage (and stile[s]) has been read for the last time
+      if (tid < 32) {   // refill with the next tile in global order
+        if (tid == 0) stile[s] = nt;
+        nt = __shfl_sync(0xffffffffu, nt, 0);
+        if (nt < uint32_t(p.ntiles))
+          ana_issue_tile<false, true>(p, &in_map, smem + s * p.stage_bytes, &bars[s],
+                                      dyn_tile(nt, uint32_t(p.ntiles), p.dyn_groups), 32768u, 1024u, pol);
+        else if ((tid & 31) == 0)
+          mbar_arrive_plain(&bars[s]);
+      }
+      if (tid < 128) {
+        const int br = tid >> 5, bc = tid & 31;
+        float x[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float4 v = *reinterpret_cast<const float4*>(ll1 + (4 * br + r) * 128 + 4 * bc);
+          x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+        }
+        ll3[br * 32 + bc] = ana_pair<float, float, 2, 5>(p, x, b, row0, col0, br, bc);
+      }
+      __syncthreads();   // LL3 complete
+      if (tid >= 224 && tid < 232) {
+        const int q = tid - 224;
+        float x[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float4 v = *reinterpret_cast<const float4*>(ll3 + r * 32 + 4 * q);
+          x[r][0] = v.x; x[r][1] = v.y; x[r][2] = v.z; x[r][3] = v.w;
+        }
+        ana_pair<double, double, 4, 5>(p, x, b, row0, col0, 0, q);
+      }
+    }
+  } else {
+  if (tid < 32) {
+    for (int s = 0; s < p.stages; ++s) {
+      const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
+      if (t < p.ntiles) ana_issue_tile<false, true>(p, &in_map, smem + s * p.stage_bytes, &bars[s], t, 32768u, 1024u, pol);
+    }
+  }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+    const int s = it % p.stages;
+    mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+#ifdef FHWT_LEAN_U32   // robustness experiment: 32-bit tile decode
+    const int64_t rt = uint32_t(tile) / uint32_t(p.tiles_c), ct = uint32_t(tile) - uint32_t(rt) * uint32_t(p.tiles_c);
+    const int64_t b = uint32_t(rt) / uint32_t(p.tiles_r);
+#else
+    const int64_t rt = tile / p.tiles_c, ct = tile - rt * p.tiles_c;
+    const int64_t b = rt / p.tiles_r;
+#endif
+    const LeanRefill refill{&p, &in_map, smem + s * p.stage_bytes, &bars[s], tile + int64_t(p.stages) * gridDim.x, pol};
+    ana_lean_tile(p, reinterpret_cast<const float*>(smem + s * p.stage_bytes), smem, b, (rt - b * p.tiles_r) * 32,
+                  ct * 256, refill);
+  }
+  }
+  if (p.tail > 0) {   // cooperative launch: every CTA is resident, so the grid barrier is safe
+    cooperative_groups::this_grid().sync();
+    if (p.tail == 1) ana_coarse<1>(p);
+    else if (p.tail == 2) ana_coarse<2>(p);
+    else ana_coarse<3>(p);
   }
 }
 
@@ -1062,12 +1243,57 @@ __device__ __forceinline__ void warp_syn_steps(const Syn2dParams& p, const float
 
 // The persistent tile loop of syn2d_warp_kernel; CLAMPR (p.clamp_rows) is compile-time so the
 // unclamped issue path carries no clamp arithmetic (as in ana2d_tiles).
-template <int LP, bool SHIFT, int TCF, bool CLAMPR>
+// DYN: the next tile of a released stage comes from the launch's tile counter (p.tile_ctr, global
+// order) instead of tile + stages * grid; its index is stored next to the stage's mbarrier
+// (stile[s]) before the arrive and read by every warp after its wait (see ana2d_lean_kernel).
+template <int LP, bool SHIFT, int TCF, bool CLAMPR, bool DYN = false>
 __device__ __forceinline__ void syn2d_warp_tiles(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* smem,
                                                  uint64_t* bars, unsigned* cnt, WarpScratch* sc) {
   constexpr unsigned NW = TCF / 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t pol = p.l2mode == 0 ? policy_evict_first() : p.l2mode == 1 ? policy_evict_normal() : policy_evict_last();
+  if constexpr (DYN) {
+    unsigned* stile = cnt + p.stages;
+    unsigned* pend = cnt + 2 * p.stages;   // next tile for stage s, fetched by warp 0 during the tile
+    if (tid == 0)
+      for (int s = 0; s < p.stages; ++s) {
+        const uint32_t t = blockIdx.x + uint32_t(s) * gridDim.x;
+        stile[s] = t;
+        if (t < uint32_t(p.ntiles))
+          syn_issue_tile_lane<SHIFT, CLAMPR, false>(p, maps, smem + s * p.stage_bytes, &bars[s],
+                                                    dyn_tile(t, uint32_t(p.ntiles), p.dyn_groups), pol);
+        else mbar_arrive_plain(&bars[s]);
+      }
+    for (int it = 0;; ++it) {
+      const int s = it % p.stages;
+      mbar_wait(&bars[s], uint32_t(it / p.stages) & 1u);
+      const uint32_t cval = stile[s];
+      if (cval >= uint32_t(p.ntiles)) break;
+      const uint32_t tile = dyn_tile(cval, uint32_t(p.ntiles), p.dyn_groups);
+      uint32_t nt = 0;
+      if (tid == 0) nt = atomicAdd(p.tile_ctr, 1u) + uint32_t(p.stages) * gridDim.x;   // overlaps the tile
+      const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, TCF, CLAMPR ? p.Hin - 32 : -1);
+      const unsigned char* stage = smem + s * p.stage_bytes;
+      const int64_t col0 = tile_col0(p, xy.col0 / TCF + p.ct0);
+      const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> LP) +
+                        (SHIFT ? int((col0 >> LP) & 3) : 0);
+      warp_syn_steps<LP, LP, SHIFT, TCF>(p, ll, (TCF >> LP) + (SHIFT ? 4 : 0), stage, warp, sc, xy.b, xy.row0,
+                                         col0 + 32 * warp, col0);
+      __syncwarp();
+      if (lane == 0) {   // stage release (as below); the last warp refills with warp 0's fetched tile
+        if (tid == 0) pend[s] = nt;   // before warp 0's release: the last warp acquires it
+        if ((atom_add_acq_rel_cta(&cnt[s], 1u) & (NW - 1)) == NW - 1) {
+          nt = pend[s];
+          stile[s] = nt;
+          if (nt < uint32_t(p.ntiles))
+            syn_issue_tile_lane<SHIFT, CLAMPR, false>(p, maps, smem + s * p.stage_bytes, &bars[s],
+                                                      dyn_tile(nt, uint32_t(p.ntiles), p.dyn_groups), pol);
+          else mbar_arrive_plain(&bars[s]);
+        }
+      }
+    }
+    return;
+  }
   if (tid == 0)
     for (int s = 0; s < p.stages; ++s) {
       const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
@@ -1105,7 +1331,7 @@ __device__ __forceinline__ void syn2d_warp_tiles(const Syn2dParams& p, const Tma
 }
 
 // TCF: tile columns, 256 (8 warps) or 128 (4 warps); each warp owns a 32-column slice.
-template <int LP, bool SHIFT = false, int TCF = 256>
+template <int LP, bool SHIFT = false, int TCF = 256, bool DYN = false>
 __global__ void __launch_bounds__(TCF, FHWT_MINB_SYN * 256 / TCF) syn2d_warp_kernel(const __grid_constant__ Syn2dParams p,
                                                                 const __grid_constant__ TmaMaps2d maps) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -1134,9 +1360,9 @@ __global__ void __launch_bounds__(TCF, FHWT_MINB_SYN * 256 / TCF) syn2d_warp_ker
     }
   }
   if (p.clamp_rows)
-    syn2d_warp_tiles<LP, SHIFT, TCF, true>(p, maps, smem, bars, cnt, sc);
+    syn2d_warp_tiles<LP, SHIFT, TCF, true, DYN>(p, maps, smem, bars, cnt, sc);
   else
-    syn2d_warp_tiles<LP, SHIFT, TCF, false>(p, maps, smem, bars, cnt, sc);
+    syn2d_warp_tiles<LP, SHIFT, TCF, false, DYN>(p, maps, smem, bars, cnt, sc);
 }
 
 template <int N>
@@ -1400,6 +1626,8 @@ static const void* ana2d_fn(bool in_f64, int fast) {
   if (in_f64) return (const void*)ana2d_kernel<double, 0, 0, 0>;
   if (fast == 0) return (const void*)ana2d_kernel<float, 0, 0, 0>;
   if (((fast >> 24) & 0xff) == 5) return (const void*)ana2d_fused3_kernel;
+  if (((fast >> 24) & 0xff) == 7) return (const void*)ana2d_lean_kernel<false>;
+  if (((fast >> 24) & 0xff) == 8) return (const void*)ana2d_lean_kernel<true>;
   return by_geometry<AnaF>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15);
 }
 
@@ -1408,6 +1636,7 @@ static const void* syn2d_fn(int fast) {
   const int mode = (fast >> 24) & 0xff;
   const bool narrow = ((fast >> 4) & 0xfff) == 128;
   if (mode == 3 && ((fast >> 4) & 0xfff) == 512) return (fast & 15) == 5 ? SynW512<5>::get() : nullptr;
+  if (mode == 9) return (fast & 15) == 5 ? (const void*)syn2d_warp_kernel<5, false, 256, true> : nullptr;
   if (mode == 3) return narrow ? warp_fn<SynW128>(fast & 15) : warp_fn<SynW>(fast & 15);
   if (mode == 6) return narrow ? warp_fn<SynWS128>(fast & 15) : warp_fn<SynWS>(fast & 15);
   return mode == 2 ? by_geometry<SynF2>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15)
@@ -1423,7 +1652,7 @@ int ana2d_threads(int fast) {
 }
 int syn2d_threads(int fast) {
   const int mode = (fast >> 24) & 0xff;
-  return (mode == 3 || mode == 6) ? ((fast >> 4) & 0xfff) : fast_threads_rt(fast);   // one warp per 32 columns
+  return (mode == 3 || mode == 6 || mode == 9) ? ((fast >> 4) & 0xfff) : fast_threads_rt(fast);   // one warp per 32 columns
 }
 
 cudaError_t ana2d_occupancy(bool in_f64, int fast_lp, size_t smem, int* blocks_per_sm) {

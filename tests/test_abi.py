@@ -89,8 +89,9 @@ def test_unsupported_filter_bank():
 
 
 def test_workspace_sizes():
-    assert fhwt.Plan2d(2048, 2048, 256, 5).workspace_bytes == 0          # c4: one fused pass
-    assert fhwt.Plan2d(32768, 32768, 1, 8).workspace_bytes == 1024 * 1024 * 8   # c5: fp64 LL_5 hand-off
+    # 2-D plans hold 256 B of tile counters (dynamic tile order) after the pass hand-offs
+    assert fhwt.Plan2d(2048, 2048, 256, 5).workspace_bytes == 256        # c4: one fused pass
+    assert fhwt.Plan2d(32768, 32768, 1, 8).workspace_bytes == 1024 * 1024 * 8 + 256   # c5: fp64 LL_5 hand-off
     assert fhwt.Plan1d(65536, 4096, 10).workspace_bytes == 0             # c2: one pass
     assert 3 * 16 * 8 <= fhwt.Plan1d(1 << 14, 3, 14).workspace_bytes < 3 * 16 * 8 + 256   # fp64 a_10 hand-off
 
@@ -161,4 +162,4 @@ def test_plan_pack_ll_rejects_bad_plans():
     assert L.fhwt_plan_pack_ll_2d(p1._h, None, None, None) == 1         # INVALID_ARG: 1-D plan
     p2 = fhwt.Plan2d(64, 64, 1, 3)
     assert L.fhwt_plan_pack_ll_2d(p2._h, None, None, None) == 1         # INVALID_ARG: NULL buffers
-    assert L.fhwt_workspace_bytes(p2._h) == L.fhwt_plan_workspace_bytes(p2._h) == 0
+    assert L.fhwt_workspace_bytes(p2._h) == L.fhwt_plan_workspace_bytes(p2._h) == 256

@@ -539,7 +539,12 @@ def test_long_signal_segments_bitwise_equal(world):
 
 @pytest.mark.parametrize("knob,values", [("FHWT_ANA_FUSED", ["1", "0", "3", "6", "8", "12"]),
                                          ("FHWT_SYN_MODE", ["0", "2", "3"]),
-                                         ("FHWT_COOP", ["1", "0"])])
+                                         ("FHWT_COOP", ["1", "0"]),
+                                         ("FHWT_ANA_LEAN", ["1", "0"]),
+                                         ("FHWT_ANA_DYN", ["1", "0"]),
+                                         ("FHWT_SYN_DYN", ["0", "1"]),
+                                         ("FHWT_ANA_DYN_GROUPS", ["1", "4"]),
+                                         ("FHWT_SYN_DYN_GROUPS", ["1", "4"])])
 @pytest.mark.parametrize("levels", [1, 3, 5, 7])
 def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
     """Every selectable 2-D kernel variant (analysis: level by level, fused level pairs, dedicated
@@ -552,8 +557,12 @@ def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
     outs = []
     for v in values:
         monkeypatch.setenv(knob, v)
-        c = fhwt.analyze_2d(xd, levels)
-        r = fhwt.synthesize_2d(c, levels)
+        # NaN-filled outputs: a variant that skipped a tile cannot inherit another variant's values
+        # from a reused allocation
+        c = torch.full_like(xd, float("nan"))
+        r = torch.full_like(xd, float("nan"))
+        fhwt.analyze_2d(xd, levels, out=c)
+        fhwt.synthesize_2d(c, levels, out=r)
         torch.cuda.synchronize()
         outs.append((c.clone(), r.clone()))
     monkeypatch.delenv(knob)
