@@ -811,7 +811,17 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       // dynamic tile order for the 32 x 256, LP = 5 warp kernel (c4 / c5 tiles), as in the analysis
       const bool sdyn = mode == 3 && p.TR == 32 && p.TC == 256 && ps.Lp == 5 && full && ps.g0 == 0 &&
                         env_int("FHWT_SYN_DYN", 0) != 0;
-      if (sdyn) {
+      // producer-warp K4 (haar2d.cu syn2d_prod_kernel; FHWT_SYN_PROD=1 static order, =2 global order,
+      // the default for full 32 x 256 LP = 5 tiles, with a 3-stage ring): c4 synthesis 6.35 -> 6.41 TB/s,
+      // c5 6.28 -> 6.44 (profiles/r02_dynamic_tiles.md)
+      const int sprod = (mode == 3 && p.TR == 32 && p.TC == 256 && ps.Lp == 5 && full && ps.g0 == 0 && !p.clamp_rows)
+                            ? env_int("FHWT_SYN_PROD", 2) : 0;
+      if (sprod > 0) {
+        mode = sprod == 2 ? 11 : 10;
+        const int g = env_int("FHWT_SYN_DYN_GROUPS", 1);
+        p.dyn_groups = (g > 1 && p.ntiles % g == 0) ? g : 1;
+        p.tile_ctr = reinterpret_cast<unsigned*>(ws + pl->ctr_off + 128);
+      } else if (sdyn) {
         mode = 9;
         const int g = env_int("FHWT_SYN_DYN_GROUPS", 1);
         p.dyn_groups = (g > 1 && p.ntiles % g == 0) ? g : 1;
@@ -840,7 +850,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       // 2 stages for 32 x 256 tiles; the cp.async variant's narrower tiles from a measured table
       int syn_stages = syn_ring_stages(p.stage_bytes), syn_cap = 0;
       if (env_int("FHWT_SYN_TILE_TABLE", 1) != 0) syn_tile_cfg(mode, p.TR, p.TC, &syn_stages, &syn_cap);
-      p.stages = env_int("FHWT_SYN_STAGES", syn_stages);
+      p.stages = env_int("FHWT_SYN_STAGES", mode == 11 ? 3 : syn_stages);
       size_t pb[2] = {0, 0};
       for (int j = 2; j <= ps.Lp; ++j) {
         const int jj = j - 1;
@@ -848,7 +858,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       }
       off = size_t(p.stages) * p.stage_bytes;
       p.p_off[0] = uint32_t(off);
-      if (mode == 3 || mode == 6 || mode == 9) {
+      if (mode == 3 || mode == 6 || mode >= 9) {
         off = align_up(off + size_t(p.TC / 32) * kSynScratchBytes, 128);
         p.p_off[1] = p.p_off[0];
       } else {
@@ -864,10 +874,10 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       // At most 2 resident CTAs/SM: the lighter LP < 5 variants fit 3-4, which measured 2.5-6.5 %
       // slower (tools/sweep_ctas.py, profiles/r01_sweep_ctas.jsonl); LP = 5 is indifferent.
       const int cap = env_int("FHWT_CTAS_PER_SM", syn_cap);   // sweep knob; 0 = the measured default
-      bps = std::min(bps, cap > 0 ? cap : 2 * kThreads2d / syn2d_threads(fast_lp));
+      bps = std::min(bps, cap > 0 ? cap : (mode >= 10 ? 2 : 2 * kThreads2d / syn2d_threads(fast_lp)));
       const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
       if (coop) {
-        if (mode != 3 && mode != 9)
+        if (mode != 3 && mode < 9)
           return fail(FHWT_ERR_CUDA, "internal: cooperative synthesis needs the warp-decoupled kernel");
         p.head = pl->passes[1].Lp;
         p.ll_ws_out = reinterpret_cast<float*>(ws + pl->ws_off[0]);
@@ -875,7 +885,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       if (env_int("FHWT_DEBUG_LAUNCH", 0))
         std::fprintf(stderr, "[fhwt] syn2d mode %d tile %dx%d LP %d stages %d smem %zu B ctas/SM %d grid %lld\n", mode,
                      p.TR, p.TC, ps.Lp, p.stages, smem, bps, (long long)grid);
-      if (mode == 9) FHWT_CUDA(cudaMemsetAsync(p.tile_ctr, 0, 16, s), "tile counter reset");
+      if (mode == 9 || mode == 11) FHWT_CUDA(cudaMemsetAsync(p.tile_ctr, 0, 16, s), "tile counter reset");
       FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
     }
   }

@@ -298,16 +298,46 @@ __device__ __forceinline__ float ldg_stream1(const float* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
   return v;
 }
+// Streaming stores of the transform outputs.  FHWT_STG_MODE (build-time experiment): 0 = L1 no-allocate
+// (default), 1 = + L2 evict_first policy, 2 = .cs, 3 = plain st.global, 4 = + L2 evict_last policy.
+#ifndef FHWT_STG_MODE
+#define FHWT_STG_MODE 0
+#endif
+#if FHWT_STG_MODE == 1 || FHWT_STG_MODE == 4
+__device__ __forceinline__ uint64_t stg_policy() {
+  uint64_t p;
+#if FHWT_STG_MODE == 1
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#else
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
+#define FHWT_STG_PFX "st.global.L1::no_allocate.L2::cache_hint"
+#define FHWT_STG_POL , "l"(stg_policy())
+#define FHWT_STG_POLARG(n) ", %" #n
+#else
+#if FHWT_STG_MODE == 2
+#define FHWT_STG_PFX "st.global.cs"
+#elif FHWT_STG_MODE == 3
+#define FHWT_STG_PFX "st.global"
+#else
+#define FHWT_STG_PFX "st.global.L1::no_allocate"
+#endif
+#define FHWT_STG_POL
+#define FHWT_STG_POLARG(n) ""
+#endif
 __device__ __forceinline__ void stg_stream4(float* p, float4 v) {
-  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
-               "f"(v.z), "f"(v.w)
+  asm volatile(FHWT_STG_PFX ".v4.f32 [%0], {%1, %2, %3, %4}" FHWT_STG_POLARG(5) ";" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w) FHWT_STG_POL
                : "memory");
 }
 __device__ __forceinline__ void stg_stream2(float* p, float2 v) {
-  asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+  asm volatile(FHWT_STG_PFX ".v2.f32 [%0], {%1, %2}" FHWT_STG_POLARG(3) ";" ::"l"(p), "f"(v.x), "f"(v.y) FHWT_STG_POL
+               : "memory");
 }
 __device__ __forceinline__ void stg_stream1(float* p, float v) {
-  asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+  asm volatile(FHWT_STG_PFX ".f32 [%0], %1" FHWT_STG_POLARG(2) ";" ::"l"(p), "f"(v) FHWT_STG_POL : "memory");
 }
 
 }  // namespace fhwt

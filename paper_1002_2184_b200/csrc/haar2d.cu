@@ -1365,6 +1365,75 @@ __global__ void __launch_bounds__(TCF, FHWT_MINB_SYN * 256 / TCF) syn2d_warp_ker
     syn2d_warp_tiles<LP, SHIFT, TCF, false, DYN>(p, maps, smem, bars, cnt, sc);
 }
 
+// K4 with a TMA producer warp (FHWT_SYN_PROD=1: static tile order, =2: global order from the tile
+// counter).  32 x 256 full tiles, LP = 5, no shifted boxes.  Warps 0-7 rebuild their 32-column
+// slices exactly as syn2d_warp_kernel<5> does (warp_syn_steps) and arrive on the stage's "empty"
+// mbarrier (count 8) after level 1; warp 8 lane 0 waits for "empty", picks the next tile, stores
+// its index next to the stage ("stile", read by the compute warps after their "full" wait) and
+// issues the 16 boxes: the issue is on no compute warp's path.  Bitwise identical output.
+template <bool DYN>
+__global__ void __launch_bounds__(288, 2) syn2d_prod_kernel(const __grid_constant__ Syn2dParams p,
+                                                           const __grid_constant__ TmaMaps2d maps) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* empty = full + p.stages;
+  unsigned* stile = reinterpret_cast<unsigned*>(empty + p.stages);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int j = 1; j <= 5; ++j) prefetch_tmap(&maps.level[j]);
+    prefetch_tmap(&maps.ll);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (p.head > 0) {   // cooperative launch: coarse levels -> fp32 LL5 hand-off, then a grid barrier
+    if (p.head == 1) syn_coarse<1>(p);
+    else if (p.head == 2) syn_coarse<2>(p);
+    else syn_coarse<3>(p);
+    fence_proxy_async_global();
+    cooperative_groups::this_grid().sync();
+    fence_proxy_async_global();
+  }
+  const uint32_t ntiles = uint32_t(p.ntiles);
+  if (warp == 8) {   // producer
+    if (lane == 0) {
+      for (int k = 0;; ++k) {
+        const int s = k % p.stages;
+        if (k >= p.stages) mbar_wait(&empty[s], uint32_t(k / p.stages - 1) & 1u);
+        uint32_t t;
+        if (DYN && k >= p.stages) t = atomicAdd(p.tile_ctr, 1u) + uint32_t(p.stages) * gridDim.x;
+        else t = blockIdx.x + uint32_t(k) * gridDim.x;
+        stile[s] = t;
+        if (t >= ntiles) {
+          mbar_arrive_plain(&full[s]);
+          break;
+        }
+        syn_issue_tile_lane<false, false, false>(p, maps, smem + s * p.stage_bytes, &full[s],
+                                                 DYN ? dyn_tile(t, ntiles, p.dyn_groups) : t, 0);
+      }
+    }
+    return;
+  }
+  WarpScratch* sc = reinterpret_cast<WarpScratch*>(smem + p.p_off[0] + warp * kSynScratchBytes);
+  for (int it = 0;; ++it) {
+    const int s = it % p.stages;
+    mbar_wait(&full[s], uint32_t(it / p.stages) & 1u);
+    const uint32_t cval = stile[s];
+    if (cval >= ntiles) break;
+    const uint32_t tile = DYN ? dyn_tile(cval, ntiles, p.dyn_groups) : cval;
+    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256, -1);
+    const unsigned char* stage = smem + s * p.stage_bytes;
+    const int64_t col0 = xy.col0;
+    const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> 5);
+    warp_syn_steps<5, 5, false, 256>(p, ll, 256 >> 5, stage, warp, sc, xy.b, xy.row0, col0 + 32 * warp, col0);
+    __syncwarp();
+    if (lane == 0) mbar_arrive_plain(&empty[s]);
+  }
+}
+
 template <int N>
 __device__ __forceinline__ void cp_async_wait_rt(int n) {  // runtime-N wrapper (n in [0, N])
   if constexpr (N > 0) {
@@ -1637,6 +1706,8 @@ static const void* syn2d_fn(int fast) {
   const bool narrow = ((fast >> 4) & 0xfff) == 128;
   if (mode == 3 && ((fast >> 4) & 0xfff) == 512) return (fast & 15) == 5 ? SynW512<5>::get() : nullptr;
   if (mode == 9) return (fast & 15) == 5 ? (const void*)syn2d_warp_kernel<5, false, 256, true> : nullptr;
+  if (mode == 10) return (fast & 15) == 5 ? (const void*)syn2d_prod_kernel<false> : nullptr;
+  if (mode == 11) return (fast & 15) == 5 ? (const void*)syn2d_prod_kernel<true> : nullptr;
   if (mode == 3) return narrow ? warp_fn<SynW128>(fast & 15) : warp_fn<SynW>(fast & 15);
   if (mode == 6) return narrow ? warp_fn<SynWS128>(fast & 15) : warp_fn<SynWS>(fast & 15);
   return mode == 2 ? by_geometry<SynF2>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15)
@@ -1652,6 +1723,7 @@ int ana2d_threads(int fast) {
 }
 int syn2d_threads(int fast) {
   const int mode = (fast >> 24) & 0xff;
+  if (mode == 10 || mode == 11) return 288;   // 8 compute warps + the producer warp
   return (mode == 3 || mode == 6 || mode == 9) ? ((fast >> 4) & 0xfff) : fast_threads_rt(fast);   // one warp per 32 columns
 }
 

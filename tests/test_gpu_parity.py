@@ -544,7 +544,8 @@ def test_long_signal_segments_bitwise_equal(world):
                                          ("FHWT_ANA_DYN", ["1", "0"]),
                                          ("FHWT_SYN_DYN", ["0", "1"]),
                                          ("FHWT_ANA_DYN_GROUPS", ["1", "4"]),
-                                         ("FHWT_SYN_DYN_GROUPS", ["1", "4"])])
+                                         ("FHWT_SYN_DYN_GROUPS", ["1", "4"]),
+                                         ("FHWT_SYN_PROD", ["0", "1", "2"])])
 @pytest.mark.parametrize("levels", [1, 3, 5, 7])
 def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
     """Every selectable 2-D kernel variant (analysis: level by level, fused level pairs, dedicated
