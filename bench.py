@@ -491,11 +491,11 @@ def run_checks(name, cfg, host, d, coeffs, rec, plan, shard, L, rank, ws, pg, de
     return out
 
 
-# Analysis-kernel variants compared under sustained load (profiles/r01_power_cap.md):
-# the default CTA-synchronous fused kernel is fastest at full clock, the dedicated-tail-warp kernel
-# (FHWT_ANA_FUSED=3, 3 stages) once the board sits at its power cap.
+# Tile-order variants compared under sustained load (profiles/r02_dynamic_tiles.md):
+# the default hands K1's and K4's tiles out in global order from a counter; "static_order" is the
+# round-1 persistent assignment (CTA i takes tiles i, i + grid, ...) with the round-1 K4.
 SUSTAINED_VARIANTS = {"default": {},
-                      "ana_fused3_st3": {"FHWT_TUNING": "1", "FHWT_ANA_FUSED": "3", "FHWT_ANA_STAGES": "3"}}
+                      "static_order": {"FHWT_TUNING": "1", "FHWT_ANA_DYN": "0", "FHWT_SYN_PROD": "0"}}
 
 
 def measure_sustained(step, stream, local, ms_per_step, seconds, bytes_per_step):

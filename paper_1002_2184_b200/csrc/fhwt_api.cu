@@ -814,10 +814,12 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       // producer-warp K4 (haar2d.cu syn2d_prod_kernel; FHWT_SYN_PROD=1 static order, =2 global order,
       // the default for full 32 x 256 LP = 5 tiles, with a 3-stage ring): c4 synthesis 6.35 -> 6.41 TB/s,
       // c5 6.28 -> 6.44 (profiles/r02_dynamic_tiles.md)
-      const int sprod = (mode == 3 && p.TR == 32 && p.TC == 256 && ps.Lp == 5 && full && ps.g0 == 0 && !p.clamp_rows)
+      const int sprod = (mode == 3 && p.TR == 32 && (p.TC == 256 || p.TC == 512) && ps.Lp == 5 && full && ps.g0 == 0 &&
+                         !p.clamp_rows)
                             ? env_int("FHWT_SYN_PROD", 2) : 0;
       if (sprod > 0) {
         mode = sprod == 2 ? 11 : 10;
+        p.issue_rev = env_int("FHWT_SYN_ISSUE_REV", 0);
         const int g = env_int("FHWT_SYN_DYN_GROUPS", 1);
         p.dyn_groups = (g > 1 && p.ntiles % g == 0) ? g : 1;
         p.tile_ctr = reinterpret_cast<unsigned*>(ws + pl->ctr_off + 128);
@@ -874,7 +876,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       // At most 2 resident CTAs/SM: the lighter LP < 5 variants fit 3-4, which measured 2.5-6.5 %
       // slower (tools/sweep_ctas.py, profiles/r01_sweep_ctas.jsonl); LP = 5 is indifferent.
       const int cap = env_int("FHWT_CTAS_PER_SM", syn_cap);   // sweep knob; 0 = the measured default
-      bps = std::min(bps, cap > 0 ? cap : (mode >= 10 ? 2 : 2 * kThreads2d / syn2d_threads(fast_lp)));
+      bps = std::min(bps, cap > 0 ? cap : (mode >= 10 ? 512 / p.TC : 2 * kThreads2d / syn2d_threads(fast_lp)));
       const int64_t grid = std::min<int64_t>(p.ntiles, int64_t(bps) * di.sms);
       if (coop) {
         if (mode != 3 && mode < 9)

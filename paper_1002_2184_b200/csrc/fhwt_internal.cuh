@@ -87,6 +87,7 @@ struct Syn2dParams {
   int row_boxes[6];        // per pass-level j: one-row boxes (1) or one (TR >> j)-row box (0); see Ana2dParams
   unsigned* tile_ctr;      // dynamic tile order (warp kernel, mode 9): next-tile counter, zeroed before the launch
   int dyn_groups;          // as Ana2dParams::dyn_groups
+  int issue_rev;           // producer K4: issue level-1 boxes first (experiment knob FHWT_SYN_ISSUE_REV)
   int l2mode;              // warp kernel's TMA loads: 0 L2::evict_first, 1 evict_normal, 2 evict_last, 3 no policy (default)
 };
 

@@ -1365,15 +1365,42 @@ __global__ void __launch_bounds__(TCF, FHWT_MINB_SYN * 256 / TCF) syn2d_warp_ker
     syn2d_warp_tiles<LP, SHIFT, TCF, false, DYN>(p, maps, smem, bars, cnt, sc);
 }
 
+// The producer's issue in the opposite order: level-1 bands first, the coarse boxes and LL last
+// (FHWT_SYN_ISSUE_REV=1; full unclamped 32-row tiles, no shifted boxes).
+__device__ __forceinline__ void syn_issue_tile_fine_first(const Syn2dParams& p, const TmaMaps2d& maps,
+                                                          unsigned char* base, uint64_t* bar, int64_t t) {
+  const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+  const int64_t b = rt / p.tiles_r;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = tile_col0(p, ct + p.ct0);
+  mbar_arrive_expect_tx(bar, p.tx_bytes);
+  const int L = p.Lp;
+  for (int j = 1; j <= L; ++j) {
+    const int64_t hg = p.H >> (p.g0 + j), wg = p.W >> (p.g0 + j);
+    const int64_t br = b * p.H + (row0 >> j), bc = col0 >> j;
+    const int rb = p.box_pitch[j] * 4;
+    const int nrows = p.row_boxes[j] ? (p.TR >> j) : 1;
+    for (int r = 0; r < nrows; ++r) {
+      tma_load_2d_nohint(base + p.box_off[j][0] + r * rb, &maps.level[j], int(wg + bc), int(br + r), bar);
+      tma_load_2d_nohint(base + p.box_off[j][1] + r * rb, &maps.level[j], int(bc), int(br + hg + r), bar);
+      tma_load_2d_nohint(base + p.box_off[j][2] + r * rb, &maps.level[j], int(wg + bc), int(br + hg + r), bar);
+    }
+  }
+  const int64_t llrow = p.ll_from_ws ? b * (p.Hin >> L) + (row0 >> L) : b * p.H + (row0 >> L);
+  const int llrows = p.row_boxes[L] ? (p.TR >> L) : 1;
+  for (int r = 0; r < llrows; ++r)
+    tma_load_2d_nohint(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int(col0 >> L), int(llrow + r), bar);
+}
+
 // K4 with a TMA producer warp (FHWT_SYN_PROD=1: static tile order, =2: global order from the tile
 // counter).  32 x 256 full tiles, LP = 5, no shifted boxes.  Warps 0-7 rebuild their 32-column
 // slices exactly as syn2d_warp_kernel<5> does (warp_syn_steps) and arrive on the stage's "empty"
 // mbarrier (count 8) after level 1; warp 8 lane 0 waits for "empty", picks the next tile, stores
 // its index next to the stage ("stile", read by the compute warps after their "full" wait) and
 // issues the 16 boxes: the issue is on no compute warp's path.  Bitwise identical output.
-template <bool DYN>
-__global__ void __launch_bounds__(288, 2) syn2d_prod_kernel(const __grid_constant__ Syn2dParams p,
-                                                           const __grid_constant__ TmaMaps2d maps) {
+template <bool DYN, int TCF = 256>
+__global__ void __launch_bounds__(TCF + 32, 512 / TCF) syn2d_prod_kernel(const __grid_constant__ Syn2dParams p,
+                                                                        const __grid_constant__ TmaMaps2d maps) {
+  constexpr int NW = TCF / 32;   // compute warps; warp NW is the producer
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
   uint64_t* empty = full + p.stages;
@@ -1384,7 +1411,7 @@ __global__ void __launch_bounds__(288, 2) syn2d_prod_kernel(const __grid_constan
     prefetch_tmap(&maps.ll);
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 8);
+      mbar_init(&empty[s], NW);
     }
     fence_mbar_init();
   }
@@ -1398,7 +1425,7 @@ __global__ void __launch_bounds__(288, 2) syn2d_prod_kernel(const __grid_constan
     fence_proxy_async_global();
   }
   const uint32_t ntiles = uint32_t(p.ntiles);
-  if (warp == 8) {   // producer
+  if (warp == NW) {   // producer
     if (lane == 0) {
       for (int k = 0;; ++k) {
         const int s = k % p.stages;
@@ -1411,8 +1438,11 @@ __global__ void __launch_bounds__(288, 2) syn2d_prod_kernel(const __grid_constan
           mbar_arrive_plain(&full[s]);
           break;
         }
-        syn_issue_tile_lane<false, false, false>(p, maps, smem + s * p.stage_bytes, &full[s],
-                                                 DYN ? dyn_tile(t, ntiles, p.dyn_groups) : t, 0);
+        if (p.issue_rev)
+          syn_issue_tile_fine_first(p, maps, smem + s * p.stage_bytes, &full[s], DYN ? dyn_tile(t, ntiles, p.dyn_groups) : t);
+        else
+          syn_issue_tile_lane<false, false, false>(p, maps, smem + s * p.stage_bytes, &full[s],
+                                                   DYN ? dyn_tile(t, ntiles, p.dyn_groups) : t, 0);
       }
     }
     return;
@@ -1424,11 +1454,11 @@ __global__ void __launch_bounds__(288, 2) syn2d_prod_kernel(const __grid_constan
     const uint32_t cval = stile[s];
     if (cval >= ntiles) break;
     const uint32_t tile = DYN ? dyn_tile(cval, ntiles, p.dyn_groups) : cval;
-    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, 256, -1);
+    const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, TCF, -1);
     const unsigned char* stage = smem + s * p.stage_bytes;
     const int64_t col0 = xy.col0;
     const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> 5);
-    warp_syn_steps<5, 5, false, 256>(p, ll, 256 >> 5, stage, warp, sc, xy.b, xy.row0, col0 + 32 * warp, col0);
+    warp_syn_steps<5, 5, false, TCF>(p, ll, TCF >> 5, stage, warp, sc, xy.b, xy.row0, col0 + 32 * warp, col0);
     __syncwarp();
     if (lane == 0) mbar_arrive_plain(&empty[s]);
   }
@@ -1706,8 +1736,12 @@ static const void* syn2d_fn(int fast) {
   const bool narrow = ((fast >> 4) & 0xfff) == 128;
   if (mode == 3 && ((fast >> 4) & 0xfff) == 512) return (fast & 15) == 5 ? SynW512<5>::get() : nullptr;
   if (mode == 9) return (fast & 15) == 5 ? (const void*)syn2d_warp_kernel<5, false, 256, true> : nullptr;
-  if (mode == 10) return (fast & 15) == 5 ? (const void*)syn2d_prod_kernel<false> : nullptr;
-  if (mode == 11) return (fast & 15) == 5 ? (const void*)syn2d_prod_kernel<true> : nullptr;
+  if (mode == 10 || mode == 11) {
+    if ((fast & 15) != 5) return nullptr;
+    if (((fast >> 4) & 0xfff) == 512)
+      return mode == 11 ? (const void*)syn2d_prod_kernel<true, 512> : (const void*)syn2d_prod_kernel<false, 512>;
+    return mode == 11 ? (const void*)syn2d_prod_kernel<true> : (const void*)syn2d_prod_kernel<false>;
+  }
   if (mode == 3) return narrow ? warp_fn<SynW128>(fast & 15) : warp_fn<SynW>(fast & 15);
   if (mode == 6) return narrow ? warp_fn<SynWS128>(fast & 15) : warp_fn<SynWS>(fast & 15);
   return mode == 2 ? by_geometry<SynF2>((fast >> 16) & 0xff, (fast >> 4) & 0xfff, fast & 15)
@@ -1723,7 +1757,7 @@ int ana2d_threads(int fast) {
 }
 int syn2d_threads(int fast) {
   const int mode = (fast >> 24) & 0xff;
-  if (mode == 10 || mode == 11) return 288;   // 8 compute warps + the producer warp
+  if (mode == 10 || mode == 11) return ((fast >> 4) & 0xfff) + 32;   // compute warps + the producer warp
   return (mode == 3 || mode == 6 || mode == 9) ? ((fast >> 4) & 0xfff) : fast_threads_rt(fast);   // one warp per 32 columns
 }
 

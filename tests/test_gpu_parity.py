@@ -545,7 +545,9 @@ def test_long_signal_segments_bitwise_equal(world):
                                          ("FHWT_SYN_DYN", ["0", "1"]),
                                          ("FHWT_ANA_DYN_GROUPS", ["1", "4"]),
                                          ("FHWT_SYN_DYN_GROUPS", ["1", "4"]),
-                                         ("FHWT_SYN_PROD", ["0", "1", "2"])])
+                                         ("FHWT_SYN_PROD", ["0", "1", "2"]),
+                                         ("FHWT_SYN_ISSUE_REV", ["0", "1"]),
+                                         ("FHWT_SYN_TC", ["256", "512"])])
 @pytest.mark.parametrize("levels", [1, 3, 5, 7])
 def test_kernel_variants_bitwise_equal(monkeypatch, knob, values, levels):
     """Every selectable 2-D kernel variant (analysis: level by level, fused level pairs, dedicated
