@@ -113,7 +113,8 @@ fhwt_status fhwt_plan_destroy(fhwt_plan p);
 size_t fhwt_plan_workspace_bytes(fhwt_plan p);
 
 /* Analysis (forward DWT): d [batch][...] -> coeffs (Mallat layout, same shape).
- * workspace: device buffer of fhwt_plan_workspace_bytes(p) bytes, or NULL (the library then
+ * workspace: 16-byte aligned device buffer of fhwt_plan_workspace_bytes(p) bytes (else
+ * FHWT_ERR_MISALIGNED), or NULL (the library then
  * allocates and frees it stream-ordered on s).  Asynchronous on s. */
 fhwt_status fhwt_plan_analyze(fhwt_plan p, const float *d, float *coeffs, void *workspace, fhwt_stream_t s);
 

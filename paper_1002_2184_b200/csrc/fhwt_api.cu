@@ -480,6 +480,11 @@ fhwt_status run_small1d(const fhwt_plan_s* pl, const float* in, float* out, cuda
 }
 
 // ------------------------------------------------------------------ 2-D execution
+// the workspace's tile-counter slot is usable (present and 16-B aligned: 32-bit atomics, memset)
+bool ctr_ok(const char* ws, const fhwt_plan_s* pl) {
+  return ws != nullptr && (reinterpret_cast<uintptr_t>(ws + pl->ctr_off) & 15) == 0;
+}
+
 fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char* ws, cudaStream_t s) {
   const int64_t H = pl->h, W = pl->w, B = pl->batch;
   if (W % 4 != 0 || !aligned16(d) || !aligned16(coeffs)) {
@@ -625,8 +630,9 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
                       p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows && p.row_boxes &&
                       env_int("FHWT_ANA_LEAN", 1) != 0;
     // dynamic tile order (tiles handed out in global order by an atomic counter in the workspace):
-    // c4 analysis 6.35 -> 6.66 TB/s, c5 6.28 -> 6.64 (profiles/r02_dynamic_tiles.md)
-    const bool dyn = lean && env_int("FHWT_ANA_DYN", 1) != 0;
+    // c4 analysis 6.35 -> 6.90 TB/s, c5 6.28 -> 6.72 (profiles/r02_dynamic_tiles.md).  A workspace
+    // whose counter slot is not 16-B aligned (a caller's offset pointer) keeps the static order.
+    const bool dyn = lean && ctr_ok(ws, pl) && env_int("FHWT_ANA_DYN", 1) != 0;
     if (dyn) {
       const int g = env_int("FHWT_ANA_DYN_GROUPS", 1);
       p.dyn_groups = (g > 1 && p.ntiles % g == 0) ? g : 1;
@@ -810,13 +816,14 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       if (shifted) mode = 6;
       // dynamic tile order for the 32 x 256, LP = 5 warp kernel (c4 / c5 tiles), as in the analysis
       const bool sdyn = mode == 3 && p.TR == 32 && p.TC == 256 && ps.Lp == 5 && full && ps.g0 == 0 &&
-                        env_int("FHWT_SYN_DYN", 0) != 0;
+                        ctr_ok(ws, pl) && env_int("FHWT_SYN_DYN", 0) != 0;
       // producer-warp K4 (haar2d.cu syn2d_prod_kernel; FHWT_SYN_PROD=1 static order, =2 global order,
       // the default for full 32 x 256 LP = 5 tiles, with a 3-stage ring): c4 synthesis 6.35 -> 6.41 TB/s,
       // c5 6.28 -> 6.44 (profiles/r02_dynamic_tiles.md)
-      const int sprod = (mode == 3 && p.TR == 32 && (p.TC == 256 || p.TC == 512) && ps.Lp == 5 && full && ps.g0 == 0 &&
-                         !p.clamp_rows)
-                            ? env_int("FHWT_SYN_PROD", 2) : 0;
+      int sprod = (mode == 3 && p.TR == 32 && (p.TC == 256 || p.TC == 512) && ps.Lp == 5 && full && ps.g0 == 0 &&
+                   !p.clamp_rows)
+                      ? env_int("FHWT_SYN_PROD", 2) : 0;
+      if (sprod == 2 && !ctr_ok(ws, pl)) sprod = 1;   // no usable counter slot: static order
       if (sprod > 0) {
         mode = sprod == 2 ? 11 : 10;
         p.issue_rev = env_int("FHWT_SYN_ISSUE_REV", 0);
@@ -1015,6 +1022,8 @@ fhwt_status run_on_device(fhwt_plan p, const float* in, float* out, void* worksp
   FHWT_TRY(check_ptrs(in, out, data_bytes(p)));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
   char* ws = static_cast<char*>(workspace);
+  if (ws && p->ws_bytes && (reinterpret_cast<uintptr_t>(ws) & 15) != 0)   // TMA maps and counters need it
+    return fail(FHWT_ERR_MISALIGNED, "workspace must be 16-byte aligned");
   bool owned = false;
   if (p->ws_bytes && !ws) {
     void* t = nullptr;

@@ -1155,14 +1155,23 @@ __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const 
   const int64_t row0 = CLAMPR ? tile_row0(p, rt - b * p.tiles_r) : (rt - b * p.tiles_r) * p.TR;
   const int64_t col0 = tile_col0(p, ct + p.ct0);
   constexpr int64_t AL = SHIFT ? ~int64_t(3) : ~int64_t(0);
+#ifdef FHWT_EXP_NOCOARSE   // timing experiment only (wrong output): level-1 boxes only
+  mbar_arrive_expect_tx(bar, 3u * uint32_t(p.TR >> 1) * uint32_t(p.box_pitch[1]) * 4u);
+#else
   mbar_arrive_expect_tx(bar, p.tx_bytes);
+#endif
   const int L = p.Lp;
   const int64_t llrow = p.ll_from_ws ? b * (p.Hin >> L) + (row0 >> L) : b * p.H + (row0 >> L);
   const int llrows = p.row_boxes[L] ? (p.TR >> L) : 1;
+#ifndef FHWT_EXP_NOCOARSE
   for (int r = 0; r < llrows; ++r)
     tma_load_2d_h<HINT>(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int((col0 >> L) & AL), int(llrow + r), bar,
                 pol);
+#endif
   for (int j = L; j >= 1; --j) {
+#ifdef FHWT_EXP_NOCOARSE
+    if (j > 1) continue;
+#endif
     const int g = p.g0 + j;
     const int64_t hg = p.H >> g, wg = p.W >> g;
     const int64_t br = b * p.H + (row0 >> j), bc = col0 >> j;
@@ -1198,10 +1207,22 @@ __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float
     if (NU % 32 != 0 && u >= NU) break;
     const int r = u / UPR, c = (u - r * UPR) * V;
     float vll[V], vhl[V], vlh[V], vhh[V];
+#if !defined(FHWT_EXP_NOCOMPUTE)
     load_row<float, V, !LLSHIFT>(ll + r * llp + c, vll);
-    load_row<float, V, !SHIFT>(hl + r * BP + c, vhl);
-    load_row<float, V, !SHIFT>(lh + r * BP + c, vlh);
-    load_row<float, V, !SHIFT>(hh + r * BP + c, vhh);
+#endif
+#if defined(FHWT_EXP_NOCOMPUTE)   // timing experiment only (wrong output): the memory pattern alone
+    if constexpr (J > 1) return;
+    for (int v = 0; v < V; ++v) vll[v] = vhl[v] = vlh[v] = vhh[v] = float(r);
+#else
+#ifdef FHWT_EXP_NOCONFLICT   // timing experiment only (wrong output): rows r, r+1 in different bank halves
+    const int xo = (J <= 2) ? (r & 1) * 16 : 0;
+#else
+    constexpr int xo = 0;
+#endif
+    load_row<float, V, !SHIFT>(hl + r * BP + c + xo, vhl);
+    load_row<float, V, !SHIFT>(lh + r * BP + c + xo, vlh);
+    load_row<float, V, !SHIFT>(hh + r * BP + c + xo, vhh);
+#endif
     float top[2 * V], bot[2 * V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {

@@ -894,3 +894,32 @@ def test_peer_memory_ll_gather_one_rank():
             g(fhwt.analyze_2d(xs[0][:512], 5), 5)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("levels", [5, 8])
+def test_tile_counter_workspace(levels):
+    """The global-order tile scheduling keeps its counters in the caller's workspace: a workspace
+    full of garbage (the library zeroes the counters before each launch) shared by analysis and
+    synthesis, and one at a 16-B offset inside a larger buffer, give the default result bitwise
+    (which matches the oracle); a workspace that is not 16-B aligned is rejected (Misaligned)."""
+    shape = (4, 512, 2048) if levels == 5 else (1, 2048, 4096)
+    x = datagen.uniform(shape, seed=levels + 101, lo=-1.0, hi=2.0)
+    xd = dev(x)
+    plan = fhwt.Plan2d(shape[1], shape[2], shape[0], levels)
+    nb = plan.workspace_bytes
+    assert nb >= 256
+    ref_c = plan.analyze(xd)
+    ref_r = plan.synthesize(ref_c)
+    garbage = torch.full((nb,), 0xAB, dtype=torch.uint8, device="cuda")
+    base = torch.full((nb + 64,), 0x5C, dtype=torch.uint8, device="cuda")
+    with pytest.raises(fhwt.Misaligned):
+        plan.analyze(xd, workspace=base[4:4 + nb])
+    for ws in (garbage, base[16:16 + nb]):
+        c = torch.full_like(xd, float("nan"))
+        r = torch.full_like(xd, float("nan"))
+        plan.analyze(xd, out=c, workspace=ws)
+        plan.synthesize(c, out=r, workspace=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(c, ref_c) and torch.equal(r, ref_r)
+    if levels == 5:
+        assert_close(host(ref_c), o.analyze_2d(x, levels), x, 2, what="counter workspace vs oracle")

@@ -31,7 +31,7 @@ plans = {L: fhwt.Plan2d(H, W, B, L) for L in (1, 5)}
 
 
 def case_membench(st):
-    return lambda: MB.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 296, st, 10, 256, 1, 0, 1)
+    return lambda: MB.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 296, st, 10, 256, 1, 0, 1, 0)
 
 
 def case_ana(L, st, hint):

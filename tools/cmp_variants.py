@@ -41,8 +41,10 @@ def membench(kind, x, y):
         bh = int(parts[1]) if len(parts) > 1 else 1
         st = int(parts[2]) if len(parts) > 2 else 3
         iss = int(parts[3]) if len(parts) > 3 else 1   # warps issuing the one-row boxes
-        return _MB.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 296, st, reps, 256, bh, 0,
-                               iss)
+        order = int(parts[4]) if len(parts) > 4 else 0   # 1: global tile order (atomic counter)
+        bw = int(parts[5]) if len(parts) > 5 else 256    # box width in floats
+        return _MB.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 296, st, reps, bw, bh, 0,
+                               iss, order)
     return _MB.mb_tile_ldg(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 592, reps)
 
 

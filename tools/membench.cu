@@ -64,7 +64,8 @@ __device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta
 
 __global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtensorMap map, float* __restrict__ y,
                                                   int64_t H, int64_t W, int64_t batch, int stages, int bw, int bh,
-                                                  const float* __restrict__ xsrc, int bulk, int issuers) {
+                                                  const float* __restrict__ xsrc, int bulk, int issuers,
+                                                  unsigned* ctr) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * 32768);
   const int64_t tiles_c = W / 256, tiles_r = H / 32, ntiles = batch * tiles_r * tiles_c;
@@ -109,11 +110,22 @@ __global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtens
             : "memory");
   };
   const bool issuer = (t & 31) == 0 && (t >> 5) < issuers;
-  if (issuer)
+  // ctr != nullptr: global tile order (the counter hands out tiles; the tile index of stage s sits in
+  // stile[s]; an index >= ntiles ends the loop)
+  unsigned* stile = reinterpret_cast<unsigned*>(bars + stages);
+  if (ctr) {
+    if (t == 0)
+      for (int s = 0; s < stages; ++s) {
+        const unsigned tt = blockIdx.x + unsigned(s) * gridDim.x;
+        stile[s] = tt;
+        if (tt < ntiles) issue(tt, s);
+        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&bars[s])) : "memory");
+      }
+  } else if (issuer)
     for (int s = 0; s < stages; ++s)
       if (blockIdx.x + int64_t(s) * gridDim.x < ntiles) issue(blockIdx.x + int64_t(s) * gridDim.x, s);
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  for (int64_t tile = blockIdx.x; ctr || tile < ntiles; tile += gridDim.x, ++it) {
     const int s = it % stages;
     const uint32_t par = (it / stages) & 1;
     asm volatile(
@@ -121,6 +133,10 @@ __global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtens
             su32(&bars[s])),
         "r"(par)
         : "memory");
+    if (ctr) {
+      tile = stile[s];
+      if (tile >= ntiles) break;
+    }
     const int64_t rt = tile / tiles_c, ct = tile - rt * tiles_c;
     const int64_t b = rt / tiles_r, row0 = (rt - b * tiles_r) * 32, col0 = ct * 256;
     const float* st = reinterpret_cast<const float*>(smem + s * 32768);
@@ -138,7 +154,16 @@ __global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtens
       stg2(pr + hw + wh, make_float2(a.y - c.y, a.w - c.w));
     }
     __syncthreads();
-    if (issuer && tile + int64_t(stages) * gridDim.x < ntiles) issue(tile + int64_t(stages) * gridDim.x, s);
+    if (ctr) {
+      if (t == 0) {
+        const unsigned nt = atomicAdd(ctr, 1u) + unsigned(stages) * gridDim.x;
+        stile[s] = nt;
+        if (nt < ntiles) issue(nt, s);
+        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&bars[s])) : "memory");
+      }
+    } else if (issuer && tile + int64_t(stages) * gridDim.x < ntiles) {
+      issue(tile + int64_t(stages) * gridDim.x, s);
+    }
   }
 }
 
@@ -179,7 +204,7 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 float mb_tile_tma(const float* x, float* y, int64_t H, int64_t W, int64_t batch, int blocks, int stages, int reps,
-                  int bw, int bh, int bulk, int issuers) {
+                  int bw, int bh, int bulk, int issuers, int order) {
   void* fp = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
@@ -192,18 +217,27 @@ float mb_tile_tma(const float* x, float* y, int64_t H, int64_t W, int64_t batch,
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -2.f;
-  const int smem = stages * 32768 + 64;
+  const int smem = stages * 32768 + 128;
+  unsigned* ctr = nullptr;
+  if (order) cudaMalloc(&ctr, 16);
   cudaFuncSetAttribute(k_tile_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int i = 0; i < 2; ++i) k_tile_tma<<<blocks, 256, smem>>>(map, y, H, W, batch, stages, bw, bh, x, bulk, issuers);
+  for (int i = 0; i < 2; ++i) {
+    if (ctr) cudaMemsetAsync(ctr, 0, 16);
+    k_tile_tma<<<blocks, 256, smem>>>(map, y, H, W, batch, stages, bw, bh, x, bulk, issuers, ctr);
+  }
   cudaEventRecord(a);
-  for (int i = 0; i < reps; ++i) k_tile_tma<<<blocks, 256, smem>>>(map, y, H, W, batch, stages, bw, bh, x, bulk, issuers);
+  for (int i = 0; i < reps; ++i) {
+    if (ctr) cudaMemsetAsync(ctr, 0, 16);
+    k_tile_tma<<<blocks, 256, smem>>>(map, y, H, W, batch, stages, bw, bh, x, bulk, issuers, ctr);
+  }
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
   cudaEventElapsedTime(&ms, a, b);
+  if (ctr) cudaFree(ctr);
   return cudaGetLastError() == cudaSuccess ? ms / reps : -1.f;
 }
 }

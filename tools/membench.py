@@ -32,6 +32,6 @@ for blocks, st, bw, bh, bulk in ((148 * 2, 3, 256, 32, 0), (148 * 2, 3, 256, 8, 
                                   (148 * 2, 3, 64, 32, 0), (148 * 2, 3, 256, 1, 0), (148 * 2, 3, 0, 0, 1),
                                   (148 * 3, 2, 256, 8, 0), (148 * 3, 2, 0, 0, 1), (148 * 4, 1, 256, 8, 0)):
     ms = L.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), ctypes.c_int64(H), ctypes.c_int64(W), ctypes.c_int64(B),
-                       blocks, st, 10, bw or 256, bh or 32, bulk, 1)
+                       blocks, st, 10, bw or 256, bh or 32, bulk, 1, 0)
     print(json.dumps({"pattern": "tile bulk-copy rows" if bulk else f"tile TMA box {bw}x{bh}", "blocks": blocks,
                       "stages": st, "gbs": gb(ms)}), flush=True)

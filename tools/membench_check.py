@@ -13,8 +13,8 @@ x = torch.rand(B, H, W, device="cuda")
 y0 = torch.zeros_like(x)
 vp, i64 = ctypes.c_void_p, ctypes.c_int64
 L.mb_tile_ldg(vp(x.data_ptr()), vp(y0.data_ptr()), i64(H), i64(W), i64(B), 592, 1)
-for bw, bh, bulk in ((256, 32, 0), (256, 1, 0, 1), (256, 8, 0), (0, 0, 1)):
+for bw, bh, bulk in ((256, 32, 0), (256, 1, 0, 1, 0), (256, 8, 0), (0, 0, 1)):
     y = torch.zeros_like(x)
-    ms = L.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 296, 3, 10, bw or 256, bh or 32, bulk, 1)
+    ms = L.mb_tile_tma(vp(x.data_ptr()), vp(y.data_ptr()), i64(H), i64(W), i64(B), 296, 3, 10, bw or 256, bh or 32, bulk, 1, 0)
     torch.cuda.synchronize()
     print(bw, bh, bulk, "equal:", torch.equal(y, y0), "GB/s", 8 * x.numel() / ms / 1e6)
