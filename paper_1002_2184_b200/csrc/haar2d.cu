@@ -1477,7 +1477,9 @@ __global__ void __launch_bounds__(TCF + 32, 512 / TCF) syn2d_prod_kernel(const _
     const uint32_t tile = DYN ? dyn_tile(cval, ntiles, p.dyn_groups) : cval;
     const TileXY xy = tile_xy(tile, p.tiles_c, p.tiles_r, 32, TCF, -1);
     const unsigned char* stage = smem + s * p.stage_bytes;
-    const int64_t col0 = xy.col0;
+    // column of the tile as the producer's boxes saw it (a ragged width runs its full tiles as a
+    // launch of its own, starting at column tile p.ct0, with the last one clamped)
+    const int64_t col0 = tile_col0(p, xy.col0 / TCF + p.ct0);
     const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> 5);
     warp_syn_steps<5, 5, false, TCF>(p, ll, TCF >> 5, stage, warp, sc, xy.b, xy.row0, col0 + 32 * warp, col0);
     __syncwarp();

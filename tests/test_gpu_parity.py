@@ -923,3 +923,49 @@ def test_tile_counter_workspace(levels):
         assert torch.equal(c, ref_c) and torch.equal(r, ref_r)
     if levels == 5:
         assert_close(host(ref_c), o.analyze_2d(x, levels), x, 2, what="counter workspace vs oracle")
+
+
+@pytest.mark.parametrize("count", [1, 2, 295, 296, 297, 593])
+def test_global_order_tile_counts(monkeypatch, count):
+    """The global-order K1 / K4 (tile counter, end marker, first `stages` tiles static) at tile
+    counts around the persistent grid (2 CTAs x 148 SMs = 296): `count` 32 x 256 images at L = 5
+    are `count` tiles.  Every output equals the oracle within the north_star bar and the
+    static-order kernels bitwise; NaN-filled outputs catch a skipped tile."""
+    x = datagen.uniform((count, 32, 256), seed=count + 7, lo=-1.0, hi=2.0)
+    xd = dev(x)
+    outs = []
+    for env in ({}, {"FHWT_ANA_DYN": "0", "FHWT_SYN_PROD": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        c = torch.full_like(xd, float("nan"))
+        r = torch.full_like(xd, float("nan"))
+        fhwt.analyze_2d(xd, 5, out=c)
+        fhwt.synthesize_2d(c, 5, out=r)
+        torch.cuda.synchronize()
+        outs.append((c, r))
+        for k in env:
+            monkeypatch.delenv(k)
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    assert_close(host(outs[0][0]), o.analyze_2d(x, 5), x, 2, what=f"{count} tiles")
+    assert_close(host(outs[0][1]), x, x, 2, what=f"{count} tiles round trip")
+
+
+@pytest.mark.parametrize("levels,shape", [(6, (37, 256, 512)), (7, (5, 256, 512)), (8, (3, 256, 512)),
+                                          (6, (3, 320, 1664)), (7, (2, 384, 1920)), (5, (2, 96, 1152))])
+def test_global_order_coarse_levels(monkeypatch, levels, shape):
+    """L = 6..8 (the cooperative launches: tiles in global order, then a grid barrier and the
+    coarse levels) against the oracle and the static-order kernels; widths with w % 256 = 128 run
+    their full 256-column tiles as a launch of its own starting at a column-tile offset, with the
+    last tile clamped (tools/stress_parity.py found the producer K4 ignoring that offset)."""
+    x = datagen.uniform(shape, seed=levels * 10 + shape[0], lo=-1.0, hi=2.0)
+    xd = dev(x)
+    c = fhwt.analyze_2d(xd, levels)
+    r = fhwt.synthesize_2d(c, levels)
+    monkeypatch.setenv("FHWT_ANA_DYN", "0")
+    monkeypatch.setenv("FHWT_SYN_PROD", "0")
+    c0 = fhwt.analyze_2d(xd, levels)
+    r0 = fhwt.synthesize_2d(c0, levels)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c0) and torch.equal(r, r0)
+    assert_close(host(c), o.analyze_2d(x, levels), x, 2, what=f"L={levels}")
+    assert_close(host(r), x, x, 2, what=f"L={levels} round trip")

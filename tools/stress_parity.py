@@ -17,7 +17,9 @@ KNOBS = [{}, {"FHWT_ANA_FUSED": "0"}, {"FHWT_ANA_FUSED": "3"}, {"FHWT_SYN_MODE":
          {"FHWT_COOP": "0"}, {"FHWT_CLAMP_LAST": "0"}, {"FHWT_SMALL_IMAGES": "0"}, {"FHWT_SMALL_SIGNALS": "0"},
          {"FHWT_CLAMP_ROWS": "0"}, {"FHWT_TC256_CLAMP": "0"}, {"FHWT_SYN_SHIFT": "0"}, {"FHWT_1D_TAIL": "0"},
          {"FHWT_ANA_TILE_TABLE": "0", "FHWT_SYN_TILE_TABLE": "0"}, {"FHWT_ANA_FUSED": "6"}, {"FHWT_ANA_FUSED": "1"},
-         {"FHWT_SYN_WARP128": "1"}, {"FHWT_SYN_WARP128": "0"}]
+         {"FHWT_SYN_WARP128": "1"}, {"FHWT_SYN_WARP128": "0"},
+         {"FHWT_ANA_DYN": "0", "FHWT_SYN_PROD": "0"}, {"FHWT_SYN_PROD": "1"}, {"FHWT_ANA_LEAN": "0"},
+         {"FHWT_SYN_DYN": "1", "FHWT_SYN_PROD": "0"}]
 
 
 def main():
