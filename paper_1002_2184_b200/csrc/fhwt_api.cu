@@ -825,7 +825,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
                       ? env_int("FHWT_SYN_PROD", 2) : 0;
       if (sprod == 2 && !ctr_ok(ws, pl)) sprod = 1;   // no usable counter slot: static order
       if (sprod > 0) {
-        mode = sprod == 2 ? 11 : 10;
+        mode = (sprod == 2 ? 11 : 10) + ((p.ct0 != 0 || p.clamp_last) ? 2 : 0);
         p.issue_rev = env_int("FHWT_SYN_ISSUE_REV", 0);
         const int g = env_int("FHWT_SYN_DYN_GROUPS", 1);
         p.dyn_groups = (g > 1 && p.ntiles % g == 0) ? g : 1;
@@ -859,7 +859,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       // 2 stages for 32 x 256 tiles; the cp.async variant's narrower tiles from a measured table
       int syn_stages = syn_ring_stages(p.stage_bytes), syn_cap = 0;
       if (env_int("FHWT_SYN_TILE_TABLE", 1) != 0) syn_tile_cfg(mode, p.TR, p.TC, &syn_stages, &syn_cap);
-      p.stages = env_int("FHWT_SYN_STAGES", mode == 11 ? 3 : syn_stages);
+      p.stages = env_int("FHWT_SYN_STAGES", (mode == 11 || mode == 13) ? 3 : syn_stages);
       size_t pb[2] = {0, 0};
       for (int j = 2; j <= ps.Lp; ++j) {
         const int jj = j - 1;
@@ -894,7 +894,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       if (env_int("FHWT_DEBUG_LAUNCH", 0))
         std::fprintf(stderr, "[fhwt] syn2d mode %d tile %dx%d LP %d stages %d smem %zu B ctas/SM %d grid %lld\n", mode,
                      p.TR, p.TC, ps.Lp, p.stages, smem, bps, (long long)grid);
-      if (mode == 9 || mode == 11) FHWT_CUDA(cudaMemsetAsync(p.tile_ctr, 0, 16, s), "tile counter reset");
+      if (mode == 9 || mode == 11 || mode == 13) FHWT_CUDA(cudaMemsetAsync(p.tile_ctr, 0, 16, s), "tile counter reset");
       FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
     }
   }

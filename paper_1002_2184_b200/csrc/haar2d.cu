@@ -1418,7 +1418,9 @@ __device__ __forceinline__ void syn_issue_tile_fine_first(const Syn2dParams& p, 
 // mbarrier (count 8) after level 1; warp 8 lane 0 waits for "empty", picks the next tile, stores
 // its index next to the stage ("stile", read by the compute warps after their "full" wait) and
 // issues the 16 boxes: the issue is on no compute warp's path.  Bitwise identical output.
-template <bool DYN, int TCF = 256>
+// RAGGED: the launch covers the full tiles of a ragged width (column-tile offset p.ct0, last tile
+// clamped); otherwise tiles start at column ct * TCF (c4, c5).
+template <bool DYN, int TCF = 256, bool RAGGED = false>
 __global__ void __launch_bounds__(TCF + 32, 512 / TCF) syn2d_prod_kernel(const __grid_constant__ Syn2dParams p,
                                                                         const __grid_constant__ TmaMaps2d maps) {
   constexpr int NW = TCF / 32;   // compute warps; warp NW is the producer
@@ -1479,7 +1481,7 @@ __global__ void __launch_bounds__(TCF + 32, 512 / TCF) syn2d_prod_kernel(const _
     const unsigned char* stage = smem + s * p.stage_bytes;
     // column of the tile as the producer's boxes saw it (a ragged width runs its full tiles as a
     // launch of its own, starting at column tile p.ct0, with the last one clamped)
-    const int64_t col0 = tile_col0(p, xy.col0 / TCF + p.ct0);
+    const int64_t col0 = RAGGED ? tile_col0(p, xy.col0 / TCF + p.ct0) : xy.col0;
     const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> 5);
     warp_syn_steps<5, 5, false, TCF>(p, ll, TCF >> 5, stage, warp, sc, xy.b, xy.row0, col0 + 32 * warp, col0);
     __syncwarp();
@@ -1759,11 +1761,13 @@ static const void* syn2d_fn(int fast) {
   const bool narrow = ((fast >> 4) & 0xfff) == 128;
   if (mode == 3 && ((fast >> 4) & 0xfff) == 512) return (fast & 15) == 5 ? SynW512<5>::get() : nullptr;
   if (mode == 9) return (fast & 15) == 5 ? (const void*)syn2d_warp_kernel<5, false, 256, true> : nullptr;
-  if (mode == 10 || mode == 11) {
+  if (mode >= 10 && mode <= 13) {   // producer K4: 10 / 11 static / global order, 12 / 13 the same, ragged
     if ((fast & 15) != 5) return nullptr;
     if (((fast >> 4) & 0xfff) == 512)
-      return mode == 11 ? (const void*)syn2d_prod_kernel<true, 512> : (const void*)syn2d_prod_kernel<false, 512>;
-    return mode == 11 ? (const void*)syn2d_prod_kernel<true> : (const void*)syn2d_prod_kernel<false>;
+      return mode == 11 ? (const void*)syn2d_prod_kernel<true, 512> : mode == 10 ? (const void*)syn2d_prod_kernel<false, 512>
+             : mode == 13 ? (const void*)syn2d_prod_kernel<true, 512, true> : (const void*)syn2d_prod_kernel<false, 512, true>;
+    return mode == 11 ? (const void*)syn2d_prod_kernel<true> : mode == 10 ? (const void*)syn2d_prod_kernel<false>
+           : mode == 13 ? (const void*)syn2d_prod_kernel<true, 256, true> : (const void*)syn2d_prod_kernel<false, 256, true>;
   }
   if (mode == 3) return narrow ? warp_fn<SynW128>(fast & 15) : warp_fn<SynW>(fast & 15);
   if (mode == 6) return narrow ? warp_fn<SynWS128>(fast & 15) : warp_fn<SynWS>(fast & 15);
@@ -1780,7 +1784,7 @@ int ana2d_threads(int fast) {
 }
 int syn2d_threads(int fast) {
   const int mode = (fast >> 24) & 0xff;
-  if (mode == 10 || mode == 11) return ((fast >> 4) & 0xfff) + 32;   // compute warps + the producer warp
+  if (mode >= 10 && mode <= 13) return ((fast >> 4) & 0xfff) + 32;   // compute warps + the producer warp
   return (mode == 3 || mode == 6 || mode == 9) ? ((fast >> 4) & 0xfff) : fast_threads_rt(fast);   // one warp per 32 columns
 }
 
