@@ -43,8 +43,8 @@ WORKLOADS = {
 
 
 KERNEL_NAMES = {
-    ("2d", "analysis"): "fhwt::ana2d_kernel (all passes of fhwt_plan_analyze)",
-    ("2d", "synthesis"): "fhwt::syn2d_kernel (all passes of fhwt_plan_synthesize)",
+    ("2d", "analysis"): "fhwt_plan_analyze (K1 ana2d_lean_kernel<true> + the coarse levels in the same launch)",
+    ("2d", "synthesis"): "fhwt_plan_synthesize (K4 syn2d_prod_kernel<true> + the coarse levels in the same launch)",
     ("1d", "analysis"): "fhwt::ana1d_kernel",
     ("1d", "synthesis"): "fhwt::syn1d_kernel",
 }
