@@ -138,7 +138,8 @@ __device__ __forceinline__ void store_ll_smem(TC* dst, const TC (&ll)[V]) {
 // level g to HBM and LL_g to smem (lldst, pitch C/2) or, on the pass's last level, to HBM (coeffs
 // LL region or the fp64 workspace).
 // RC, CC: compile-time R, C (0 = runtime).  FAST: full, 8-B aligned tile (no masks, no checks).
-template <typename TS, typename TC, int V, int RC, int CC, bool FAST, int NT = kThreads2d>
+// UNR: unroll the unit loop; the lean K1 keeps it rolled (measured +0.9 % c4, +0.4 % c5 analysis)
+template <typename TS, typename TC, int V, int RC, int CC, bool FAST, int NT = kThreads2d, bool UNR = true>
 __device__ __forceinline__ void ana_level(const Ana2dParams& p, const TS* __restrict__ src, int R_, int C_, int j,
                                           int64_t b, int64_t row0, int64_t col0, TC* __restrict__ lldst,
                                           bool last) {
@@ -155,10 +156,9 @@ __device__ __forceinline__ void ana_level(const Ana2dParams& p, const TS* __rest
   const int64_t nvalid_row = FAST ? int64_t(OC) : (p.Win >> j) - bcol;
   const TC half = TC(0.5);
   const int iters = (nunits + NT - 1) / NT;
-#pragma unroll
-  for (int it = 0; it < iters; ++it) {
+  auto unit = [&](int it) -> bool {
     const int u = int(threadIdx.x) + it * NT;
-    if ((nunits % NT) != 0 && u >= nunits) break;
+    if ((nunits % NT) != 0 && u >= nunits) return false;
     const int orow = u / upr;
     const int oc = (u - orow * upr) * V;
     TS t0[2 * V], t1[2 * V];
@@ -195,6 +195,16 @@ __device__ __forceinline__ void ana_level(const Ana2dParams& p, const TS* __rest
       for (int v = 0; v < V; ++v)
         if (v < nv) w[v] = double(ll[v]);
     }
+    return true;
+  };
+  if constexpr (UNR) {
+#pragma unroll
+    for (int it = 0; it < iters; ++it)
+      if (!unit(it)) break;
+  } else {
+#pragma unroll 1
+    for (int it = 0; it < iters; ++it)
+      if (!unit(it)) break;
   }
 }
 
@@ -773,7 +783,7 @@ __device__ __forceinline__ void ana_lean_tile(const Ana2dParams& p, const float*
                                               int64_t b, int64_t row0, int64_t col0, const LeanRefill& refill) {
   float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]);   // 16 x 128
   float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);   // 4 x 32
-  ana_level<float, float, 2, 32, 256, true>(p, stage, 32, 256, 1, b, row0, col0, ll1, false);
+  ana_level<float, float, 2, 32, 256, true, kThreads2d, false>(p, stage, 32, 256, 1, b, row0, col0, ll1, false);
   __syncthreads();   // LL1 complete; the stage has been read for the last time
   refill();
   const int tid = threadIdx.x;
@@ -846,7 +856,7 @@ __global__ void __launch_bounds__(256, FHWT_MINB_ANA) ana2d_lean_kernel(const __
       float* ll1 = reinterpret_cast<float*>(smem + p.p_off[1]);
       float* ll3 = reinterpret_cast<float*>(smem + p.p_off[0]);
       const int64_t row0 = (rt - b * p.tiles_r) * 32, col0 = ct * 256;
-      ana_level<float, float, 2, 32, 256, true>(p, stage, 32, 256, 1, b, row0, col0, ll1, false);
+      ana_level<float, float, 2, 32, 256, true, kThreads2d, false>(p, stage, 32, 256, 1, b, row0, col0, ll1, false);
       __syncthreads();   // LL1 complete; the stage (and stile[s]) has been read for the last time
       if (tid < 32) {   // refill with the next tile in global order
         if (tid == 0) stile[s] = nt;
@@ -1185,7 +1195,9 @@ __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const 
   }
 }
 
-template <int J, bool SHIFT, bool LLSHIFT, int TCF>
+// UNR: unroll the unit loop (syn2d_warp_kernel); the producer K4 keeps it rolled, measured +1 % on
+// c4 / c5 synthesis (profiles/r02_dynamic_tiles.md)
+template <int J, bool SHIFT, bool LLSHIFT, int TCF, bool UNR = true>
 __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float* __restrict__ ll, int llp,
                                                const unsigned char* stage, int warp, float* __restrict__ dst,
                                                int64_t b, int64_t row0, int64_t colw, int64_t col0) {
@@ -1201,7 +1213,8 @@ __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float
   const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]) + coh;
   const int lane = threadIdx.x & 31;
   float* const obase = p.out + (b * p.Hin + row0) * p.out_pitch + colw;
-#pragma unroll
+  constexpr int UNROLL = UNR ? (NU + 31) / 32 : 1;
+#pragma unroll UNROLL
   for (int it = 0; it < (NU + 31) / 32; ++it) {
     const int u = lane + 32 * it;
     if (NU % 32 != 0 && u >= NU) break;
@@ -1250,15 +1263,15 @@ __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float
   }
 }
 
-template <int J, int LP, bool SHIFT, int TCF>
+template <int J, int LP, bool SHIFT, int TCF, bool UNR = true>
 __device__ __forceinline__ void warp_syn_steps(const Syn2dParams& p, const float* ll, int llp,
                                                const unsigned char* stage, int warp, WarpScratch* sc, int64_t b,
                                                int64_t row0, int64_t colw, int64_t col0) {
   float* dst = J == 5 ? reinterpret_cast<float*>(sc->ll4) : J == 4 ? sc->ll3 : J == 3 ? sc->ll2 : sc->ll1;
-  warp_syn_level<J, SHIFT, SHIFT && J == LP, TCF>(p, ll, llp, stage, warp, dst, b, row0, colw, col0);
+  warp_syn_level<J, SHIFT, SHIFT && J == LP, TCF, UNR>(p, ll, llp, stage, warp, dst, b, row0, colw, col0);
   if constexpr (J > 1) {
     __syncwarp();
-    warp_syn_steps<J - 1, LP, SHIFT, TCF>(p, dst, 2 * (32 >> J), stage, warp, sc, b, row0, colw, col0);
+    warp_syn_steps<J - 1, LP, SHIFT, TCF, UNR>(p, dst, 2 * (32 >> J), stage, warp, sc, b, row0, colw, col0);
   }
 }
 
@@ -1421,7 +1434,10 @@ __device__ __forceinline__ void syn_issue_tile_fine_first(const Syn2dParams& p, 
 // RAGGED: the launch covers the full tiles of a ragged width (column-tile offset p.ct0, last tile
 // clamped); otherwise tiles start at column ct * TCF (c4, c5).
 template <bool DYN, int TCF = 256, bool RAGGED = false>
-__global__ void __launch_bounds__(TCF + 32, 512 / TCF) syn2d_prod_kernel(const __grid_constant__ Syn2dParams p,
+#ifndef FHWT_PROD_MINB
+#define FHWT_PROD_MINB 2   // resident CTAs the producer K4's registers are capped for (TCF = 256)
+#endif
+__global__ void __launch_bounds__(TCF + 32, TCF == 256 ? FHWT_PROD_MINB : 1) syn2d_prod_kernel(const __grid_constant__ Syn2dParams p,
                                                                         const __grid_constant__ TmaMaps2d maps) {
   constexpr int NW = TCF / 32;   // compute warps; warp NW is the producer
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -1483,7 +1499,7 @@ __global__ void __launch_bounds__(TCF + 32, 512 / TCF) syn2d_prod_kernel(const _
     // launch of its own, starting at column tile p.ct0, with the last one clamped)
     const int64_t col0 = RAGGED ? tile_col0(p, xy.col0 / TCF + p.ct0) : xy.col0;
     const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> 5);
-    warp_syn_steps<5, 5, false, TCF>(p, ll, TCF >> 5, stage, warp, sc, xy.b, xy.row0, col0 + 32 * warp, col0);
+    warp_syn_steps<5, 5, false, TCF, false>(p, ll, TCF >> 5, stage, warp, sc, xy.b, xy.row0, col0 + 32 * warp, col0);
     __syncwarp();
     if (lane == 0) mbar_arrive_plain(&empty[s]);
   }
