@@ -536,7 +536,8 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     // LP = 3, 4 level by level.  Mode 6 (LP = 3: levels 2+3 by all 256 threads, two lanes per 4 x 4
     // LL1 block) won on two boxes (+1-3.5 %) and lost on two (-7 %, 2048^2 images): kept as an option.
     p.fused = env_int("FHWT_ANA_FUSED", ps.Lp == 5 ? 1 : 0);
-    p.row_boxes = size_t(p.TC) * (in64 ? 8 : 4) >= 1024 && (size_t(p.TC) * (in64 ? 8 : 4)) % 128 == 0;
+    p.row_boxes = size_t(p.TC) * (in64 ? 8 : 4) >= 1024 && (size_t(p.TC) * (in64 ? 8 : 4)) % 128 == 0 &&
+                  env_int("FHWT_ANA_ROWBOXES", 1) != 0;
     FHWT_TRY(encode_2d(&map, in, in64, p.Win, B * p.Hin, in_pitch, p.TC, p.row_boxes ? 1 : p.TR));
     // shared memory layout: stages | P[0] | P[1] | barriers
     const size_t es = in64 ? 8 : 4;
@@ -627,7 +628,7 @@ fhwt_status run_ana2d(const fhwt_plan_s* pl, const float* d, float* coeffs, char
     // the lean K1 (haar2d.cu ana2d_lean_kernel): full, unclamped, aligned 32 x 256 tiles at LP = 5 —
     // every c4 / c5 tile — with the default fused chain
     const bool lean = fast_ok && p.fused == 1 && ps.Lp == 5 && p.TR == 32 && p.TC == 256 && p.mask_mode == 0 &&
-                      p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows && p.row_boxes &&
+                      p.aligned_levels >= ps.Lp && !p.clamp_last && !p.clamp_rows &&
                       env_int("FHWT_ANA_LEAN", 1) != 0;
     // dynamic tile order (tiles handed out in global order by an atomic counter in the workspace):
     // c4 analysis 6.35 -> 6.90 TB/s, c5 6.28 -> 6.72 (profiles/r02_dynamic_tiles.md).  A workspace
