@@ -133,6 +133,25 @@ fhwt_status encode_2d(CUtensorMap* m, const void* base, bool f64, int64_t cols, 
   return FHWT_OK;
 }
 
+// The level-j coefficient array as a 3-D view {32 floats, W / 32 lines of 128 B, rows} with
+// SWIZZLE_128B, box {32, nch, bh}: one (bh)-row band box of nch * 128 B per row, landed with each
+// 128-B line's 16-B granules permuted (haar2d.cu syn_issue_tile_swz / warp_syn_level<SWZ>).
+fhwt_status encode_3d_swz(CUtensorMap* m, const void* base, int64_t W, int64_t rows, int nch, int bh) {
+  auto fn = get_encode();
+  if (!fn) return fail(FHWT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[3] = {32, cuuint64_t(W / 32), cuuint64_t(rows)};
+  cuuint64_t strides[2] = {128, cuuint64_t(W) * 4};
+  cuuint32_t box[3] = {32, cuuint32_t(nch), cuuint32_t(bh)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(FHWT_ERR_CUDA, "cuTensorMapEncodeTiled (swizzled) failed (%d): W %lld rows %lld box %d x %d", int(r),
+                (long long)W, (long long)rows, nch, bh);
+  return FHWT_OK;
+}
+
 // Tuning knobs (defaults chosen by measurement).  The env overrides exist
 // only for the sweeps in tools/ and the A/B tests: every FHWT_* variable is ignored unless
 // FHWT_TUNING=1 is set too, so a stray variable in a user's environment cannot change which
@@ -825,8 +844,20 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
                    !p.clamp_rows)
                       ? env_int("FHWT_SYN_PROD", 2) : 0;
       if (sprod == 2 && !ctr_ok(ws, pl)) sprod = 1;   // no usable counter slot: static order
+      p.swz = 0;
       if (sprod > 0) {
         mode = (sprod == 2 ? 11 : 10) + ((p.ct0 != 0 || p.clamp_last) ? 2 : 0);
+        // level-1/2 boxes through 128-B-swizzled 3-D maps (no 2-way bank conflicts on the band reads;
+        // c4 synthesis 6.45 -> 6.93 TB/s, profiles/r02_swizzle.md): global order, 256-column unclamped
+        // tiles, every level-1/2 band block a whole number of 128-B lines (W % 128 == 0), one
+        // (TR >> j)-row box per band.  (Level 3 swizzled too measured 0.5 % slower.)
+        if (mode == 11 && p.TC == 256 && W % 128 == 0 && !p.row_boxes[1] && !p.row_boxes[2] && bw[1] == 128 &&
+            bw[2] == 64 && env_int("FHWT_SYN_SWZ", 1) != 0) {
+          p.swz = 2;
+          mode = 14;
+          for (int j = 1; j <= p.swz; ++j)
+            FHWT_TRY(encode_3d_swz(&maps.sw[j], coeffs, W, B * H, bw[j] / 32, p.TR >> j));
+        }
         p.issue_rev = env_int("FHWT_SYN_ISSUE_REV", 0);
         const int g = env_int("FHWT_SYN_DYN_GROUPS", 1);
         p.dyn_groups = (g > 1 && p.ntiles % g == 0) ? g : 1;
@@ -841,13 +872,23 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       // with cp.async a 16-B packing would admit a 3rd CTA/SM, which measured slower: 5.54 vs 6.10 TB/s)
       const size_t balign = 128;
       size_t off = 0, tx = 0;
+      if (p.swz) {   // the swizzled boxes first, each 1024-B aligned (the 128-B swizzle atom is 8 lines)
+        for (int j = 1; j <= p.swz; ++j) {
+          const size_t bytes = size_t(p.TR >> j) * bw[j] * 4;
+          for (int q = 0; q < 3; ++q) {
+            p.box_off[j][q] = uint32_t(off);
+            off = align_up(off + bytes, 1024);
+            tx += bytes;
+          }
+        }
+      }
       {
         const size_t bytes = size_t(p.TR >> ps.Lp) * bw[ps.Lp] * 4;
         p.box_off[0][0] = uint32_t(off);
         off = align_up(off + bytes, balign);
         tx += bytes;
       }
-      for (int j = 1; j <= ps.Lp; ++j) {
+      for (int j = p.swz + 1; j <= ps.Lp; ++j) {
         const size_t bytes = size_t(p.TR >> j) * bw[j] * 4;
         for (int q = 0; q < 3; ++q) {
           p.box_off[j][q] = uint32_t(off);
@@ -860,7 +901,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       // 2 stages for 32 x 256 tiles; the cp.async variant's narrower tiles from a measured table
       int syn_stages = syn_ring_stages(p.stage_bytes), syn_cap = 0;
       if (env_int("FHWT_SYN_TILE_TABLE", 1) != 0) syn_tile_cfg(mode, p.TR, p.TC, &syn_stages, &syn_cap);
-      p.stages = env_int("FHWT_SYN_STAGES", (mode == 11 || mode == 13) ? 3 : syn_stages);
+      p.stages = env_int("FHWT_SYN_STAGES", (mode == 11 || mode == 13 || mode == 14) ? 3 : syn_stages);
       size_t pb[2] = {0, 0};
       for (int j = 2; j <= ps.Lp; ++j) {
         const int jj = j - 1;
@@ -895,7 +936,7 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       if (env_int("FHWT_DEBUG_LAUNCH", 0))
         std::fprintf(stderr, "[fhwt] syn2d mode %d tile %dx%d LP %d stages %d smem %zu B ctas/SM %d grid %lld\n", mode,
                      p.TR, p.TC, ps.Lp, p.stages, smem, bps, (long long)grid);
-      if (mode == 9 || mode == 11 || mode == 13) FHWT_CUDA(cudaMemsetAsync(p.tile_ctr, 0, 16, s), "tile counter reset");
+      if (mode == 9 || mode == 11 || mode == 13 || mode == 14) FHWT_CUDA(cudaMemsetAsync(p.tile_ctr, 0, 16, s), "tile counter reset");
       FHWT_CUDA(launch_syn2d(p, maps, fast_lp, int(grid), smem, s), "syn2d launch");
     }
   }

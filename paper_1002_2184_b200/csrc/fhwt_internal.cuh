@@ -89,11 +89,14 @@ struct Syn2dParams {
   int dyn_groups;          // as Ana2dParams::dyn_groups
   int issue_rev;           // producer K4: issue level-1 boxes first (experiment knob FHWT_SYN_ISSUE_REV)
   int l2mode;              // warp kernel's TMA loads: 0 L2::evict_first, 1 evict_normal, 2 evict_last, 3 no policy (default)
+  int swz;                 // producer K4: levels 1..swz (2) boxes through the 128-B-swizzled 3-D maps (TmaMaps2d::sw)
 };
 
 struct TmaMaps2d {
   CUtensorMap level[6];  // coeff view box for pass-level j = 1..Lp ([0] unused)
   CUtensorMap ll;        // LL_{g0+Lp} source box
+  CUtensorMap sw[3];     // [1], [2]: level-1/2 coefficient view as {32 floats, W/32 lines, rows} with
+                         // SWIZZLE_128B (producer K4, Syn2dParams::swz); [0] unused
 };
 
 // ------------------------------------------------------------------ small 2-D images
@@ -243,6 +246,16 @@ __device__ __forceinline__ void tma_load_2d_nohint(void* smem_dst, const CUtenso
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMA 3-D tile load (the swizzled level-1/2 synthesis boxes: {32 floats, lines, rows}).
+__device__ __forceinline__ void tma_load_3d_nohint(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                   uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
 

@@ -1197,20 +1197,24 @@ __device__ __forceinline__ void syn_issue_tile_lane(const Syn2dParams& p, const 
 
 // UNR: unroll the unit loop (syn2d_warp_kernel); the producer K4 keeps it rolled, measured +1 % on
 // c4 / c5 synthesis (profiles/r02_dynamic_tiles.md)
-template <int J, bool SHIFT, bool LLSHIFT, int TCF, bool UNR = true>
+// SWZ: the level's three band boxes were landed by the 128-B-swizzled 3-D maps (syn_issue_tile_swz):
+// box row r is NCH = BP / 32 lines of 128 B, and the 16-B granule g of line l sits at g ^ (l & 7), so
+// rows r and r + 1 (J = 1) or r .. r + 3 (J = 2) of a warp's column slice fall in different banks.
+template <int J, bool SHIFT, bool LLSHIFT, int TCF, bool UNR = true, bool SWZ = false>
 __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float* __restrict__ ll, int llp,
                                                const unsigned char* stage, int warp, float* __restrict__ dst,
                                                int64_t b, int64_t row0, int64_t colw, int64_t col0) {
   constexpr int R = 32 >> J, C = 32 >> J, BP = (TCF >> J) + (SHIFT ? 4 : 0);
+  static_assert(!SWZ || (!SHIFT && BP % 32 == 0), "swizzled boxes: whole 128-B lines, no shift");
   constexpr int V = C >= 2 ? 2 : 1, UPR = C / V, NU = R * UPR, OC = 2 * C;
   int co = (32 * warp) >> J, coh = co;
   if constexpr (SHIFT) {   // see syn_issue_tile_lane<true>
     co += int((col0 >> J) & 3);
     coh += int(((p.W >> (p.g0 + J)) + (col0 >> J)) & 3);
   }
-  const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]) + coh;
-  const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]) + co;
-  const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]) + coh;
+  const float* hl = reinterpret_cast<const float*>(stage + p.box_off[J][0]) + (SWZ ? 0 : coh);
+  const float* lh = reinterpret_cast<const float*>(stage + p.box_off[J][1]) + (SWZ ? 0 : co);
+  const float* hh = reinterpret_cast<const float*>(stage + p.box_off[J][2]) + (SWZ ? 0 : coh);
   const int lane = threadIdx.x & 31;
   float* const obase = p.out + (b * p.Hin + row0) * p.out_pitch + colw;
   constexpr int UNROLL = UNR ? (NU + 31) / 32 : 1;
@@ -1232,9 +1236,18 @@ __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float
 #else
     constexpr int xo = 0;
 #endif
-    load_row<float, V, !SHIFT>(hl + r * BP + c + xo, vhl);
-    load_row<float, V, !SHIFT>(lh + r * BP + c + xo, vlh);
-    load_row<float, V, !SHIFT>(hh + r * BP + c + xo, vhh);
+    if constexpr (SWZ) {
+      constexpr int NCH = BP / 32;
+      const int cc = co + c, line = r * NCH + (cc >> 5);
+      const int o = line * 32 + ((((cc >> 2) & 7) ^ (line & 7)) << 2) + (cc & 3);
+      load_row<float, V, true>(hl + o, vhl);
+      load_row<float, V, true>(lh + o, vlh);
+      load_row<float, V, true>(hh + o, vhh);
+    } else {
+      load_row<float, V, !SHIFT>(hl + r * BP + c + xo, vhl);
+      load_row<float, V, !SHIFT>(lh + r * BP + c + xo, vlh);
+      load_row<float, V, !SHIFT>(hh + r * BP + c + xo, vhh);
+    }
 #endif
     float top[2 * V], bot[2 * V];
 #pragma unroll
@@ -1263,15 +1276,16 @@ __device__ __forceinline__ void warp_syn_level(const Syn2dParams& p, const float
   }
 }
 
-template <int J, int LP, bool SHIFT, int TCF, bool UNR = true>
+// SWZL: levels 1..SWZL read swizzled boxes
+template <int J, int LP, bool SHIFT, int TCF, bool UNR = true, int SWZL = 0>
 __device__ __forceinline__ void warp_syn_steps(const Syn2dParams& p, const float* ll, int llp,
                                                const unsigned char* stage, int warp, WarpScratch* sc, int64_t b,
                                                int64_t row0, int64_t colw, int64_t col0) {
   float* dst = J == 5 ? reinterpret_cast<float*>(sc->ll4) : J == 4 ? sc->ll3 : J == 3 ? sc->ll2 : sc->ll1;
-  warp_syn_level<J, SHIFT, SHIFT && J == LP, TCF, UNR>(p, ll, llp, stage, warp, dst, b, row0, colw, col0);
+  warp_syn_level<J, SHIFT, SHIFT && J == LP, TCF, UNR, (J <= SWZL)>(p, ll, llp, stage, warp, dst, b, row0, colw, col0);
   if constexpr (J > 1) {
     __syncwarp();
-    warp_syn_steps<J - 1, LP, SHIFT, TCF, UNR>(p, dst, 2 * (32 >> J), stage, warp, sc, b, row0, colw, col0);
+    warp_syn_steps<J - 1, LP, SHIFT, TCF, UNR, SWZL>(p, dst, 2 * (32 >> J), stage, warp, sc, b, row0, colw, col0);
   }
 }
 
@@ -1425,6 +1439,42 @@ __device__ __forceinline__ void syn_issue_tile_fine_first(const Syn2dParams& p, 
     tma_load_2d_nohint(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int(col0 >> L), int(llrow + r), bar);
 }
 
+// The producer's issue with the level-1/2/3 band boxes through the swizzled 3-D maps (p.swz; full
+// unclamped 32 x 256 tiles, no row boxes at levels 1-3): the same bytes land in the same boxes, each
+// 128-B line's 16-B granules permuted by SWIZZLE_128B (read back by warp_syn_level<SWZ>).
+template <int SWZL>
+__device__ __forceinline__ void syn_issue_tile_swz(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* base,
+                                                   uint64_t* bar, int64_t t) {
+  const int64_t rt = t / p.tiles_c, ct = t - rt * p.tiles_c;
+  const int64_t b = rt / p.tiles_r;
+  const int64_t row0 = (rt - b * p.tiles_r) * p.TR, col0 = tile_col0(p, ct + p.ct0);
+  mbar_arrive_expect_tx(bar, p.tx_bytes);
+  const int L = p.Lp;
+  const int64_t llrow = p.ll_from_ws ? b * (p.Hin >> L) + (row0 >> L) : b * p.H + (row0 >> L);
+  const int llrows = p.row_boxes[L] ? (p.TR >> L) : 1;
+  for (int r = 0; r < llrows; ++r)
+    tma_load_2d_nohint(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int(col0 >> L), int(llrow + r), bar);
+  for (int j = L; j > SWZL; --j) {
+    const int64_t hg = p.H >> j, wg = p.W >> j;
+    const int64_t br = b * p.H + (row0 >> j), bc = col0 >> j;
+    const int rb = p.box_pitch[j] * 4;
+    const int nrows = p.row_boxes[j] ? (p.TR >> j) : 1;
+    for (int r = 0; r < nrows; ++r) {
+      tma_load_2d_nohint(base + p.box_off[j][0] + r * rb, &maps.level[j], int(wg + bc), int(br + r), bar);
+      tma_load_2d_nohint(base + p.box_off[j][1] + r * rb, &maps.level[j], int(bc), int(br + hg + r), bar);
+      tma_load_2d_nohint(base + p.box_off[j][2] + r * rb, &maps.level[j], int(wg + bc), int(br + hg + r), bar);
+    }
+  }
+#pragma unroll
+  for (int j = SWZL; j >= 1; --j) {
+    const int64_t hg = p.H >> j, wg = p.W >> j;
+    const int64_t br = b * p.H + (row0 >> j), bc = col0 >> j;
+    tma_load_3d_nohint(base + p.box_off[j][0], &maps.sw[j], 0, int((wg + bc) >> 5), int(br), bar);
+    tma_load_3d_nohint(base + p.box_off[j][1], &maps.sw[j], 0, int(bc >> 5), int(br + hg), bar);
+    tma_load_3d_nohint(base + p.box_off[j][2], &maps.sw[j], 0, int((wg + bc) >> 5), int(br + hg), bar);
+  }
+}
+
 // K4 with a TMA producer warp (FHWT_SYN_PROD=1: static tile order, =2: global order from the tile
 // counter).  32 x 256 full tiles, LP = 5, no shifted boxes.  Warps 0-7 rebuild their 32-column
 // slices exactly as syn2d_warp_kernel<5> does (warp_syn_steps) and arrive on the stage's "empty"
@@ -1433,7 +1483,8 @@ __device__ __forceinline__ void syn_issue_tile_fine_first(const Syn2dParams& p, 
 // issues the 16 boxes: the issue is on no compute warp's path.  Bitwise identical output.
 // RAGGED: the launch covers the full tiles of a ragged width (column-tile offset p.ct0, last tile
 // clamped); otherwise tiles start at column ct * TCF (c4, c5).
-template <bool DYN, int TCF = 256, bool RAGGED = false>
+// SWZL > 0: level-1..SWZL boxes through the swizzled maps (syn_issue_tile_swz, warp_syn_level<SWZ>).
+template <bool DYN, int TCF = 256, bool RAGGED = false, int SWZL = 0>
 #ifndef FHWT_PROD_MINB
 #define FHWT_PROD_MINB 2   // resident CTAs the producer K4's registers are capped for (TCF = 256)
 #endif
@@ -1446,7 +1497,8 @@ __global__ void __launch_bounds__(TCF + 32, TCF == 256 ? FHWT_PROD_MINB : 1) syn
   unsigned* stile = reinterpret_cast<unsigned*>(empty + p.stages);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int j = 1; j <= 5; ++j) prefetch_tmap(&maps.level[j]);
+    for (int j = SWZL + 1; j <= 5; ++j) prefetch_tmap(&maps.level[j]);
+    for (int j = 1; j <= SWZL; ++j) prefetch_tmap(&maps.sw[j]);
     prefetch_tmap(&maps.ll);
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -1477,7 +1529,9 @@ __global__ void __launch_bounds__(TCF + 32, TCF == 256 ? FHWT_PROD_MINB : 1) syn
           mbar_arrive_plain(&full[s]);
           break;
         }
-        if (p.issue_rev)
+        if constexpr (SWZL > 0)
+          syn_issue_tile_swz<SWZL>(p, maps, smem + s * p.stage_bytes, &full[s], DYN ? dyn_tile(t, ntiles, p.dyn_groups) : t);
+        else if (p.issue_rev)
           syn_issue_tile_fine_first(p, maps, smem + s * p.stage_bytes, &full[s], DYN ? dyn_tile(t, ntiles, p.dyn_groups) : t);
         else
           syn_issue_tile_lane<false, false, false>(p, maps, smem + s * p.stage_bytes, &full[s],
@@ -1499,7 +1553,7 @@ __global__ void __launch_bounds__(TCF + 32, TCF == 256 ? FHWT_PROD_MINB : 1) syn
     // launch of its own, starting at column tile p.ct0, with the last one clamped)
     const int64_t col0 = RAGGED ? tile_col0(p, xy.col0 / TCF + p.ct0) : xy.col0;
     const float* ll = reinterpret_cast<const float*>(stage + p.box_off[0][0]) + ((32 * warp) >> 5);
-    warp_syn_steps<5, 5, false, TCF, false>(p, ll, TCF >> 5, stage, warp, sc, xy.b, xy.row0, col0 + 32 * warp, col0);
+    warp_syn_steps<5, 5, false, TCF, false, SWZL>(p, ll, TCF >> 5, stage, warp, sc, xy.b, xy.row0, col0 + 32 * warp, col0);
     __syncwarp();
     if (lane == 0) mbar_arrive_plain(&empty[s]);
   }
@@ -1777,6 +1831,8 @@ static const void* syn2d_fn(int fast) {
   const bool narrow = ((fast >> 4) & 0xfff) == 128;
   if (mode == 3 && ((fast >> 4) & 0xfff) == 512) return (fast & 15) == 5 ? SynW512<5>::get() : nullptr;
   if (mode == 9) return (fast & 15) == 5 ? (const void*)syn2d_warp_kernel<5, false, 256, true> : nullptr;
+  if (mode == 14)   // producer K4, global order, level-1/2 boxes swizzled
+    return (fast & 15) == 5 && ((fast >> 4) & 0xfff) == 256 ? (const void*)syn2d_prod_kernel<true, 256, false, 2> : nullptr;
   if (mode >= 10 && mode <= 13) {   // producer K4: 10 / 11 static / global order, 12 / 13 the same, ragged
     if ((fast & 15) != 5) return nullptr;
     if (((fast >> 4) & 0xfff) == 512)
@@ -1800,7 +1856,7 @@ int ana2d_threads(int fast) {
 }
 int syn2d_threads(int fast) {
   const int mode = (fast >> 24) & 0xff;
-  if (mode >= 10 && mode <= 13) return ((fast >> 4) & 0xfff) + 32;   // compute warps + the producer warp
+  if (mode >= 10 && mode <= 14) return ((fast >> 4) & 0xfff) + 32;   // compute warps + the producer warp
   return (mode == 3 || mode == 6 || mode == 9) ? ((fast >> 4) & 0xfff) : fast_threads_rt(fast);   // one warp per 32 columns
 }
 

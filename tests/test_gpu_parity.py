@@ -617,6 +617,37 @@ def test_warp_private_synthesis_bitwise(monkeypatch, capfd, shape, levels, stage
     assert_close(host(r), host(x), host(x), 2, what="wp7 round trip")
 
 
+@pytest.mark.parametrize("shape,levels", [((4, 512, 2048), 5), ((4, 512, 2048), 7), ((1, 2048, 4096), 8),
+                                          ((300, 32, 256), 5), ((8, 128, 4096), 5), ((1, 256, 32768), 8)])
+@pytest.mark.parametrize("stages", ["2", "3"])
+def test_swizzled_synthesis_boxes_bitwise(monkeypatch, capfd, shape, levels, stages):
+    """The producer K4's default on W % 128 == 0 (mode 14): the level-1/2 band boxes land through
+    128-B-swizzled 3-D tensor maps and are read back through the same permutation.  Same bytes,
+    same arithmetic: the reconstruction equals the unswizzled producer K4 (FHWT_SYN_SWZ=0) bitwise,
+    with and without the cooperative coarse levels (a ragged width with W % 128 == 0 always runs
+    the clamped K4, mode 13, unswizzled); oracle round trip; the debug lines prove which kernel ran."""
+    x = dev(datagen.uniform(shape, seed=levels + 53, lo=-1.0, hi=2.0))
+    c = fhwt.analyze_2d(x, levels)
+    monkeypatch.setenv("FHWT_SYN_STAGES", stages)
+    monkeypatch.setenv("FHWT_DEBUG_LAUNCH", "1")
+    capfd.readouterr()
+    r = torch.full_like(x, float("nan"))
+    fhwt.synthesize_2d(c, levels, out=r)
+    torch.cuda.synchronize()
+    err = capfd.readouterr().err
+    monkeypatch.setenv("FHWT_SYN_SWZ", "0")
+    r0 = torch.full_like(x, float("nan"))
+    fhwt.synthesize_2d(c, levels, out=r0)
+    torch.cuda.synchronize()
+    err0 = capfd.readouterr().err
+    assert "syn2d mode 14 " in err and "syn2d mode 14 " not in err0, (err, err0)
+    assert torch.equal(r, r0)
+    assert_close(host(r), host(x), host(x), 2, what="swizzled K4 round trip")
+    if levels <= 6:
+        assert_close(host(r), o.synthesize_2d(o.analyze_2d(host(x), levels), levels), host(x), 2,
+                     what="swizzled K4 vs oracle synthesis")
+
+
 @pytest.mark.parametrize("batch,n,levels", [(16, 2048, 11), (8, 4096, 12), (8, 4096, 11), (4, 8192, 13),
                                              (4, 8192, 12), (6, 4096, 12), (3, 4096, 12), (1, 8192, 13)])
 def test_1d_coarse_levels_inside_the_cta(monkeypatch, batch, n, levels):

@@ -6,6 +6,7 @@ reads `dram_bytes_per_launch` as the roofline's `traffic`.
 python tools/ncu_traffic.py out.json c4=raw_c4.csv [c2=raw_c2.csv c5=raw_c5.csv]"""
 import csv
 import json
+import os
 import sys
 
 SAMPLES = {"c4": 256 * 2048 * 2048, "c2": 4096 * 65536, "c5": 32768 * 32768}
@@ -27,6 +28,10 @@ def main(out, *specs):
                       "store sectors/request = l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum / "
                       "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum (4 = full 128-B lines per request), "
                       "smem bank conflicts = l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_{ld,st}.sum"}
+    if os.path.exists(out):   # merge: a capture per kernel file updates only that workload / kind
+        old = json.load(open(out))
+        old.update({k: v for k, v in res.items() if k == "_source"})
+        res = old
     for spec in specs:
         wl, path = spec.split("=")
         rows = list(csv.reader(open(path)))
@@ -70,7 +75,7 @@ def main(out, *specs):
                     "registers_per_thread": val(r, "launch__registers_per_thread"),
                     "issue_active_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
                 }
-        res[wl] = best
+        res.setdefault(wl, {}).update(best)
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
