@@ -82,10 +82,11 @@ def ncu_traffic(workload, kernel):
 
 
 class ClockSampler:
-    """SM clock, board power and clock-event (throttle) reasons sampled through NVML every ~2 ms by
-    a background thread while the timed region runs (the c4 region is ~55 ms: nvidia-smi's 200 ms
-    polling saw 3 mostly idle samples in round 1).  Falls back to nvidia-smi if NVML is missing."""
-    PERIOD_S = 0.002
+    """SM clock, board power and clock-event (throttle) reasons sampled through NVML every ~0.5 ms
+    (plus the ~0.7 ms the four NVML queries take) by a background thread while the timed region runs
+    (the c4 region is ~50 ms at --steps 20: nvidia-smi's 200 ms polling saw 3 mostly idle samples in
+    round 1, a 2 ms period 18).  Falls back to nvidia-smi if NVML is missing."""
+    PERIOD_S = 0.0005
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap"}
 
@@ -143,7 +144,7 @@ class ClockSampler:
                 "reasons": sorted(v for k, v in self.REASONS.items() if reasons & k),
                 "power_w_max": max(s[1] for s in loaded), "samples": len(self.samples),
                 "samples_under_load": sum(1 for s in self.samples if s[3] > 0),
-                "sampler": f"NVML every {self.PERIOD_S * 1e3:.0f} ms during the timed region"}
+                "sampler": f"NVML every {self.PERIOD_S * 1e3:.1f} ms + query time during the timed region"}
 
 
 # ---------------------------------------------------------------------------------- data
