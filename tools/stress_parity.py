@@ -19,7 +19,7 @@ KNOBS = [{}, {"FHWT_ANA_FUSED": "0"}, {"FHWT_ANA_FUSED": "3"}, {"FHWT_SYN_MODE":
          {"FHWT_ANA_TILE_TABLE": "0", "FHWT_SYN_TILE_TABLE": "0"}, {"FHWT_ANA_FUSED": "6"}, {"FHWT_ANA_FUSED": "1"},
          {"FHWT_SYN_WARP128": "1"}, {"FHWT_SYN_WARP128": "0"},
          {"FHWT_ANA_DYN": "0", "FHWT_SYN_PROD": "0"}, {"FHWT_SYN_PROD": "1"}, {"FHWT_ANA_LEAN": "0"},
-         {"FHWT_SYN_DYN": "1", "FHWT_SYN_PROD": "0"}]
+         {"FHWT_SYN_DYN": "1", "FHWT_SYN_PROD": "0"}, {"FHWT_SYN_SWZ": "0"}]
 
 
 def main():
@@ -40,6 +40,12 @@ def main():
                 h = max(blk, h // 2 // blk * blk)
             w = w if w % 4 == 0 or L == 1 else w
             b = int(rng.integers(1, 4))
+            if rng.random() < 0.3:   # the c4 / c5 kernels' tiles (32 x 256, LP = 5, swizzled K4 boxes)
+                L = int(rng.integers(5, 9))
+                h = 32 * int(rng.integers(1, 24)) * (1 << max(0, L - 5))
+                w = 256 * int(rng.integers(1, 9)) if rng.random() < 0.7 else max(128, 1 << L) * int(rng.integers(2, 17))
+                while h * w > 1 << 20:
+                    h = max(1 << L, h // 2 // (1 << L) * (1 << L))
             x = (rng.standard_normal((b, h, w)) * rng.choice([1e-3, 1.0, 1e3])).astype(np.float32)
             xd = torch.from_numpy(x).cuda()
             c = fhwt.analyze_2d(xd, L)
@@ -73,8 +79,7 @@ def main():
             torch.cuda.synchronize()
             ref = o.decompose_1d(x, J)
             scale = np.abs(x).max(axis=1, keepdims=True)
-            tol = max(1e-5, 4 * 2.0 ** (J / 2 - 24))
-            e1 = float((np.abs(c.double().cpu().numpy() - ref) / scale).max()) * 1e-5 / tol
+            e1 = float((np.abs(c.double().cpu().numpy() - ref) / scale).max())   # fp64 levels 1-3 for J > 10
             e2 = float((np.abs(r.double().cpu().numpy() - x) / scale).max())
             det = bool(torch.equal(c, c2))
             case = ("1d", b, nn, J, knob)
