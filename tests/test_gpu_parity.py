@@ -648,6 +648,27 @@ def test_swizzled_synthesis_boxes_bitwise(monkeypatch, capfd, shape, levels, sta
                      what="swizzled K4 vs oracle synthesis")
 
 
+@pytest.mark.parametrize("offset", [4, 8, 20])
+def test_swizzled_synthesis_offset_buffers(offset):
+    """The swizzled K4's 3-D tensor maps are defined relative to the coefficient base: a base that
+    is only 16-B aligned (a view at `offset` floats into a larger buffer), and an output view at
+    the same offset, give the same reconstruction bitwise as 128-B aligned buffers."""
+    x = dev(datagen.uniform((4, 256, 2048), seed=offset, lo=-1.0, hi=1.0))
+    c = fhwt.analyze_2d(x, 5)
+    ref = fhwt.synthesize_2d(c, 5)
+    big = torch.full((c.numel() + offset,), float("nan"), device=c.device)
+    cv = big[offset:].view_as(c)
+    cv.copy_(c)
+    outb = torch.full((c.numel() + offset,), float("nan"), device=c.device)
+    rv = outb[offset:].view_as(c)
+    fhwt.synthesize_2d(cv, 5, out=rv)
+    cv2 = torch.full_like(c, float("nan"))
+    fhwt.analyze_2d(x, 5, out=cv2)
+    torch.cuda.synchronize()
+    assert torch.equal(rv, ref)
+    assert torch.isnan(outb[:offset]).all()
+
+
 @pytest.mark.parametrize("batch,n,levels", [(16, 2048, 11), (8, 4096, 12), (8, 4096, 11), (4, 8192, 13),
                                              (4, 8192, 12), (6, 4096, 12), (3, 4096, 12), (1, 8192, 13)])
 def test_1d_coarse_levels_inside_the_cta(monkeypatch, batch, n, levels):
