@@ -208,7 +208,7 @@ def measure(name, cfg, args, ws, rank, local, pg, timed=True):
         plan = fhwt.Plan1d(d.shape[-1], d.numel() // d.shape[-1], L, device=local)
     wsb = torch.empty(max(plan.workspace_bytes, 1), dtype=torch.uint8, device=dev)
     rowband = cfg["shard"] == "rowband"
-    gather = rowband and ws > 1
+    gather = rowband and (ws > 1 or getattr(args, "force_gather", False))
     p2p = None
     if rowband:
         ll_rows, ll_cols = d.shape[0] >> L, d.shape[1] >> L
@@ -864,6 +864,9 @@ def main():
     ap.add_argument("--weak", action="store_true",
                     help="c2 / c4: every rank transforms a full batch (weak scaling) instead of batch/N units")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA graph replays")
+    ap.add_argument("--force-gather", action="store_true",
+                    help="check of the N > 1 code path on one GPU: c5's LL all-gather through a one-rank NCCL "
+                         "group, captured in the CUDA graph like at N > 1")
     ap.add_argument("--no-t1", action="store_true",
                     help="N > 1: skip rank 0's single-GPU run of the whole workload (the T(1) of the self-check)")
     args = ap.parse_args()
@@ -886,7 +889,7 @@ def main():
         else:
             dist.init_process_group(args.dist_backend)
         pg = dist.group.WORLD
-    elif args.ll_gather == "p2p":   # one GPU: a one-rank group exercises the peer-store path on itself
+    elif args.ll_gather == "p2p" or args.force_gather:   # one GPU: a one-rank group exercises the gather path
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
