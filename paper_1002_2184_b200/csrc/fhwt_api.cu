@@ -847,9 +847,10 @@ fhwt_status run_syn2d(const fhwt_plan_s* pl, const float* coeffs, float* dR, cha
       p.swz = 0;
       if (sprod > 0) {
         mode = (sprod == 2 ? 11 : 10) + ((p.ct0 != 0 || p.clamp_last) ? 2 : 0);
-        // level-1/2 boxes through 128-B-swizzled 3-D maps (no 2-way bank conflicts on the band reads;
-        // c4 synthesis 6.45 -> 6.93 TB/s, profiles/r02_swizzle.md): global order, 256-column unclamped
-        // tiles, every level-1/2 band block a whole number of 128-B lines (W % 128 == 0), one
+        // level-1/2 boxes through 128-B-swizzled 3-D maps {32 floats, lines, rows} (c4 synthesis
+        // 6.45 -> 6.93 TB/s: the 128-B innermost box dimension, 7.4 %; the swizzle, which removes the
+        // band reads' bank conflicts, 0.15 %; profiles/r02_swizzle.md): global order, 256-column
+        // unclamped tiles, every level-1/2 band block a whole number of 128-B lines (W % 128 == 0), one
         // (TR >> j)-row box per band.  (Level 3 swizzled too measured 0.5 % slower.)
         if (mode == 11 && p.TC == 256 && W % 128 == 0 && !p.row_boxes[1] && !p.row_boxes[2] && bw[1] == 128 &&
             bw[2] == 64 && env_int("FHWT_SYN_SWZ", 1) != 0) {

@@ -1439,9 +1439,11 @@ __device__ __forceinline__ void syn_issue_tile_fine_first(const Syn2dParams& p, 
     tma_load_2d_nohint(base + p.box_off[0][0] + r * p.box_pitch[L] * 4, &maps.ll, int(col0 >> L), int(llrow + r), bar);
 }
 
-// The producer's issue with the level-1/2/3 band boxes through the swizzled 3-D maps (p.swz; full
-// unclamped 32 x 256 tiles, no row boxes at levels 1-3): the same bytes land in the same boxes, each
-// 128-B line's 16-B granules permuted by SWIZZLE_128B (read back by warp_syn_level<SWZ>).
+// The producer's issue with the level-1..SWZL (1-2) band boxes through the swizzled 3-D maps (p.swz;
+// full unclamped 32 x 256 tiles, one box per band at those levels): the same bytes land in the same
+// boxes, each 128-B line's 16-B granules permuted by SWIZZLE_128B (read back by warp_syn_level<SWZ>).
+// A box whose innermost dimension is one 128-B line streams far faster than the 2-D box with 512-B
+// rows (c4 synthesis 6.45 -> 6.92 TB/s unswizzled, 6.93 swizzled; profiles/r02_swizzle.md).
 template <int SWZL>
 __device__ __forceinline__ void syn_issue_tile_swz(const Syn2dParams& p, const TmaMaps2d& maps, unsigned char* base,
                                                    uint64_t* bar, int64_t t) {
